@@ -1,0 +1,389 @@
+"""Benchmark: nbnxn search + force on synthetic SPC water (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--atoms 96000] [--elec ewald|rf|cutoff] [--nstlist 10]
+
+One STEP = one MD step of the non-bonded hot path: every `nstlist` steps the
+grid, the cluster-pair search and the prune are redone from scratch at the
+current positions, and every step runs the force + energy pass.  Positions
+are static (the reference's SPC water has no exclusions/constraints, so its
+MD diverges -- SURVEY.md 0.3); nothing is cached across rebuilds.
+
+value   = useful pair interactions (admitted slot pairs with r <= r_c) per
+          second, whole job, inputs resident in HBM, per-step CUDA events,
+          L2 flushed (256 MiB write) between steps outside the timed events.
+e2e     = the same metric with host (pinned) positions/charges/types copied
+          H2D and forces + energies copied D2H inside every timed step.
+roofline= the force kernel (k_force) against the FP32 pipe peak
+          (148 SMs x 128 lanes x 2 flop x sm_max_mhz from MEASURED_PEAKS.json),
+          flops = admitted slot pairs x per-pair cost (kernels.FLOPS_PER_PAIR
+          = 40, +12 for Ewald).
+cpu_baseline = the reference algorithm's CPU port (oracle/, FP64, all host
+          threads) on the same system: one rebuild + one force pass.
+--impl reference: that CPU port timed for W + K steps (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+DT_PS = 0.002
+R_CUT, R_LIST, M = 1.0, 1.1, 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--atoms", type=int, default=96000)
+    ap.add_argument("--elec", default="ewald", choices=["ewald", "rf", "cutoff"])
+    ap.add_argument("--nstlist", type=int, default=10)
+    ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_1506_00716_b200.systems import spc_water, tuned_occupancy
+
+    system, table = spc_water(args.atoms, seed=2024)
+    L = float(system.box.lengths[0])
+    occ = tuned_occupancy(args.atoms, L, M) if args.occupancy == "tuned" else None
+    return system, table, occ
+
+
+def make_params(args, table):
+    import paper_1506_00716_b200 as nbx
+
+    if args.elec == "ewald":
+        return nbx.NonbondedParams(r_cut=R_CUT, r_list=R_LIST, lj_table=table, shift_potential=True,
+                                   elec="ewald", ewald_beta=nbx.ewald_beta(R_CUT, 1e-5))
+    if args.elec == "rf":
+        return nbx.NonbondedParams(r_cut=R_CUT, r_list=R_LIST, lj_table=table, shift_potential=True,
+                                   elec="reaction_field", epsilon_rf=0.0)
+    return nbx.NonbondedParams(r_cut=R_CUT, r_list=R_LIST, lj_table=table, shift_potential=True)
+
+
+def config(args, occ, extra=None):
+    c = {"workload": f"SPC water {args.atoms // 1000}k atoms, LJ+{ {'ewald': 'Ewald real-space (erfc, beta: erfc(beta rc)=1e-5)', 'rf': 'reaction-field (eps_rf=inf)', 'cutoff': 'shifted cutoff Coulomb (= RF eps_rf=1, reference physics)'}[args.elec]}",
+         "n_atoms": args.atoms, "r_cut_nm": R_CUT, "r_list_nm": R_LIST, "cluster_size": M,
+         "nstlist": args.nstlist, "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
+         "positions": "static (search+prune from scratch every nstlist steps, forces every step, energies every nstlist steps)",
+         "l2": "flushed between steps by a 256 MiB write outside the timed events",
+         "parallelism": f"{'replicas' if args.gpus > 1 else 'single'} x{args.gpus}"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, idx):
+        self.proc = None
+        self.path = REPO / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(idx), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU port
+def cpu_port_times(system, params_phys, occ, nstlist, reps=1):
+    """Reference algorithm (oracle/, FP64): numpy grid, O(n_c^2) AABB search
+    (pairlist.py:185-189), prune, and the blocked force kernel (kernels.py:124-221)
+    on all host threads."""
+    from oracle import native, search
+
+    L = system.box.lengths
+    threads = native.default_threads()
+    t0 = time.perf_counter()
+    og = search.build_grid(system.positions, L, M, occ)
+    t1 = time.perf_counter()
+    ol = native.search_list(og, L, R_LIST, method="n2", threads=threads)
+    t2 = time.perf_counter()
+    op = native.prune_list(ol, og["clustered_positions"], L, threads=threads)
+    t3 = time.perf_counter()
+    bits = np.ascontiguousarray(search.pack_masks(op["masks"]))
+    tf = []
+    for _ in range(reps):
+        t4 = time.perf_counter()
+        native.list_forces(op, og, system.positions, system.charges, system.lj_type, L, params_phys,
+                           threads=threads, packed_masks=bits)
+        tf.append(time.perf_counter() - t4)
+    return dict(grid=t1 - t0, search=t2 - t1, prune=t3 - t2, force=min(tf), threads=threads, og=og, op=op)
+
+
+def oracle_physics(params):
+    from oracle import forces as of
+
+    return of.Physics(r_cut=params.r_cut, lj_table=params.lj_table, coulomb_scale=params.coulomb_scale,
+                      shift_potential=params.shift_potential, elec=params.elec,
+                      epsilon_rf=params.epsilon_rf, ewald_beta=params.ewald_beta)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    system, table, occ = workload(args)
+    params = make_params(args, table)
+    phys = oracle_physics(params)
+    from oracle import native, search
+
+    L = system.box.lengths
+    threads = native.default_threads()
+    state = {}
+
+    def step(k):
+        if k % args.nstlist == 0 or not state:
+            og = search.build_grid(system.positions, L, M, occ)
+            ol = native.search_list(og, L, R_LIST, method="n2", threads=threads)
+            op = native.prune_list(ol, og["clustered_positions"], L, threads=threads)
+            state.update(og=og, op=op, bits=np.ascontiguousarray(search.pack_masks(op["masks"])))
+        native.list_forces(state["op"], state["og"], system.positions, system.charges, system.lj_type, L, phys,
+                           threads=threads, packed_masks=state["bits"])
+
+    for k in range(args.warmup):
+        step(k)
+    n_within = native.count_within(state["op"], state["og"]["clustered_positions"], L, R_CUT, threads=threads)
+    t0 = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        step(k)
+    dt = time.perf_counter() - t0
+    value = n_within * args.steps / dt
+    line = {
+        "impl": "reference", "metric": "nonbonded pair-interactions/s (useful, r<=r_c)", "value": value,
+        "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ns_per_day": args.steps / dt * DT_PS * 86.4,
+        "config": config(args, occ, {"impl": "oracle/ C port of the reference CPU path (no GPU)"}),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} steps (rebuild every {args.nstlist}) of the full workload"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+
+    import paper_1506_00716_b200 as nbx
+    from paper_1506_00716_b200 import _lib
+    from paper_1506_00716_b200.kernels import flops_per_pair
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    system, table, occ = workload(args)
+    params = nbx.NonbondedParams(**{k: getattr(make_params(args, table), k) for k in (
+        "r_cut", "r_list", "lj_table", "coulomb_scale", "shift_potential", "elec", "epsilon_rf", "ewald_beta")})
+    box = system.box
+    dev = torch.device("cuda", local)
+    pos_d = torch.from_numpy(np.array(system.positions)).to(dev)
+    q_d = torch.from_numpy(np.array(system.charges)).to(dev)
+    t_d = torch.from_numpy(np.array(system.lj_type)).to(dev)
+    f_d = torch.empty((system.n, 3), dtype=torch.float64, device=dev)
+    e_d = torch.zeros(2, dtype=torch.float64, device=dev)
+    bad_d = torch.empty(2, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = {}
+
+    def rebuild(pos):
+        grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
+        built = nbx.build_pair_list(grid, box, R_LIST)
+        st["grid"] = grid
+        st["plist"] = nbx.prune_pair_list(built, grid.clustered_positions_device, box)
+
+    def step(k, pos, q, t, out):
+        if k % args.nstlist == 0 or "plist" not in st:
+            rebuild(pos)
+        # energies on list steps (nstcalcenergy = nstlist), forces every step
+        nbx.compute_nonbonded_device(st["plist"], st["grid"], pos, q, t, params, box,
+                                     energy=(k % args.nstlist == 0), out=out, e_out=e_d, bad=bad_d)
+
+    clocks = Clocks(local)
+    for k in range(max(3, args.warmup)):
+        step(k, pos_d, q_d, t_d, f_d)
+    torch.cuda.synchronize()
+    if int(bad_d[0].item()) != -1:
+        raise RuntimeError("singular pair in the benchmark system")
+    stats = nbx.interaction_stats(st["plist"], st["grid"], st["grid"].clustered_positions_device, box, R_CUT)
+    n_within, n_admitted = stats.n_within_cutoff, stats.n_admitted
+
+    # ---- device-resident timed region
+    W = max(3, args.warmup)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    lib.nbx_timing_query(None, None)
+    lib.nbx_timing_enable(1)
+    launches0 = lib.nbx_launch_count()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record()
+        step(W + i, pos_d, q_d, t_d, f_d)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = lib.nbx_launch_count() - launches0
+    lib.nbx_timing_enable(0)
+    fk_ms, fk_n = (np.zeros(1), np.zeros(1, dtype=np.int64))
+    _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
+    clk = clocks.stop()
+    t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if dist is not None:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = world * n_within * args.steps / (t_ms * 1e-3)
+
+    # ---- end-to-end through the public API with host (pinned) buffers
+    pos_h = torch.from_numpy(np.array(system.positions)).pin_memory()
+    q_h = torch.from_numpy(np.array(system.charges)).pin_memory()
+    t_h = torch.from_numpy(np.array(system.lj_type)).pin_memory()
+    f_h = torch.empty((system.n, 3), dtype=torch.float64).pin_memory()
+    e_h = torch.empty(2, dtype=torch.float64).pin_memory()
+    pos_s = torch.empty_like(pos_d)
+    q_s = torch.empty_like(q_d)
+    t_s = torch.empty_like(t_d)
+    st.clear()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(W + args.steps):
+        if i >= W:
+            flush.zero_()
+            ev2[i - W][0].record()
+        pos_s.copy_(pos_h, non_blocking=True)
+        q_s.copy_(q_h, non_blocking=True)
+        t_s.copy_(t_h, non_blocking=True)
+        step(i, pos_s, q_s, t_s, f_d)
+        f_h.copy_(f_d, non_blocking=True)
+        e_h.copy_(e_d, non_blocking=True)
+        if i >= W:
+            ev2[i - W][1].record()
+    torch.cuda.synchronize()
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in ev2))
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    h2d = system.n * (24 + 8 + 8)
+    d2h = system.n * 24 + 16
+
+    # ---- roofline (force kernel, FP32 pipe)
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tf = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
+    fpp = flops_per_pair(params)
+    fk_avg_ms = float(fk_ms[0]) / max(1, int(fk_n[0]))
+    achieved = n_admitted * fpp / (fk_avg_ms * 1e-3) / 1e12
+    traffic = None
+    prof = REPO / "profiles" / "force_kernel_ncu.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "nonbonded pair-interactions/s (useful, r<=r_c)",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": W,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 (pair math; fp64 energy + final force accumulation)",
+        "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
+        "config": config(args, occ),
+        "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
+        "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted,
+                           "admitted_per_s": world * n_admitted * args.steps / (t_ms * 1e-3)},
+        "e2e": {"value": world * n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms / args.steps},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp32", "kernel": "k_force", "achieved": achieved, "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+                     "kernel_ms": fk_avg_ms, "flops_per_pair": fpp,
+                     "peak_note": f"nominal FP32: {n_sm} SMs x 128 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)"},
+        "clocks": clk,
+        "wall_s_timed": wall,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c = cpu_port_times(system, oracle_physics(params), occ, args.nstlist)
+        per_step = c["force"] + (c["grid"] + c["search"] + c["prune"]) / args.nstlist
+        line["cpu_baseline"] = {
+            "value": n_within / per_step, "unit": "pairs/s", "cores": c["threads"], "kind": "port",
+            "sample": (f"one rebuild (grid {c['grid']:.3f}s, O(n_c^2) search {c['search']:.3f}s, "
+                       f"prune {c['prune']:.3f}s) + one force pass {c['force']:.3f}s, amortised over "
+                       f"nstlist={args.nstlist}")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * nbx -- B200 (sm_100a) cluster-pair (nbnxn) neighbour search and
+ * short-range non-bonded force: the C ABI.
+ *
+ * Every entry point replaces one function of the reference Python package
+ * clustermd (/root/reference/pkg/src/clustermd); the citation on each
+ * declaration names it.  Conventions:
+ *   - plain pointers + sizes, no C++ or torch types;
+ *   - pointers documented "device" are CUDA device pointers (any allocator,
+ *     e.g. torch tensors), "host" are host pointers;
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *     all work is enqueued on it; functions documented "syncs" wait on it;
+ *   - return 0 on success, NBX_ERR_PARAM on a contract violation (the
+ *     reference raises ParameterError), NBX_ERR_SINGULAR when an admitted
+ *     pair inside the cutoff has r^2 == 0 (SingularityError), NBX_ERR_CUDA
+ *     on a CUDA failure; nbx_last_error() describes the last failure.
+ *   - grids and lists are opaque, device-resident handles owned by the
+ *     library; they are immutable after creation (like the reference's
+ *     frozen dataclasses) except for lazily built caches.
+ */
+#ifndef NBX_H
+#define NBX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  NBX_OK = 0,
+  NBX_ERR_PARAM = 1,
+  NBX_ERR_SINGULAR = 2,
+  NBX_ERR_CUDA = 3
+};
+
+enum { NBX_ELEC_CUTOFF = 0, NBX_ELEC_REACTION_FIELD = 1, NBX_ELEC_EWALD = 2 };
+
+enum {
+  NBX_FORCE_ENERGY = 1,      /* compute e_lj / e_coulomb (else e_out untouched)         */
+  NBX_FORCE_ACCUMULATE = 2,  /* f_out += forces (compute_nonbonded_into semantics)      */
+  NBX_FORCE_CLUSTERED = 4,   /* f_out is (n_slots, 3) in slot order, else (n, 3) original */
+  NBX_FORCE_CANONICAL = 8    /* evaluate the canonical CSR rows (generic kernel) even
+                                when the grouped fast layout exists (testing aid)      */
+};
+
+typedef struct nbx_grid nbx_grid_t;
+typedef struct nbx_list nbx_list_t;
+
+typedef struct {
+  int32_t n_types;          /* t                                                     */
+  const double* lj_table;   /* host, (t, t, 2): [epsilon kJ/mol, sigma nm]            */
+  double coulomb_scale;     /* kJ mol^-1 nm e^-2 (model.py:17)                         */
+  double r_cut;             /* nm                                                      */
+  int32_t shift_potential;  /* subtract the pair energy at r_cut (kernels.py:105-110)  */
+  int32_t elec;             /* NBX_ELEC_*                                              */
+  double k_rf, c_rf;        /* reaction field (elec == NBX_ELEC_REACTION_FIELD)        */
+  double ewald_beta;        /* nm^-1 (elec == NBX_ELEC_EWALD)                          */
+} nbx_params_t;
+
+int nbx_version(void);
+const char* nbx_last_error(void);
+/* instrumentation: kernels launched by this library since load; event
+ * timing of the force kernel (enable, then query: total ms + launch count
+ * since the last query; the query syncs on the recorded events) */
+int64_t nbx_launch_count(void);
+void nbx_timing_enable(int32_t on);
+int nbx_timing_query(double* total_ms, int64_t* n_launches);
+
+/* ---------------------------------------------------------------- grid
+ * Replaces gridder.build_cluster_grid (gridder.py:69-146).  positions:
+ * device (n, 3) f64 in original order (wrapped internally, model.py:147).
+ * cells = round(sqrt(n / target_occupancy)) computed by the caller exactly
+ * as gridder.py:91 does.  Output perm / fill_mask / cell_of_cluster /
+ * clustered_positions / bboxes are bit-identical to the reference. */
+int nbx_grid_build(const double* positions, int64_t n, const double box[3], int32_t m,
+                   int64_t cells, void* stream, nbx_grid_t** out);
+/* out = {n, m, cells, n_clusters, n_slots}; syncs */
+int nbx_grid_info(const nbx_grid_t* grid, int64_t out[5]);
+/* host outputs (any may be NULL): perm (n_slots), inverse_perm (n),
+ * fill_mask (n_slots), cell_of_cluster (n_clusters), clustered_positions
+ * (n_slots*3), bboxes (n_clusters*6: lo xyz, hi xyz); syncs */
+int nbx_grid_download(const nbx_grid_t* grid, int64_t* perm, int64_t* inverse_perm,
+                      uint8_t* fill_mask, int64_t* cell_of_cluster, double* clustered_positions,
+                      double* bboxes, void* stream);
+/* device pointer to the wrapped build-time clustered positions (n_slots, 3) */
+const double* nbx_grid_clustered_positions(const nbx_grid_t* grid);
+/* gridder.scatter_to_original (gridder.py:149-162): device (n_slots, k) f64
+ * -> device (n, k) f64, filler slots dropped */
+int nbx_scatter_to_original(const nbx_grid_t* grid, const double* clustered, int32_t k,
+                            double* out, void* stream);
+void nbx_grid_free(nbx_grid_t* grid);
+
+/* ---------------------------------------------------------------- lists
+ * Replaces pairlist.build_pair_list (pairlist.py:147-217): every cluster
+ * pair (ci, cj >= ci) whose periodic bounding-box gap is <= r_list, CSR
+ * ascending in cj, masks per pairlist.py:106-112.  Errors as :164-175. */
+int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], double r_list, void* stream,
+                       nbx_list_t** out);
+/* Replaces pairlist.prune_pair_list (pairlist.py:242-282): keep rows whose
+ * exact FP64 min-image distance over admitted slot pairs is <= r_list, plus
+ * every diagonal row.  clustered_positions: device (n_slots, 3) f64. */
+int nbx_pairlist_prune(const nbx_list_t* list, const nbx_grid_t* grid,
+                       const double* clustered_positions, const double box[3], void* stream,
+                       nbx_list_t** out);
+/* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; syncs */
+int nbx_list_info(const nbx_list_t* list, int64_t out[5]);
+/* host outputs (any may be NULL): offsets (n_i_clusters+1), j_idx (n_rows),
+ * masks (n_rows, bit a*m+b of uint64); syncs */
+int nbx_list_download(const nbx_list_t* list, int64_t* offsets, int64_t* j_idx, uint64_t* masks,
+                      void* stream);
+/* Replaces pairlist._build_super_layout (pairlist.py:115-144) for groups of
+ * `size` consecutive i-clusters; returns the union entry count; syncs. */
+int nbx_super_layout(const nbx_list_t* list, int32_t size, void* stream, int64_t* n_entries);
+/* host outputs: super_offsets (n_groups+1), super_j (n_entries),
+ * super_pair_idx (n_entries*size, -1 = absent); syncs */
+int nbx_super_download(const nbx_list_t* list, int64_t* super_offsets, int64_t* super_j,
+                       int64_t* super_pair_idx, void* stream);
+/* pairlist.interaction_stats / _count_within (pairlist.py:303-346):
+ * out = {n_admitted, n_within_cutoff} at clustered_positions; syncs */
+int nbx_count_within(const nbx_list_t* list, const double* clustered_positions,
+                     const double box[3], double r_cut, void* stream, int64_t out[2]);
+void nbx_list_free(nbx_list_t* list);
+
+/* ---------------------------------------------------------------- force
+ * Replaces kernels.compute_nonbonded_into (kernels.py:328-396) and its
+ * numba kernels (_kernel_blocks :124-221, _kernel_super_blocks :224-312).
+ * positions/charges/lj_type: device, original order (n,3) f64, (n) f64,
+ * (n) i64.  i_sel: device int32 list of i-clusters (NULL = all).
+ * f_out: device f64, (n,3) original order or (n_slots,3) with
+ * NBX_FORCE_CLUSTERED.  e_out: device f64[2] = {e_lj, e_coulomb}.
+ * bad: device int64[2], set to the clustered slots of a singular pair or -1.
+ * FP32 pair arithmetic, FP64 accumulation of energies and of the final
+ * forces; results are bit-identical across reruns.  Does not sync; the
+ * caller reads bad[] to raise SingularityError. */
+int nbx_force(const nbx_list_t* list, const nbx_grid_t* grid, const double* positions,
+              const double* charges, const int64_t* lj_type, const nbx_params_t* params,
+              const double box[3], const int32_t* i_sel, int64_t n_sel, int32_t flags,
+              double* f_out, double* e_out, int64_t* bad, void* stream);
+
+/* Exact FP64 scan of every admitted pair for a coincident in-range pair
+ * (kernels.py:184-187, 390-395); run when nbx_force reported bad = {-2,-2}
+ * (non-finite forces).  out = clustered slots or {-1,-1}; syncs. */
+int nbx_find_singular(const nbx_list_t* list, const nbx_grid_t* grid, const double* positions,
+                      double r_cut, const double box[3], void* stream, int64_t out[2]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBX_H */

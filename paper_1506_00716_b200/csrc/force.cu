@@ -1,0 +1,867 @@
+// Non-bonded force + energy over the cluster-pair list (sm_100a).
+//
+// Replaces kernels.compute_nonbonded_into (kernels.py:328-396) with its numba
+// kernels _kernel_blocks (:124-221) and _kernel_super_blocks (:224-312) of
+// /root/reference/pkg/src/clustermd, and extends the pair potential
+// (lj_coulomb_terms, :84-111) with reaction-field and Ewald real-space terms.
+//
+// Work unit: a GROUP of G consecutive i-clusters (16 i-atoms) and its ENTRIES
+// (one per j-cluster, carrying every member's m x m mask; search.cu).  One
+// warp per group.  Lane (r, b) = (entry slot r of 32/m, j-atom b of m): each
+// lane holds one j-atom in registers and sweeps the group's 16 i-atoms, which
+// live in shared memory (broadcast LDS).  Consequences:
+//   * j-forces accumulate in registers across all members -> one float4 store
+//     per (entry, j-atom): no atomics, no shuffles;
+//   * i-forces accumulate in registers across all entries -> one shared-memory
+//     transpose-reduce per group;
+//   * members absent from every entry of an iteration are skipped
+//     warp-uniformly.
+// The j-side partials are summed per atom by k_reduce in a fixed order
+// (entries sorted by j-cluster), so forces are bit-reproducible with no
+// fixed-point or float atomics.  Energies: FP32 per pair, FP64 per lane,
+// fixed-order reduction.
+//
+// Periodicity: every entry carries the image shift of its j-cluster relative
+// to the group (search.cu); a per-pair FP32 minimum image is used instead for
+// the (rare) iterations holding an entry whose slack cannot guarantee a single
+// image at the current displacements.  Cutoff decisions within a narrow band
+// around r_c are re-made in FP64 exactly as the reference (kernels.py:165-184)
+// when the Coulomb force is discontinuous at r_c (cutoff / reaction-field).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace nbx {
+
+enum { FE_RF = 0, FE_EWALD = 1 };
+
+struct ForceArgs {
+  // work items
+  int64_t n_work;
+  const int32_t* sel;         // optional: work item -> group / i-cluster
+  const int32_t* grp_first;   // group -> first member cluster (NULL: identity, canonical)
+  const int32_t* grp_nmem;    // group -> member count (NULL: 1)
+  const int32_t* ent_off;     // group -> entry range
+  const int32_t* ent_j;
+  const float4* ent_delta;    // j-local -> group-local offset (image included)
+  const float* ent_slack;
+  const uint64_t* ent_mask;
+  // per-slot inputs
+  const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
+  const double* bbox;         // grid bboxes (origins of the local frames)
+  const int32_t* type;
+  const float4* lj;           // (nt * nt) {6 c6, 12 c12, shift_lj, 0}
+  int nt;
+  // outputs
+  float4* part_i;
+  float4* part_j;
+  double* e_grp;              // 2 per work item
+  unsigned int* scalars;      // [0] max displacement (float bits); [2..3] bad key
+  // physics
+  float rc2, k2rf, krf, crf, coul;
+  float beta, beta3, ew_shift, ew_a;
+  float ew_f[13], ew_v[13];         // EW_DEG + 1 coefficients, highest first
+  float slack_base;           // 2 r_c + margin; unsafe if slack < base + 4 d_max
+  float band;
+  float L[3], invL[3];
+  // exact re-check
+  const double* pos;          // original order
+  const int32_t* perm;
+  double rc2d;
+  Box box;
+};
+
+__device__ __forceinline__ void record_bad(unsigned int* scalars, int64_t si, int64_t sj) {
+  unsigned long long key = ((unsigned long long)si << 32) | (unsigned long long)(sj & 0xffffffff);
+  atomicMin(reinterpret_cast<unsigned long long*>(scalars + 2), key);
+}
+
+// Exact reference decision for one pair (kernels.py:165-184): raw gathered
+// positions, numba min image, sequential r^2.  Returns 1 inside, 0 outside,
+// -1 singular.
+__device__ __noinline__ int exact_inside(const ForceArgs& A, int64_t si, int64_t sj) {
+  const int64_t oi = A.perm[si], oj = A.perm[sj];
+  double d[3];
+  for (int k = 0; k < 3; ++k)
+    d[k] = min_image_kernel(__dsub_rn(A.pos[3 * oi + k], A.pos[3 * oj + k]), A.box.L[k], A.box.invL[k]);
+  const double r2 = d2_seq(d[0], d[1], d[2]);
+  if (r2 > A.rc2d) return 0;
+  if (r2 == 0.0) return -1;
+  return 1;
+}
+
+constexpr int FW = 4;  // warps per block
+
+template <int M>
+__host__ __device__ constexpr uint64_t column_bits() {
+  uint64_t c = 0;
+  for (int a = 0; a < M; ++a) c |= 1ull << (a * M);
+  return c;
+}
+
+// Ewald real-space correction polynomials (host-fitted, force.cu
+// ewald_fit): with w = beta^2 r^2 and u = w * (2/w_max) - 1 in [-1, 1],
+//   Gf(u) ~ erf(z)/z^3 - 2/sqrt(pi) exp(-w)/w   (force)
+//   Gv(u) ~ erf(z)/z                            (energy),  z = beta r,
+// so that F_c/r = qq (1/r^3 - beta^3 Gf) and E_c = qq (1/r - beta Gv - shift):
+// no transcendental beyond the rsqrt every pair needs anyway.
+constexpr int EW_DEG = 12;
+
+// One pair: F/r, plus energies when requested.  `inc` masks everything:
+// rinv is zeroed, and qq too where a term does not carry rinv.
+template <int ELEC, bool KRF, bool ENERGY>
+__device__ __forceinline__ float pair_eval(const ForceArgs& A, const float4& xi, const float4& lj, float xjw,
+                                           float r2, bool inc, float& elj, float& ec) {
+  float rinv = rsqrtf(r2);
+  rinv = inc ? rinv : 0.f;
+  const float rinv2 = rinv * rinv;
+  const float rinv6 = rinv2 * rinv2 * rinv2;
+  const float qq = xi.w * xjw;
+  const float flj = rinv6 * fmaf(lj.y, rinv6, -lj.x);  // 12 c12/r^12 - 6 c6/r^6
+  float fscal;
+  if (ELEC == FE_RF) {
+    fscal = fmaf(qq, rinv, flj) * rinv2;
+    if (KRF || ENERGY) {
+      const float qm = inc ? qq : 0.f;
+      if (KRF) fscal = fmaf(-qm, A.k2rf, fscal);
+      if (ENERGY) ec = qm * (rinv + fmaf(A.krf, r2, -A.crf));
+    }
+  } else {
+    const float qm = inc ? qq : 0.f;
+    const float u = fmaf(r2, A.ew_a, -1.f);
+    float pf = A.ew_f[0];
+#pragma unroll
+    for (int k = 1; k <= EW_DEG; ++k) pf = fmaf(pf, u, A.ew_f[k]);
+    const float t = fmaf(-A.beta3, pf, rinv * rinv2);
+    fscal = fmaf(qm, t, flj * rinv2);
+    if (ENERGY) {
+      float pv = A.ew_v[0];
+#pragma unroll
+      for (int k = 1; k <= EW_DEG; ++k) pv = fmaf(pv, u, A.ew_v[k]);
+      ec = qm * (rinv - fmaf(A.beta, pv, A.ew_shift));
+    }
+  }
+  if (ENERGY) elj = inc ? fmaf(rinv6, fmaf(lj.y * (1.f / 12.f), rinv6, -lj.x * (1.f / 6.f)), -lj.z) : 0.f;
+  return fscal;
+}
+
+template <bool MI>
+__device__ __forceinline__ float pair_geom(const ForceArgs& A, const float4& xi, const float4& xj, float& dx,
+                                           float& dy, float& dz) {
+  dx = xi.x - xj.x;
+  dy = xi.y - xj.y;
+  dz = xi.z - xj.z;
+  if (MI) {
+    dx = fmaf(-A.L[0], rintf(dx * A.invL[0]), dx);
+    dy = fmaf(-A.L[1], rintf(dy * A.invL[1]), dy);
+    dz = fmaf(-A.L[2], rintf(dz * A.invL[2]), dz);
+  }
+  return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+// One iteration body: this lane's entry (j-atom xj, pre-shifted masks mk)
+// against the group's i-atoms.  MI = per-pair minimum image.
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND, bool MI>
+__device__ __forceinline__ void sweep(const ForceArgs& A, const float4* __restrict__ s_xi,
+                                      const float4* __restrict__ s_ljt, const uint64_t* mk, unsigned wpres,
+                                      const float4& xj, float (&fi)[G * M][3], float& fjx, float& fjy,
+                                      float& fjz, float& elj, float& ec, uint32_t& near) {
+  constexpr int MM = M * M;
+  constexpr int W = (G * M * M > 64) ? 2 : 1;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    if (!((wpres >> k) & 1u)) continue;
+    // this member's m x m bits (pre-shifted by b): 32-bit for m <= 4
+    uint64_t word64;
+    if constexpr (W == 2) word64 = mk[k];
+    else word64 = mk[0] >> (k * MM);
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      const int ia = k * M + a;
+      const float4 xi = s_xi[ia];
+      const float4 lj = s_ljt[ia];
+      float dx, dy, dz;
+      const float r2 = pair_geom<MI>(A, xi, xj, dx, dy, dz);
+      bool adm;
+      if constexpr (M <= 4) adm = ((uint32_t)word64 >> (a * M)) & 1u;
+      else adm = (a < 4) ? (((uint32_t)word64 >> (a * M)) & 1u) : (((uint32_t)(word64 >> 32) >> ((a - 4) * M)) & 1u);
+      const bool inc = adm && (r2 <= A.rc2);
+      if (BAND) near |= (adm && fabsf(r2 - A.rc2) < A.band) ? (1u << ia) : 0u;
+      float pe_lj = 0.f, pe_c = 0.f;
+      const float fscal = pair_eval<ELEC, KRF, ENERGY>(A, xi, lj, xj.w, r2, inc, pe_lj, pe_c);
+      if (ENERGY) {
+        elj += pe_lj;
+        ec += pe_c;
+      }
+      fi[ia][0] = fmaf(fscal, dx, fi[ia][0]);
+      fi[ia][1] = fmaf(fscal, dy, fi[ia][1]);
+      fi[ia][2] = fmaf(fscal, dz, fi[ia][2]);
+      fjx = fmaf(-fscal, dx, fjx);
+      fjy = fmaf(-fscal, dy, fjy);
+      fjz = fmaf(-fscal, dz, fjz);
+    }
+  }
+}
+
+// Rare path: pairs whose FP32 r^2 fell within `band` of r_c^2 get the exact
+// FP64 reference decision; when it differs the pair's contribution is added
+// or removed (i-side through shared-memory atomics).
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool MI>
+__device__ __noinline__ void band_fix(const ForceArgs& A, const float4* __restrict__ s_xi,
+                                      const float4* __restrict__ s_ljt, float* s_corr, uint32_t near,
+                                      const float4& xj, int32_t first, int32_t cj, int b, float& fjx,
+                                      float& fjy, float& fjz, float& elj, float& ec) {
+  while (near) {
+    const int ia = __ffs(near) - 1;
+    near &= near - 1;
+    const float4 xi = s_xi[ia];
+    float dx, dy, dz;
+    const float r2 = pair_geom<MI>(A, xi, xj, dx, dy, dz);
+    const bool inc32 = r2 <= A.rc2;
+    const int ex = exact_inside(A, (int64_t)first * M + ia, (int64_t)cj * M + b);
+    if (ex < 0) record_bad(A.scalars, (int64_t)first * M + ia, (int64_t)cj * M + b);
+    const bool inc64 = ex > 0;
+    if (inc64 == inc32) continue;
+    float pe_lj = 0.f, pe_c = 0.f;
+    const float fscal = pair_eval<ELEC, KRF, ENERGY>(A, xi, s_ljt[ia], xj.w, r2, true, pe_lj, pe_c);
+    const float sg = inc64 ? 1.f : -1.f;
+    atomicAdd(&s_corr[3 * ia + 0], sg * fscal * dx);
+    atomicAdd(&s_corr[3 * ia + 1], sg * fscal * dy);
+    atomicAdd(&s_corr[3 * ia + 2], sg * fscal * dz);
+    fjx -= sg * fscal * dx;
+    fjy -= sg * fscal * dy;
+    fjz -= sg * fscal * dz;
+    if (ENERGY) {
+      elj += sg * pe_lj;
+      ec += sg * pe_c;
+    }
+  }
+}
+
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND>
+__global__ void __launch_bounds__(FW * 32)
+k_force(const ForceArgs A) {
+  constexpr int R = 32 / M;   // entries per iteration
+  constexpr int IA = G * M;   // i-atoms per group
+  constexpr int W = (G * M * M > 64) ? 2 : 1;
+  constexpr int MM = M * M;
+  extern __shared__ float4 s_dyn[];  // [FW][nt][IA] LJ params per (j-type, i-atom)
+  __shared__ float4 s_xi[FW][IA];
+  __shared__ float s_red[FW][32][IA * 3 + 1];
+  __shared__ float s_corr[FW][IA * 3];
+
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane / M, b = lane % M;
+  const int64_t wi = blockIdx.x * (int64_t)FW + w;
+  if (wi >= A.n_work) return;
+  const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
+  const int32_t first = A.grp_first ? A.grp_first[g] : g;
+  const int nmem = A.grp_nmem ? A.grp_nmem[g] : 1;
+  const int32_t e_beg = A.ent_off[g], e_end = A.ent_off[g + 1];
+  float4* s_lj = s_dyn + (size_t)w * IA * A.nt;
+
+  // stage the group's i-atoms and their LJ parameters per j-type
+  for (int ia = lane; ia < IA; ia += 32) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ia < nmem * M) {
+      // member-local -> group-local (origin: first member's bbox low corner), FP64 offset
+      v = A.xyzq[(int64_t)first * M + ia];
+      const int64_t c = first + ia / M;
+      v.x = (float)((A.bbox[6 * c + 0] - A.bbox[6 * (int64_t)first + 0]) + (double)v.x);
+      v.y = (float)((A.bbox[6 * c + 1] - A.bbox[6 * (int64_t)first + 1]) + (double)v.y);
+      v.z = (float)((A.bbox[6 * c + 2] - A.bbox[6 * (int64_t)first + 2]) + (double)v.z);
+      v.w *= A.coul;
+    }
+    s_xi[w][ia] = v;
+  }
+  for (int idx = lane; idx < IA * A.nt; idx += 32) {
+    const int t = idx / IA, ia = idx - t * IA;
+    const int ti = ia < nmem * M ? A.type[(int64_t)first * M + ia] : 0;
+    s_lj[idx] = __ldg(&A.lj[ti * A.nt + t]);
+  }
+  if (BAND)
+    for (int c = lane; c < IA * 3; c += 32) s_corr[w][c] = 0.f;
+  __syncwarp();
+
+  const float slack_thr = A.slack_base + 4.f * __uint_as_float(A.scalars[0]);
+  float fi[IA][3];
+#pragma unroll
+  for (int ia = 0; ia < IA; ++ia) fi[ia][0] = fi[ia][1] = fi[ia][2] = 0.f;
+  double elj_acc = 0.0, ec_acc = 0.0;
+  constexpr uint64_t colmask = column_bits<M>();
+
+  for (int32_t e0 = e_beg; e0 < e_end; e0 += R) {
+    const int32_t e = e0 + r;
+    const bool valid = e < e_end;
+    uint64_t mk[W];
+    float4 xj = make_float4(0.f, 0.f, 0.f, 0.f);
+    int tj = 0;
+    bool unsafe = false;
+    int32_t cj = 0;
+    if (valid) {
+      cj = A.ent_j[e];
+      const float4 S = A.ent_delta[e];
+#pragma unroll
+      for (int q = 0; q < W; ++q) mk[q] = A.ent_mask[(int64_t)e * W + q] >> b;
+      xj = A.xyzq[(int64_t)cj * M + b];
+      tj = A.type[(int64_t)cj * M + b];
+      xj.x += S.x;
+      xj.y += S.y;
+      xj.z += S.z;
+      unsafe = A.ent_slack[e] < slack_thr;
+    } else {
+#pragma unroll
+      for (int q = 0; q < W; ++q) mk[q] = 0ull;
+    }
+    unsigned pres = 0;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      uint64_t word;
+      if constexpr (W == 2) word = mk[k];
+      else word = mk[0] >> (k * MM);
+      pres |= ((word & colmask) != 0ull) ? (1u << k) : 0u;
+    }
+    const unsigned wpres = __reduce_or_sync(0xffffffffu, pres);
+    const bool wunsafe = __any_sync(0xffffffffu, unsafe);
+    const float4* s_ljt = s_lj + tj * IA;
+    float fjx = 0.f, fjy = 0.f, fjz = 0.f;
+    float elj = 0.f, ec = 0.f;
+    uint32_t near = 0;
+    if (!wunsafe)
+      sweep<M, G, ELEC, KRF, ENERGY, BAND, false>(A, s_xi[w], s_ljt, mk, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+    else
+      sweep<M, G, ELEC, KRF, ENERGY, BAND, true>(A, s_xi[w], s_ljt, mk, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+    if (BAND && __any_sync(0xffffffffu, near != 0)) {
+      if (near) {
+        if (!wunsafe)
+          band_fix<M, G, ELEC, KRF, ENERGY, false>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cj, b, fjx, fjy, fjz, elj, ec);
+        else
+          band_fix<M, G, ELEC, KRF, ENERGY, true>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cj, b, fjx, fjy, fjz, elj, ec);
+      }
+      __syncwarp();
+    }
+    if (valid) A.part_j[(int64_t)e * M + b] = make_float4(fjx, fjy, fjz, 0.f);
+    if (ENERGY) {
+      elj_acc += (double)elj;
+      ec_acc += (double)ec;
+    }
+  }
+
+  // i-force transpose-reduce through shared memory
+#pragma unroll
+  for (int ia = 0; ia < IA; ++ia) {
+    s_red[w][lane][3 * ia + 0] = fi[ia][0];
+    s_red[w][lane][3 * ia + 1] = fi[ia][1];
+    s_red[w][lane][3 * ia + 2] = fi[ia][2];
+  }
+  __syncwarp();
+  for (int c = lane; c < IA * 3; c += 32) {
+    float sacc = BAND ? s_corr[w][c] : 0.f;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) sacc += s_red[w][l][c];
+    s_red[w][0][c] = sacc;  // column c is read and written by this lane only
+  }
+  __syncwarp();
+  if (lane < nmem * M) {
+    A.part_i[(int64_t)first * M + lane] =
+        make_float4(s_red[w][0][3 * lane], s_red[w][0][3 * lane + 1], s_red[w][0][3 * lane + 2], 0.f);
+  }
+  if (ENERGY) {
+    for (int o = 16; o; o >>= 1) {
+      elj_acc += __shfl_xor_sync(0xffffffffu, elj_acc, o);
+      ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
+    }
+    if (lane == 0) {
+      A.e_grp[2 * wi] = elj_acc;
+      A.e_grp[2 * wi + 1] = ec_acc;
+    }
+  }
+}
+
+// Gather positions for this evaluation: clustered FP32 coordinates placed in
+// the periodic image nearest to the build-time positions (so build-time shift
+// vectors stay valid), charges, types, and the max displacement since build.
+__global__ void k_gather(const double* __restrict__ pos, const double* __restrict__ q,
+                         const int64_t* __restrict__ typ, const int32_t* __restrict__ perm,
+                         const uint8_t* __restrict__ fill, const double* __restrict__ cpos,
+                         const double* __restrict__ bbox, int m, int64_t n_slots, Box box,
+                         float4* __restrict__ xyzq,
+                         int32_t* __restrict__ type_out, unsigned int* __restrict__ scalars) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float disp = 0.f;
+  if (s < n_slots) {
+    const int64_t o = perm[s];
+    float v[3];
+    double d2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      const double x = pos[3 * o + d], xb = cpos[3 * s + d];
+      const double xu = x - box.L[d] * rint((x - xb) * box.invL[d]);
+      v[d] = (float)(xu - bbox[6 * (s / m) + d]);
+      d2 += (xu - xb) * (xu - xb);
+    }
+    disp = (float)sqrt(d2);
+    xyzq[s] = make_float4(v[0], v[1], v[2], fill[s] ? 0.f : (float)q[o]);
+    type_out[s] = (int32_t)typ[o];
+  }
+  for (int o = 16; o; o >>= 1) disp = fmaxf(disp, __shfl_xor_sync(0xffffffffu, disp, o));
+  if ((threadIdx.x & 31) == 0 && disp > 0.f) atomicMax(&scalars[0], __float_as_uint(disp));
+}
+
+// Final per-atom forces: own i-partial + j-partials of every entry whose
+// j-cluster holds the atom, summed in FP64 in ascending entry order.
+__global__ void k_reduce(const float4* __restrict__ part_i, const float4* __restrict__ part_j,
+                         const int32_t* __restrict__ t_first, const int32_t* __restrict__ t_items,
+                         const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
+                         int64_t n_slots, int m, int flags, double* __restrict__ f_out,
+                         unsigned int* __restrict__ flag) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  const int64_t c = s / m, b = s - c * m;
+  const float4 pi = part_i[s];
+  double fx = pi.x, fy = pi.y, fz = pi.z;
+  for (int32_t t = t_first[c]; t < t_first[c + 1]; ++t) {
+    const float4 pj = part_j[(int64_t)t_items[t] * m + b];
+    fx += pj.x;
+    fy += pj.y;
+    fz += pj.z;
+  }
+  if (!isfinite(fx) || !isfinite(fy) || !isfinite(fz)) atomicOr(flag, 1u);
+  int64_t o;
+  if (flags & NBX_FORCE_CLUSTERED) {
+    o = s;
+  } else {
+    if (fill[s]) return;
+    o = perm[s];
+  }
+  if (flags & NBX_FORCE_ACCUMULATE) {
+    f_out[3 * o] += fx;
+    f_out[3 * o + 1] += fy;
+    f_out[3 * o + 2] += fz;
+  } else {
+    f_out[3 * o] = fx;
+    f_out[3 * o + 1] = fy;
+    f_out[3 * o + 2] = fz;
+  }
+}
+
+__global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __restrict__ e_out,
+                         const unsigned int* __restrict__ scalars, int64_t* __restrict__ bad) {
+  __shared__ double s[2][256];
+  double a = 0.0, c = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    a += e_grp[2 * i];
+    c += e_grp[2 * i + 1];
+  }
+  s[0][threadIdx.x] = a;
+  s[1][threadIdx.x] = c;
+  __syncthreads();
+  for (int h = 128; h; h >>= 1) {
+    if (threadIdx.x < h) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + h];
+      s[1][threadIdx.x] += s[1][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (e_out) {
+      e_out[0] = s[0][0];
+      e_out[1] = s[1][0];
+    }
+    if (bad) {
+      const unsigned long long key = *reinterpret_cast<const unsigned long long*>(scalars + 2);
+      if (key == ~0ull) {
+        // non-finite forces without a located pair: the host runs
+        // nbx_find_singular (exact scan) to name the coincident pair
+        bad[0] = bad[1] = scalars[1] ? -2 : -1;
+      } else {
+        bad[0] = (int64_t)(key >> 32);
+        bad[1] = (int64_t)(key & 0xffffffffull);
+      }
+    }
+  }
+}
+
+__global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, int shift,
+                           float4* __restrict__ lj) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt * nt) return;
+  const double eps = tab[2 * i], sig = tab[2 * i + 1];
+  const double s2 = sig * sig, s6 = s2 * s2 * s2;
+  const double c6 = 4.0 * eps * s6, c12 = 4.0 * eps * s6 * s6;
+  double sh = 0.0;
+  if (shift) {
+    const double sr2 = s2 / rc2, sr6 = sr2 * sr2 * sr2;
+    sh = 4.0 * eps * (sr6 * sr6 - sr6);
+  }
+  lj[i] = make_float4((float)(6.0 * c6), (float)(12.0 * c12), (float)sh, 0.f);
+}
+
+// ---------------------------------------------------------------- dispatch
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND>
+static cudaError_t launch_one(const ForceArgs& A, cudaStream_t s) {
+  constexpr int IA = G * M;
+  const size_t dyn = sizeof(float4) * (size_t)FW * IA * A.nt;
+  auto kern = k_force<M, G, ELEC, KRF, ENERGY, BAND>;
+  if (dyn > 32 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t blocks = (A.n_work + FW - 1) / FW;
+  if (blocks > 0) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool tm = timing_enabled();
+    if (tm) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+    count_launch();
+    kern<<<(unsigned)blocks, FW * 32, dyn, s>>>(A);
+    if (tm) {
+      cudaEventRecord(e1, s);
+      timing_record(e0, e1);
+    }
+  }
+  return cudaGetLastError();
+}
+
+template <int M, int G>
+static cudaError_t launch_mg(const ForceArgs& A, int elec, bool krf, bool energy, bool band, cudaStream_t s) {
+  if (elec == FE_EWALD)
+    return energy ? launch_one<M, G, FE_EWALD, false, true, false>(A, s)
+                  : launch_one<M, G, FE_EWALD, false, false, false>(A, s);
+  if (krf) {
+    if (band)
+      return energy ? launch_one<M, G, FE_RF, true, true, true>(A, s) : launch_one<M, G, FE_RF, true, false, true>(A, s);
+    return energy ? launch_one<M, G, FE_RF, true, true, false>(A, s) : launch_one<M, G, FE_RF, true, false, false>(A, s);
+  }
+  if (band)
+    return energy ? launch_one<M, G, FE_RF, false, true, true>(A, s) : launch_one<M, G, FE_RF, false, false, true>(A, s);
+  return energy ? launch_one<M, G, FE_RF, false, true, false>(A, s) : launch_one<M, G, FE_RF, false, false, false>(A, s);
+}
+
+static cudaError_t launch_force(int m, bool grouped, const ForceArgs& A, int elec, bool krf, bool energy, bool band,
+                                cudaStream_t s) {
+  switch (m) {
+    case 1: return grouped ? launch_mg<1, 16>(A, elec, krf, energy, band, s) : launch_mg<1, 1>(A, elec, krf, energy, band, s);
+    case 2: return grouped ? launch_mg<2, 8>(A, elec, krf, energy, band, s) : launch_mg<2, 1>(A, elec, krf, energy, band, s);
+    case 4: return grouped ? launch_mg<4, 4>(A, elec, krf, energy, band, s) : launch_mg<4, 1>(A, elec, krf, energy, band, s);
+    default: return grouped ? launch_mg<8, 2>(A, elec, krf, energy, band, s) : launch_mg<8, 1>(A, elec, krf, energy, band, s);
+  }
+}
+
+// Chebyshev fit of the Ewald correction functions (see EW_DEG above), in
+// double precision on the host, converted to a power series in u.
+static double ew_gf(double w) {
+  if (w < 0.5) {  // series: (2/sqrt(pi)) sum_{n>=1} (-1)^(n+1) w^(n-1) 2n / (n! (2n+1))
+    double s = 0.0, term = 1.0;  // term = w^(n-1)/n!
+    for (int n = 1; n < 30; ++n) {
+      term = (n == 1) ? 1.0 : term * w / n;
+      s += ((n & 1) ? 1.0 : -1.0) * term * (2.0 * n) / (2.0 * n + 1.0);
+    }
+    return 2.0 / sqrt(M_PI) * s;
+  }
+  const double z = sqrt(w);
+  return erf(z) / (z * w) - 2.0 / sqrt(M_PI) * exp(-w) / w;
+}
+static double ew_gv(double w) {
+  if (w < 1e-12) return 2.0 / sqrt(M_PI);
+  const double z = sqrt(w);
+  return erf(z) / z;
+}
+static void ew_fit(double (*f)(double), double wmax, float* out /* EW_DEG+1, highest first */) {
+  const int N = EW_DEG + 1;
+  double c[EW_DEG + 1] = {0};
+  for (int k = 0; k < N; ++k) {
+    double acc = 0.0;
+    for (int j = 0; j < N; ++j) {
+      const double x = cos(M_PI * (j + 0.5) / N);
+      acc += f((x + 1.0) * 0.5 * wmax) * cos(M_PI * k * (j + 0.5) / N);
+    }
+    c[k] = acc * 2.0 / N;
+  }
+  c[0] *= 0.5;
+  // Chebyshev -> power series in u: T_{k+1} = 2u T_k - T_{k-1}
+  double Tprev[EW_DEG + 1] = {0}, Tcur[EW_DEG + 1] = {0}, p[EW_DEG + 1] = {0};
+  Tprev[0] = 1.0;            // T_0
+  Tcur[1] = 1.0;             // T_1
+  p[0] += c[0];
+  for (int i = 0; i <= EW_DEG; ++i) p[i] += c[1] * Tcur[i];
+  for (int k = 2; k < N; ++k) {
+    double Tn[EW_DEG + 1] = {0};
+    for (int i = 0; i <= EW_DEG; ++i) {
+      if (i > 0) Tn[i] += 2.0 * Tcur[i - 1];
+      Tn[i] -= Tprev[i];
+    }
+    for (int i = 0; i <= EW_DEG; ++i) {
+      p[i] += c[k] * Tn[i];
+      Tprev[i] = Tcur[i];
+      Tcur[i] = Tn[i];
+    }
+  }
+  for (int i = 0; i <= EW_DEG; ++i) out[i] = (float)p[EW_DEG - i];
+}
+
+// transposed index: items (entries or rows) sorted by j-cluster, stable
+static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clusters, DBuf<int32_t>& first,
+                                   DBuf<int32_t>& items, cudaStream_t s);
+
+static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+__global__ void k_first_sorted(const int32_t* __restrict__ keys, int64_t n, int64_t n_keys,
+                               int32_t* __restrict__ first) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int32_t prev = i == 0 ? -1 : keys[i - 1];
+  const int32_t cur = i == n ? (int32_t)n_keys : keys[i];
+  for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
+}
+
+static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clusters, DBuf<int32_t>& first,
+                                   DBuf<int32_t>& items, cudaStream_t s) {
+  DBuf<int32_t> vals, skeys;
+  cudaError_t e;
+  if ((e = first.alloc(n_clusters + 1, s)) || (e = items.alloc(n, s)) || (e = vals.alloc(n, s)) ||
+      (e = skeys.alloc(n, s)))
+    return e;
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) <= n_clusters) ++end_bit;
+  if (n > 0) {
+    count_launch(), k_iota<<<nb(n, 256), 256, 0, s>>>(vals.p, n);
+    if ((e = sort_pairs_i32(keys, skeys.p, vals.p, items.p, n, end_bit, s))) return e;
+  }
+  count_launch(), k_first_sorted<<<nb(n + 1, 256), 256, 0, s>>>(skeys.p, n, n_clusters, first.p);
+  vals.release(s);
+  skeys.release(s);
+  return cudaGetLastError();
+}
+
+}  // namespace nbx
+
+using namespace nbx;
+
+extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
+                         const double* charges, const int64_t* lj_type, const nbx_params_t* p,
+                         const double box[3], const int32_t* i_sel, int64_t n_sel, int32_t flags,
+                         double* f_out, double* e_out, int64_t* bad, void* stream) {
+  if (!lc || !grid || !p || !box || !f_out) {
+    set_error("nbx_force: null argument");
+    return NBX_ERR_PARAM;
+  }
+  nbx_list* l = const_cast<nbx_list*>(static_cast<const nbx_list*>(lc));
+  if (grid->m != l->m || grid->n_clusters != l->n_clusters) {
+    set_error("layout m=%d, grid m=%d, list m=%d must agree", l->m, grid->m, l->m);
+    return NBX_ERR_PARAM;
+  }
+  if (p->n_types < 1 || p->n_types > 64 || !p->lj_table) {
+    set_error("nbx_force: n_types must be in [1, 64]");
+    return NBX_ERR_PARAM;
+  }
+  if (p->elec < 0 || p->elec > 2) {
+    set_error("nbx_force: unknown electrostatics %d", p->elec);
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  ForceWork& wk = l->work;
+  const int m = l->m;
+  const int64_t ns = l->n_clusters * m;
+  const bool canonical = (i_sel != nullptr) || (flags & NBX_FORCE_CANONICAL);
+  const int64_t n_items = canonical ? l->n_rows : l->n_entries;
+  const int64_t n_work = canonical ? (i_sel ? n_sel : l->n_clusters) : l->n_groups;
+  Box bx;
+  for (int d = 0; d < 3; ++d) {
+    bx.L[d] = box[d];
+    bx.invL[d] = 1.0 / box[d];
+  }
+  cudaError_t e;
+  double* dtab = nullptr;
+  // workspace (cached across calls on this list)
+  if (wk.xyzq.n < ns) { if ((e = wk.xyzq.alloc(ns, s))) goto cuda_fail; }
+  if (wk.type.n < ns) { if ((e = wk.type.alloc(ns, s))) goto cuda_fail; }
+  if (wk.part_i.n < ns) { if ((e = wk.part_i.alloc(ns, s))) goto cuda_fail; }
+  if (wk.part_j.n < n_items * m) { if ((e = wk.part_j.alloc(n_items * m, s))) goto cuda_fail; }
+  if (wk.e_grp.n < 2 * n_work) { if ((e = wk.e_grp.alloc(2 * n_work + 2, s))) goto cuda_fail; }
+  if (wk.scalars.n < 4) { if ((e = wk.scalars.alloc(4, s))) goto cuda_fail; }
+  if (wk.lj.n < (int64_t)p->n_types * p->n_types) {
+    if ((e = wk.lj.alloc((int64_t)p->n_types * p->n_types, s))) goto cuda_fail;
+  }
+  if (!canonical && !wk.t_ready) {
+    if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s))) goto cuda_fail;
+    wk.t_ready = true;
+  }
+  if (canonical && !wk.tc_ready) {
+    if ((e = build_transpose(l->j.p, l->n_rows, l->n_clusters, wk.tc_first, wk.tc_items, s))) goto cuda_fail;
+    wk.tc_ready = true;
+  }
+  {
+    // LJ table -> device (tiny; stream-ordered through a temporary)
+    const int nt = p->n_types;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&dtab), sizeof(double) * 2 * nt * nt, s))) goto cuda_fail;
+    if ((e = cudaMemcpyAsync(dtab, p->lj_table, sizeof(double) * 2 * nt * nt, cudaMemcpyHostToDevice, s))) goto cuda_fail;
+    count_launch(), k_build_lj<<<nb(nt * nt, 64), 64, 0, s>>>(dtab, nt, p->r_cut * p->r_cut, p->shift_potential, wk.lj.p);
+    cudaFreeAsync(dtab, s);
+    dtab = nullptr;
+    // scalars: [0] = 0 (max displacement), [2..3] = ~0 (bad key)
+    const unsigned int init[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
+    if ((e = cudaMemcpyAsync(wk.scalars.p, init, sizeof(init), cudaMemcpyHostToDevice, s))) goto cuda_fail;
+    if (ns > 0)
+      count_launch(), k_gather<<<nb(ns, 256), 256, 0, s>>>(positions, charges, lj_type, grid->perm.p, grid->fill.p,
+                                           grid->cpos.p, grid->bbox.p, m, ns, bx, wk.xyzq.p, wk.type.p,
+                                           wk.scalars.p);
+    if (canonical) {
+      if (ns > 0 && (e = cudaMemsetAsync(wk.part_i.p, 0, sizeof(float4) * ns, s))) goto cuda_fail;
+      if (i_sel && n_items > 0 && (e = cudaMemsetAsync(wk.part_j.p, 0, sizeof(float4) * n_items * m, s))) goto cuda_fail;
+    }
+    ForceArgs A{};
+    A.n_work = n_work;
+    A.sel = canonical ? i_sel : nullptr;
+    A.grp_first = canonical ? nullptr : l->group_first.p;
+    A.grp_nmem = canonical ? nullptr : l->group_nmem.p;
+    A.ent_off = canonical ? l->offsets.p : l->ent_offsets.p;
+    A.ent_j = canonical ? l->j.p : l->ent_j.p;
+    A.ent_delta = canonical ? l->delta.p : l->ent_delta.p;
+    A.ent_slack = canonical ? l->slack.p : l->ent_slack.p;
+    A.ent_mask = canonical ? l->mask.p : l->ent_mask.p;
+    A.xyzq = wk.xyzq.p;
+    A.bbox = grid->bbox.p;
+    A.type = wk.type.p;
+    A.lj = wk.lj.p;
+    A.nt = nt;
+    A.part_i = wk.part_i.p;
+    A.part_j = wk.part_j.p;
+    A.e_grp = wk.e_grp.p;
+    A.scalars = wk.scalars.p;
+    const double rc = p->r_cut;
+    A.rc2 = (float)(rc * rc);
+    A.rc2d = rc * rc;
+    const bool ewald = p->elec == NBX_ELEC_EWALD;
+    double krf = 0.0, crf = 0.0;
+    if (p->elec == NBX_ELEC_REACTION_FIELD) {
+      krf = p->k_rf;
+      crf = p->c_rf;
+    } else if (p->elec == NBX_ELEC_CUTOFF) {
+      crf = p->shift_potential ? 1.0 / rc : 0.0;
+    }
+    A.krf = (float)krf;
+    A.k2rf = (float)(2.0 * krf);
+    A.crf = (float)crf;
+    A.coul = (float)p->coulomb_scale;
+    A.beta = (float)p->ewald_beta;
+    A.beta3 = (float)(p->ewald_beta * p->ewald_beta * p->ewald_beta);
+    A.ew_shift = p->shift_potential ? (float)(erfc(p->ewald_beta * rc) / rc) : 0.f;
+    if (ewald) {
+      // fit range: r^2 up to (r_c^2 + band) with margin
+      const double wmax = p->ewald_beta * p->ewald_beta * rc * rc * 1.02;
+      A.ew_a = (float)(2.0 / wmax * p->ewald_beta * p->ewald_beta);
+      ew_fit(ew_gf, wmax, A.ew_f);
+      ew_fit(ew_gv, wmax, A.ew_v);
+    }
+    A.slack_base = (float)(2.0 * rc + 1e-3);
+    double Lmax = fmax(box[0], fmax(box[1], box[2]));
+    A.band = (float)(64.0 * 5.96e-8 * (Lmax * rc + rc * rc));
+    for (int d = 0; d < 3; ++d) {
+      A.L[d] = (float)box[d];
+      A.invL[d] = (float)(1.0 / box[d]);
+    }
+    A.pos = positions;
+    A.perm = grid->perm.p;
+    A.box = bx;
+    const bool band = !ewald;
+    const bool use_krf = !ewald && krf != 0.0;
+    if ((e = launch_force(m, !canonical, A, ewald ? FE_EWALD : FE_RF, use_krf, (flags & NBX_FORCE_ENERGY) != 0, band, s)))
+      goto cuda_fail;
+    if (ns > 0)
+      count_launch(), k_reduce<<<nb(ns, 256), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
+                                           canonical ? wk.tc_items.p : wk.t_items.p, grid->perm.p,
+                                           grid->fill.p, ns, m, flags, f_out, wk.scalars.p + 1);
+    if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
+      // nothing else to produce
+    } else {
+      if (!(flags & NBX_FORCE_ENERGY)) {
+        count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, 0, nullptr, wk.scalars.p, bad);
+      } else {
+        count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, n_work, e_out, wk.scalars.p, bad);
+      }
+    }
+    if ((e = cudaGetLastError())) goto cuda_fail;
+  }
+  return NBX_OK;
+cuda_fail:
+  if (dtab) cudaFreeAsync(dtab, s);
+  set_error("nbx_force: %s", cudaGetErrorString(e));
+  return NBX_ERR_CUDA;
+}
+
+namespace nbx {
+// Exact scan of every admitted pair (kernels.py:184-187 semantics): first
+// coincident in-range pair in (i-cluster, row, a, b) order.
+__global__ void k_find_singular(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv,
+                                const uint64_t* __restrict__ mask, int64_t n_clusters, int m,
+                                ForceArgs A) {
+  const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (ci >= n_clusters) return;
+  for (int32_t row = offsets[ci]; row < offsets[ci + 1]; ++row) {
+    const uint64_t mk = mask[row];
+    for (int a = 0; a < m; ++a)
+      for (int b = 0; b < m; ++b)
+        if ((mk >> (a * m + b)) & 1ull) {
+          const int64_t si = ci * m + a, sj = (int64_t)jv[row] * m + b;
+          if (exact_inside(A, si, sj) < 0) {
+            record_bad(A.scalars, si, sj);
+            return;
+          }
+        }
+  }
+}
+}  // namespace nbx
+
+extern "C" int nbx_find_singular(const nbx_list_t* l, const nbx_grid_t* grid, const double* positions,
+                                 double r_cut, const double box[3], void* stream, int64_t out[2]) {
+  if (!l || !grid || !positions || !box || !out) {
+    set_error("nbx_find_singular: null argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  DBuf<unsigned int> sc;
+  unsigned int h[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
+  cudaError_t e;
+  ForceArgs A{};
+  A.pos = positions;
+  A.perm = grid->perm.p;
+  A.rc2d = r_cut * r_cut;
+  for (int d = 0; d < 3; ++d) {
+    A.box.L[d] = box[d];
+    A.box.invL[d] = 1.0 / box[d];
+  }
+  if ((e = sc.alloc(4, s))) goto fail;
+  if ((e = cudaMemcpyAsync(sc.p, h, 16, cudaMemcpyHostToDevice, s))) goto fail;
+  A.scalars = sc.p;
+  if (l->n_clusters > 0)
+    count_launch(), k_find_singular<<<nb(l->n_clusters, 128), 128, 0, s>>>(l->offsets.p, l->j.p, l->mask.p, l->n_clusters,
+                                                            l->m, A);
+  if ((e = cudaGetLastError())) goto fail;
+  if ((e = cudaMemcpyAsync(h, sc.p, 16, cudaMemcpyDeviceToHost, s))) goto fail;
+  if ((e = cudaStreamSynchronize(s))) goto fail;
+  sc.release(s);
+  {
+    const unsigned long long key = ((unsigned long long)h[3] << 32) | h[2];
+    if (key == ~0ull) {
+      out[0] = out[1] = -1;
+    } else {
+      out[0] = (int64_t)(key >> 32);
+      out[1] = (int64_t)(key & 0xffffffffull);
+    }
+  }
+  return NBX_OK;
+fail:
+  sc.release(s);
+  set_error("nbx_find_singular: %s", cudaGetErrorString(e));
+  return NBX_ERR_CUDA;
+}

@@ -1,0 +1,116 @@
+// Internal (device-resident) data structures of the nbx library.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "nbx.h"
+
+namespace nbx {
+
+// Device buffer with stream-ordered allocation.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  cudaError_t alloc(int64_t count, cudaStream_t s) {
+    release(s);
+    n = count;
+    if (count <= 0) return cudaSuccess;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, s);
+  }
+  void release(cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Clustered layout (gridder.ClusterGrid, gridder.py:23-66).
+struct Grid {
+  int64_t n = 0;        // particles
+  int m = 0;            // cluster size
+  int64_t cells = 0;    // columns per side
+  int64_t n_clusters = 0;
+  double L[3] = {0, 0, 0};
+  DBuf<int32_t> perm;           // (n_slots) slot -> original index
+  DBuf<int32_t> inverse_perm;   // (n)
+  DBuf<uint8_t> fill;           // (n_slots)
+  DBuf<int32_t> cell_of_cluster;// (n_clusters)
+  DBuf<int32_t> col_first;      // (cells^2 + 1) first cluster of each column
+  DBuf<double> cpos;            // (n_slots, 3) wrapped build-time positions
+  DBuf<double> bbox;            // (n_clusters, 6) lo xyz, hi xyz
+  DBuf<int8_t> nreal;           // (n_clusters) real (non-filler) slots
+  int64_t n_slots() const { return n_clusters * m; }
+};
+
+// Force workspace cached on a list (lazily sized on first force call).
+struct ForceWork {
+  DBuf<float4> xyzq;      // (n_slots) cluster-local FP32 positions (near-build image) + charge
+  DBuf<int32_t> type;     // (n_slots)
+  DBuf<float4> part_i;    // (n_slots) i-side partial forces
+  DBuf<float4> part_j;    // (n_entries * m) or (n_rows * m) j-side partials
+  DBuf<double> e_grp;     // (2 * n_work_groups) per-group energies
+  DBuf<unsigned int> scalars;   // [0] max displacement bits, [1..2] bad key (u64)
+  DBuf<float4> lj;        // (t*t) {6 c6, 12 c12, shift_lj, 0}
+  int64_t lj_types = -1;
+  // transposed index: entries (or rows) sorted by j-cluster
+  DBuf<int32_t> t_first;  // (n_clusters + 1)
+  DBuf<int32_t> t_items;  // (n_entries)
+  bool t_ready = false;
+  DBuf<int32_t> tc_first; // canonical-row transpose
+  DBuf<int32_t> tc_items;
+  bool tc_ready = false;
+};
+
+// Cluster-pair list (pairlist.ClusterPairList, pairlist.py:27-94) plus the
+// grouped force layout: G = 16/m consecutive clusters of one column form a
+// group; an entry is (group, j-cluster) with the masks of every member.
+struct List {
+  int m = 0;
+  int G = 0;
+  int64_t n_clusters = 0;
+  int64_t n_rows = 0;
+  int64_t n_groups = 0;
+  int64_t n_entries = 0;
+  double r_list = 0.0;
+  double L[3] = {0, 0, 0};
+  // canonical CSR
+  DBuf<int32_t> offsets;    // (n_clusters + 1)
+  DBuf<int32_t> j;          // (n_rows)
+  DBuf<uint64_t> mask;      // (n_rows)
+  DBuf<float4> delta;       // (n_rows) j-local -> i-local offset (image included)
+  DBuf<float> slack;        // (n_rows) min_d (L - ext_i - ext_j)
+  DBuf<int32_t> row_entry;  // (n_rows) entry holding this row
+  // groups / entries
+  DBuf<int32_t> group_first;  // (n_groups) first member cluster
+  DBuf<int32_t> group_nmem;   // (n_groups)
+  DBuf<int32_t> ent_offsets;  // (n_groups + 1)
+  DBuf<int32_t> ent_j;        // (n_entries)
+  DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset
+  DBuf<float> ent_slack;      // (n_entries)
+  DBuf<uint64_t> ent_mask;    // (n_entries * W), W = 2 for m == 8 else 1
+  // reference super layout (on demand)
+  int64_t super_size = 0, super_groups = 0, super_entries = 0;
+  DBuf<int32_t> super_offsets, super_j, super_pair;
+  ForceWork work;
+  int mask_words() const { return m == 8 ? 2 : 1; }
+};
+
+inline cudaStream_t to_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// count of kernels this library launched (nbx_launch_count)
+void count_launch(int64_t k = 1);
+// k_force event timing (nbx_timing_*)
+bool timing_enabled();
+void timing_record(cudaEvent_t a, cudaEvent_t b);
+
+// exclusive scan helpers (CUB), defined in scan.cu
+cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
+cudaError_t sort_pairs_i32(const int32_t* keys_in, int32_t* keys_out, const int32_t* vals_in,
+                           int32_t* vals_out, int64_t n, int end_bit, cudaStream_t s);
+
+}  // namespace nbx
+
+struct nbx_grid : nbx::Grid {};
+struct nbx_list : nbx::List {};

@@ -1,0 +1,893 @@
+// Cluster-pair search, pruning, statistics and list layouts.
+//
+// Replaces pairlist.build_pair_list (pairlist.py:147-217), _build_masks
+// (:106-112), prune_pair_list (:242-282), _build_super_layout (:115-144) and
+// interaction_stats/_count_within (:303-346) of
+// /root/reference/pkg/src/clustermd.  Every inclusion decision is the
+// reference's FP64 expression in the reference's operation order
+// (common.cuh), so the canonical list is bit-identical (set-identical rows
+// and masks, same CSR order).
+//
+// The search runs per GROUP: G = 16/m consecutive clusters of one x/y column
+// (a z-stack).  One warp enumerates the j-clusters of the columns within
+// r_list of the group (ascending cluster index, so CSR order falls out), tests
+// each against every member with the exact AABB gap, and emits in one pass
+//   * the canonical rows (ci, cj >= ci) -- the parity object, and
+//   * the grouped force layout: one ENTRY per (group, cj) carrying the
+//     m x m masks of all members, a periodic shift and a slack for the
+//     single-shift validity test (force.cu).
+// Two passes (count, write) around a scan keep the output deterministic.
+#include <cub/cub.cuh>
+#include <utility>
+
+#include "internal.cuh"
+
+namespace nbx {
+
+struct Ranges {
+  int64_t lo[2], hi[2];
+  int n;
+};
+
+// Columns (along one axis) that can hold clusters within r of [lo, hi]:
+// nominal column index range padded by one column each side (binning can
+// place a particle a few ulp outside its nominal column), wrapped and split
+// into at most two ascending segments.
+__device__ __forceinline__ Ranges col_ranges(double lo, double hi, double r, double w, int64_t cells) {
+  Ranges R;
+  int64_t a = (int64_t)floor((lo - r) / w) - 1;
+  int64_t b = (int64_t)floor((hi + r) / w) + 1;
+  if (b - a + 1 >= cells) {
+    R.n = 1; R.lo[0] = 0; R.hi[0] = cells - 1;
+    return R;
+  }
+  int64_t am = ((a % cells) + cells) % cells;
+  int64_t bm = ((b % cells) + cells) % cells;
+  if (am <= bm) {
+    R.n = 1; R.lo[0] = am; R.hi[0] = bm;
+  } else {
+    R.n = 2; R.lo[0] = 0; R.hi[0] = bm; R.lo[1] = am; R.hi[1] = cells - 1;
+  }
+  return R;
+}
+
+__device__ __forceinline__ uint64_t row_mask(int m, int nr_i, int nr_j, bool diag) {
+  uint64_t jb = (nr_j >= 64) ? ~0ull : ((1ull << nr_j) - 1ull);
+  uint64_t mk = 0;
+  for (int a = 0; a < nr_i; ++a) {
+    uint64_t row = jb;
+    if (diag) row &= ~((2ull << a) - 1ull);  // b > a only (strict upper triangle)
+    mk |= row << (a * m);
+  }
+  return mk;
+}
+
+// Periodic image of the j-cluster relative to the i-side box (bi) and the
+// FP32 offset that maps j-local coordinates (relative to the j-cluster's
+// bbox low corner) into the i-side frame (origin `oi`):
+//   delta = lo_j + n L - oi  (FP64, rounded once),
+// plus slack = min_d (L - ext_i - ext_j) for the single-image validity test.
+__device__ __forceinline__ void image_delta(const double* bi, const double* oi, const double* bj,
+                                            const Box& box, float4* delta, float* slack) {
+  double dl[3];
+  double sl = 1e300;
+  for (int d = 0; d < 3; ++d) {
+    const double ci = 0.5 * (bi[d] + bi[3 + d]);
+    const double cj = 0.5 * (bj[d] + bj[3 + d]);
+    double n = rint((ci - cj) * box.invL[d]);
+    n = fmin(1.0, fmax(-1.0, n));
+    dl[d] = (bj[d] + n * box.L[d]) - oi[d];
+    const double s = box.L[d] - (bi[3 + d] - bi[d]) - (bj[3 + d] - bj[d]);
+    sl = fmin(sl, s);
+  }
+  *delta = make_float4((float)dl[0], (float)dl[1], (float)dl[2], 0.f);
+  *slack = (float)sl;
+}
+
+constexpr int SEARCH_WARPS = 4;
+constexpr int GMAX = 16;
+
+struct SearchOut {
+  // counting pass
+  int32_t* row_count;   // (n_clusters)
+  int32_t* ent_count;   // (n_groups)
+  // writing pass
+  const int32_t* offsets;
+  const int32_t* ent_offsets;
+  int32_t* j;
+  uint64_t* mask;
+  float4* delta;
+  float* slack;
+  int32_t* row_entry;
+  int32_t* ent_j;
+  float4* ent_delta;
+  float* ent_slack;
+  uint64_t* ent_mask;
+};
+
+template <bool WRITE>
+__global__ void __launch_bounds__(SEARCH_WARPS * 32)
+k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
+         int64_t n_groups, int m, int G, const double* __restrict__ bbox,
+         const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first, int64_t cells,
+         Box box, double r_list, SearchOut out) {
+  __shared__ double s_bb[SEARCH_WARPS][GMAX][6];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.x * (int64_t)SEARCH_WARPS + w;
+  if (g >= n_groups) return;
+  const int32_t first = group_first[g];
+  const int nmem = group_nmem[g];
+  if (lane < nmem)
+    for (int d = 0; d < 6; ++d) s_bb[w][lane][d] = bbox[6 * (int64_t)(first + lane) + d];
+  __syncwarp();
+  double gb[6];  // group AABB
+  for (int d = 0; d < 3; ++d) {
+    gb[d] = s_bb[w][0][d];
+    gb[3 + d] = s_bb[w][0][3 + d];
+    for (int k = 1; k < nmem; ++k) {
+      gb[d] = fmin(gb[d], s_bb[w][k][d]);
+      gb[3 + d] = fmax(gb[3 + d], s_bb[w][k][3 + d]);
+    }
+  }
+  const double r2 = __dmul_rn(r_list, r_list);
+  // conservative FP64-free prefilter margin (exact test follows)
+  const float r2_pre = (float)(r2 * (1.0 + 1e-4)) + 1e-6f;
+  const double wx = box.L[0] / (double)cells, wy = box.L[1] / (double)cells;
+  Ranges RX = col_ranges(gb[0], gb[3], r_list, wx, cells);
+  Ranges RY = col_ranges(gb[1], gb[4], r_list, wy, cells);
+
+  int32_t cnt = 0;   // lane k < nmem: rows emitted for member k
+  int32_t ecnt = 0;  // entries emitted (uniform)
+  int32_t row_base = 0, ent_base = 0;
+  if (WRITE) {
+    if (lane < nmem) row_base = out.offsets[first + lane];
+    ent_base = out.ent_offsets[g];
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  const int W = (m == 8) ? 2 : 1;
+
+  for (int sx = 0; sx < RX.n; ++sx) {
+    for (int64_t ix = RX.lo[sx]; ix <= RX.hi[sx]; ++ix) {
+      for (int sy = 0; sy < RY.n; ++sy) {
+        const int32_t c0 = col_first[ix * cells + RY.lo[sy]];
+        const int32_t c1 = col_first[ix * cells + RY.hi[sy] + 1];
+        int32_t start = c0 > first ? c0 : first;
+        for (int32_t base = start; base < c1; base += 32) {
+          const int32_t cj = base + lane;
+          uint32_t bits = 0;
+          double bj[6];
+          if (cj < c1) {
+            for (int d = 0; d < 6; ++d) bj[d] = bbox[6 * (int64_t)cj + d];
+            // prefilter on the group box (FP32, conservative)
+            float pre = 0.f;
+            for (int d = 0; d < 3; ++d) {
+              float gg = (float)gap_1d(gb[d], gb[3 + d], bj[d], bj[3 + d], box.L[d]);
+              pre += gg * gg;
+            }
+            if (pre <= r2_pre) {
+              for (int k = 0; k < nmem; ++k) {
+                if (cj >= first + k && gap_sq(s_bb[w][k], bj, box) <= r2) bits |= 1u << k;
+              }
+            }
+          }
+          const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
+          if (eb == 0) continue;
+          int ent_pos = ent_base + ecnt + __popc(eb & lt);
+          uint64_t emask[2] = {0ull, 0ull};
+          float4 e_delta = make_float4(0.f, 0.f, 0.f, 0.f);
+          float e_slack = 0.f;
+          if (WRITE && bits) image_delta(gb, s_bb[w][0], bj, box, &e_delta, &e_slack);
+          for (int k = 0; k < nmem; ++k) {
+            const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+            if (!b) continue;
+            if (WRITE) {
+              const int32_t before = __shfl_sync(0xffffffffu, cnt, k);
+              const int32_t rbase = __shfl_sync(0xffffffffu, row_base, k);
+              if ((bits >> k) & 1u) {
+                const int32_t ci = first + k;
+                const int64_t row = (int64_t)rbase + before + __popc(b & lt);
+                const uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
+                out.j[row] = cj;
+                out.mask[row] = mk;
+                float4 rdelta;
+                float rslack;
+                image_delta(s_bb[w][k], s_bb[w][k], bj, box, &rdelta, &rslack);
+                out.delta[row] = rdelta;
+                out.slack[row] = rslack;
+                out.row_entry[row] = ent_pos;
+                if (W == 2) emask[k] = mk;
+                else emask[0] |= mk << (k * m * m);
+              }
+            }
+            if (lane == k) cnt += __popc(b);
+          }
+          if (WRITE && bits) {
+            out.ent_j[ent_pos] = cj;
+            out.ent_delta[ent_pos] = e_delta;
+            out.ent_slack[ent_pos] = e_slack;
+            out.ent_mask[(int64_t)ent_pos * W] = emask[0];
+            if (W == 2) out.ent_mask[(int64_t)ent_pos * W + 1] = emask[1];
+          }
+          ecnt += __popc(eb);
+        }
+      }
+    }
+  }
+  if (!WRITE) {
+    if (lane < nmem) out.row_count[first + lane] = cnt;
+    if (lane == 0) out.ent_count[g] = ecnt;
+  }
+}
+
+__global__ void k_groups(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
+                         const int32_t* __restrict__ grp_col_first, int32_t* __restrict__ group_first,
+                         int32_t* __restrict__ group_nmem) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const int32_t f = col_first[c], ncl = col_first[c + 1] - f;
+  const int32_t g0 = grp_col_first[c];
+  for (int32_t t = 0; t * G < ncl; ++t) {
+    group_first[g0 + t] = f + t * G;
+    group_nmem[g0 + t] = min(G, ncl - t * G);
+  }
+}
+
+__global__ void k_groups_per_col(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
+                                 int32_t* __restrict__ ng) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < n_cols) ng[c] = (col_first[c + 1] - col_first[c] + G - 1) / G;
+  if (c == n_cols) ng[c] = 0;
+}
+
+// ---------------------------------------------------------------- exact pair decisions
+// d2 of slots (si, sj) of `pos` with the reference's min image
+// (model.py:159-172) and einsum order (pairlist.py:236).
+__device__ __forceinline__ double d2_exact(const double* __restrict__ pos, int64_t si, int64_t sj,
+                                           const Box& box) {
+  const double dx = min_image_np(__dsub_rn(pos[3 * si], pos[3 * sj]), box.L[0], box.invL[0]);
+  const double dy = min_image_np(__dsub_rn(pos[3 * si + 1], pos[3 * sj + 1]), box.L[1], box.invL[1]);
+  const double dz = min_image_np(__dsub_rn(pos[3 * si + 2], pos[3 * sj + 2]), box.L[2], box.invL[2]);
+  return d2_einsum(dx, dy, dz);
+}
+
+// FP32 estimate of the same d2 (any image convention gives the same minimum
+// for |d| < L/2; the margin covers FP32 rounding).
+__device__ __forceinline__ float d2_fast(const double* __restrict__ pos, int64_t si, int64_t sj,
+                                         const float Lf[3], const float iLf[3]) {
+  float s = 0.f;
+  for (int d = 0; d < 3; ++d) {
+    float v = (float)__dsub_rn(pos[3 * si + d], pos[3 * sj + d]);
+    v = v - Lf[d] * rintf(v * iLf[d]);
+    s += v * v;
+  }
+  return s;
+}
+
+// Three-way decision d2 <= r2: the FP32 estimate decides unless it is inside
+// +-1e-4 relative of r2, then the exact FP64 replay decides.
+__device__ __forceinline__ bool within_exact(const double* __restrict__ pos, int64_t si, int64_t sj,
+                                             const Box& box, double r2, float lo, float hi,
+                                             const float Lf[3], const float iLf[3]) {
+  const float f = d2_fast(pos, si, sj, Lf, iLf);
+  if (f < lo) return true;
+  if (f > hi) return false;
+  return d2_exact(pos, si, sj, box) <= r2;
+}
+
+constexpr int ROWS_WARPS = 4;
+
+// Prune (pairlist.py:242-282): one warp per i-cluster, lanes over its rows.
+// Removed rows clear their member bits in the (copied) entry masks; kept rows
+// mark their entry alive.
+__global__ void __launch_bounds__(ROWS_WARPS * 32)
+k_prune(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv,
+        const uint64_t* __restrict__ mask, const int32_t* __restrict__ row_entry,
+        int64_t n_clusters, int m, int G, const double* __restrict__ pos, Box box, double r2,
+        const int32_t* __restrict__ cell_of_cluster, const int32_t* __restrict__ col_first,
+        int32_t* __restrict__ keep, uint64_t* __restrict__ ent_mask, int32_t* __restrict__ ent_alive) {
+  const int64_t ci = blockIdx.x * (int64_t)ROWS_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (ci >= n_clusters) return;
+  const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
+  const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
+  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
+  const int k = (int)((ci - col_first[cell_of_cluster[ci]]) % G);
+  const int W = (m == 8) ? 2 : 1;
+  for (int32_t row = offsets[ci] + lane; row < offsets[ci + 1]; row += 32) {
+    const int32_t cj = jv[row];
+    const uint64_t mk = mask[row];
+    bool kp = (cj == ci);
+    if (!kp) {
+      for (int a = 0; a < m && !kp; ++a)
+        for (int b = 0; b < m; ++b) {
+          if (!((mk >> (a * m + b)) & 1ull)) continue;
+          if (within_exact(pos, ci * m + a, (int64_t)cj * m + b, box, r2, lo, hi, Lf, iLf)) {
+            kp = true;
+            break;
+          }
+        }
+    }
+    keep[row] = kp ? 1 : 0;
+    const int32_t e = row_entry[row];
+    if (kp) {
+      ent_alive[e] = 1;
+    } else if (mk) {
+      if (W == 2) {
+        atomicAnd((unsigned long long*)&ent_mask[(int64_t)e * 2 + k], 0ull);
+      } else {
+        atomicAnd((unsigned long long*)&ent_mask[e], ~(unsigned long long)(mk << (k * m * m)));
+      }
+    }
+  }
+}
+
+// interaction_stats (pairlist.py:323-346): admitted + within-r_cut counts.
+__global__ void __launch_bounds__(ROWS_WARPS * 32)
+k_count_within(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv,
+               const uint64_t* __restrict__ mask, int64_t n_clusters, int m,
+               const double* __restrict__ pos, Box box, double r2,
+               unsigned long long* __restrict__ counts) {
+  const int64_t ci = blockIdx.x * (int64_t)ROWS_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (ci >= n_clusters) return;
+  const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
+  const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
+  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
+  unsigned long long adm = 0, win = 0;
+  for (int32_t row = offsets[ci] + lane; row < offsets[ci + 1]; row += 32) {
+    const int32_t cj = jv[row];
+    const uint64_t mk = mask[row];
+    adm += __popcll(mk);
+    for (int a = 0; a < m; ++a)
+      for (int b = 0; b < m; ++b)
+        if ((mk >> (a * m + b)) & 1ull)
+          win += within_exact(pos, ci * m + a, (int64_t)cj * m + b, box, r2, lo, hi, Lf, iLf);
+  }
+  for (int o = 16; o; o >>= 1) {
+    adm += __shfl_xor_sync(0xffffffffu, adm, o);
+    win += __shfl_xor_sync(0xffffffffu, win, o);
+  }
+  if (lane == 0 && (adm || win)) {
+    atomicAdd(&counts[0], adm);
+    atomicAdd(&counts[1], win);
+  }
+}
+
+// ---------------------------------------------------------------- compaction helpers
+__global__ void k_new_offsets(const int32_t* __restrict__ old_off, int64_t n,
+                              const int32_t* __restrict__ scan, int32_t* __restrict__ new_off) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i <= n) new_off[i] = scan[old_off[i]];
+}
+
+__global__ void k_compact_rows(int64_t n_rows, const int32_t* __restrict__ keep,
+                               const int32_t* __restrict__ scan, const int32_t* __restrict__ ent_scan,
+                               const int32_t* j, const uint64_t* mask, const float4* delta,
+                               const float* slack, const int32_t* row_entry, int32_t* j2,
+                               uint64_t* mask2, float4* delta2, float* slack2, int32_t* row_entry2) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows || !keep[r]) return;
+  const int32_t p = scan[r];
+  j2[p] = j[r];
+  mask2[p] = mask[r];
+  delta2[p] = delta[r];
+  slack2[p] = slack[r];
+  row_entry2[p] = ent_scan[row_entry[r]];
+}
+
+__global__ void k_compact_entries(int64_t n_ent, int W, const int32_t* __restrict__ alive,
+                                  const int32_t* __restrict__ scan, const int32_t* ej,
+                                  const float4* edelta, const float* eslack, const uint64_t* emask,
+                                  int32_t* ej2, float4* edelta2, float* eslack2, uint64_t* emask2) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_ent || !alive[e]) return;
+  const int32_t p = scan[e];
+  ej2[p] = ej[e];
+  edelta2[p] = edelta[e];
+  eslack2[p] = eslack[e];
+  for (int w = 0; w < W; ++w) emask2[(int64_t)p * W + w] = emask[e * W + w];
+}
+
+// CSR "first" array from keys sorted ascending: first[c] = lower_bound(c).
+__global__ void k_first_from_sorted(const int32_t* __restrict__ keys, int64_t n, int64_t n_keys,
+                                    int32_t* __restrict__ first) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int32_t prev = i == 0 ? -1 : keys[i - 1];
+  const int32_t cur = i == n ? (int32_t)n_keys : keys[i];
+  for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
+}
+
+// super layout (pairlist.py:115-144): rows sorted by (ci / size, cj)
+__global__ void k_row_ci(const int32_t* __restrict__ offsets, int64_t n_clusters, int32_t* __restrict__ ci_of_row) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_clusters) return;
+  for (int32_t r = offsets[c]; r < offsets[c + 1]; ++r) ci_of_row[r] = (int32_t)c;
+}
+
+__global__ void k_super_keys(const int32_t* __restrict__ ci_of_row, const int32_t* __restrict__ j,
+                             int64_t n_rows, int size, int64_t n_clusters, uint64_t* __restrict__ keys,
+                             int32_t* __restrict__ vals) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  keys[r] = (uint64_t)(ci_of_row[r] / size) * (uint64_t)n_clusters + (uint64_t)j[r];
+  vals[r] = (int32_t)r;
+}
+
+__global__ void k_super_heads(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ head) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+  if (i == n) head[i] = 0;
+}
+
+__global__ void k_super_fill(const uint64_t* __restrict__ keys, const int32_t* __restrict__ rows,
+                             const int32_t* __restrict__ head_scan, const int32_t* __restrict__ ci_of_row,
+                             int64_t n, int size, int64_t n_clusters, int32_t* __restrict__ sj,
+                             int32_t* __restrict__ spair, int32_t* __restrict__ group_count) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool head = (i == 0 || keys[i] != keys[i - 1]);
+  const int32_t e = head_scan[i + 1] - 1;  // inclusive head count - 1
+  const int32_t r = rows[i];
+  const int32_t ci = ci_of_row[r];
+  if (head) {
+    sj[e] = (int32_t)(keys[i] % (uint64_t)n_clusters);
+    atomicAdd(&group_count[ci / size], 1);
+  }
+  spair[(int64_t)e * size + (ci % size)] = r;
+}
+
+
+// ---------------------------------------------------------------- entry order
+// Within each group, order entries by member-presence pattern (stable, then
+// by j-cluster) so that the 32/m entries a force-kernel warp handles per
+// iteration share their members: the kernel skips a member only when no
+// entry of the iteration has it, so homogeneous iterations waste no lanes.
+constexpr int SORT_SMEM = 1024;
+
+__device__ __forceinline__ uint32_t entry_pattern(const uint64_t* emask, int64_t e, int m, int G) {
+  const int W = (m == 8) ? 2 : 1;
+  uint32_t pat = 0;
+  const int mm = m * m;
+  for (int k = 0; k < G; ++k) {
+    uint64_t bits;
+    if (W == 2) bits = emask[e * 2 + k];
+    else bits = (emask[e] >> (k * mm)) & (mm == 64 ? ~0ull : ((1ull << mm) - 1ull));
+    pat |= (bits != 0ull ? 1u : 0u) << k;
+  }
+  return pat;
+}
+
+__global__ void __launch_bounds__(ROWS_WARPS * 32)
+k_entry_order(const int32_t* __restrict__ ent_off, int64_t n_groups, const uint64_t* __restrict__ emask,
+              int m, int G, int32_t* __restrict__ newpos) {
+  __shared__ uint32_t s_key[ROWS_WARPS][SORT_SMEM];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.x * (int64_t)ROWS_WARPS + w;
+  if (g >= n_groups) return;
+  const int32_t e0 = ent_off[g], n = ent_off[g + 1] - e0;
+  if (n > SORT_SMEM) {  // very long lists (needle clusters): keep j order
+    for (int t = lane; t < n; t += 32) newpos[e0 + t] = e0 + t;
+    return;
+  }
+  for (int t = lane; t < n; t += 32) s_key[w][t] = entry_pattern(emask, e0 + t, m, G);
+  __syncwarp();
+  for (int t = lane; t < n; t += 32) {
+    const uint32_t k = s_key[w][t];
+    int32_t rank = 0;
+    for (int u = 0; u < n; ++u) {
+      const uint32_t ku = s_key[w][u];
+      rank += (ku < k) || (ku == k && u < t);
+    }
+    newpos[e0 + t] = e0 + rank;
+  }
+}
+
+__global__ void k_permute_entries(int64_t n_ent, int W, const int32_t* __restrict__ newpos, const int32_t* ej,
+                                  const float4* edelta, const float* eslack, const uint64_t* emask, int32_t* ej2,
+                                  float4* edelta2, float* eslack2, uint64_t* emask2) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_ent) return;
+  const int32_t p = newpos[e];
+  ej2[p] = ej[e];
+  edelta2[p] = edelta[e];
+  eslack2[p] = eslack[e];
+  for (int w = 0; w < W; ++w) emask2[(int64_t)p * W + w] = emask[e * W + w];
+}
+
+__global__ void k_remap_rows(int64_t n_rows, const int32_t* __restrict__ newpos, int32_t* __restrict__ row_entry) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < n_rows) row_entry[r] = newpos[row_entry[r]];
+}
+
+static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// reorder a freshly built / pruned list's entries (see k_entry_order)
+static cudaError_t order_entries(List* l, cudaStream_t s) {
+  const int64_t ne = l->n_entries;
+  if (ne == 0 || l->n_groups == 0) return cudaSuccess;
+  const int W = l->mask_words();
+  DBuf<int32_t> newpos, ej;
+  DBuf<float4> ed;
+  DBuf<float> es;
+  DBuf<uint64_t> em;
+  cudaError_t e;
+  if ((e = newpos.alloc(ne, s)) || (e = ej.alloc(ne, s)) || (e = ed.alloc(ne, s)) || (e = es.alloc(ne, s)) ||
+      (e = em.alloc(ne * W, s)))
+    return e;
+  count_launch(3);
+  k_entry_order<<<nb(l->n_groups, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(l->ent_offsets.p, l->n_groups,
+                                                                         l->ent_mask.p, l->m, l->G, newpos.p);
+  k_permute_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, newpos.p, l->ent_j.p, l->ent_delta.p, l->ent_slack.p,
+                                                 l->ent_mask.p, ej.p, ed.p, es.p, em.p);
+  if (l->n_rows) k_remap_rows<<<nb(l->n_rows, 256), 256, 0, s>>>(l->n_rows, newpos.p, l->row_entry.p);
+  std::swap(l->ent_j, ej);
+  std::swap(l->ent_delta, ed);
+  std::swap(l->ent_slack, es);
+  std::swap(l->ent_mask, em);
+  newpos.release(s); ej.release(s); ed.release(s); es.release(s); em.release(s);
+  return cudaGetLastError();
+}
+
+}  // namespace nbx
+
+using namespace nbx;
+
+static void list_release(nbx_list* l, cudaStream_t s) {
+  l->offsets.release(s); l->j.release(s); l->mask.release(s); l->delta.release(s);
+  l->slack.release(s); l->row_entry.release(s); l->group_first.release(s);
+  l->group_nmem.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
+  l->ent_delta.release(s); l->ent_slack.release(s); l->ent_mask.release(s);
+  l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
+  ForceWork& w = l->work;
+  w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
+  w.e_grp.release(s); w.scalars.release(s); w.lj.release(s); w.t_first.release(s);
+  w.t_items.release(s); w.tc_first.release(s); w.tc_items.release(s);
+}
+
+extern "C" void nbx_list_free(nbx_list_t* l) {
+  if (!l) return;
+  list_release(l, 0);
+  delete l;
+}
+
+static Box make_box(const double L[3]) {
+  Box b;
+  for (int d = 0; d < 3; ++d) {
+    b.L[d] = L[d];
+    b.invL[d] = 1.0 / L[d];
+  }
+  return b;
+}
+
+#define TRY(x)                                                      \
+  do {                                                              \
+    cudaError_t e_ = (x);                                           \
+    if (e_ != cudaSuccess) {                                        \
+      set_error("%s:%d %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      goto fail;                                                    \
+    }                                                               \
+  } while (0)
+
+extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], double r_list,
+                                  void* stream, nbx_list_t** out) {
+  if (!grid || !box || !out) {
+    set_error("nbx_pairlist_build: null argument");
+    return NBX_ERR_PARAM;
+  }
+  if (!(r_list > 0.0)) {
+    set_error("r_list must be positive, got %g", r_list);
+    return NBX_ERR_PARAM;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (box[d] < 2.0 * r_list) {
+      set_error("every box edge must be >= 2*r_list=%g for the single-image convention", 2.0 * r_list);
+      return NBX_ERR_PARAM;
+    }
+  cudaStream_t s = to_stream(stream);
+  nbx_list* l = new nbx_list();
+  *out = nullptr;
+  const int m = grid->m, G = 16 / grid->m;
+  const int64_t nc = grid->n_clusters, n_cols = grid->cells * grid->cells;
+  l->m = m;
+  l->G = G;
+  l->n_clusters = nc;
+  l->r_list = r_list;
+  for (int d = 0; d < 3; ++d) l->L[d] = box[d];
+  Box bx = make_box(box);
+  DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
+  int32_t h[2] = {0, 0};
+  SearchOut so{};
+  TRY(ng.alloc(n_cols + 1, s));
+  TRY(grp_col_first.alloc(n_cols + 1, s));
+  count_launch(), k_groups_per_col<<<nb(n_cols + 1, 256), 256, 0, s>>>(grid->col_first.p, n_cols, G, ng.p);
+  TRY(exclusive_scan_i32(ng.p, grp_col_first.p, n_cols + 1, s));
+  TRY(cudaMemcpyAsync(&h[0], grp_col_first.p + n_cols, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaStreamSynchronize(s));
+  l->n_groups = h[0];
+  TRY(l->group_first.alloc(l->n_groups, s));
+  TRY(l->group_nmem.alloc(l->n_groups, s));
+  if (n_cols > 0)
+    count_launch(), k_groups<<<nb(n_cols, 256), 256, 0, s>>>(grid->col_first.p, n_cols, G, grp_col_first.p,
+                                             l->group_first.p, l->group_nmem.p);
+  TRY(row_count.alloc(nc + 1, s));
+  TRY(ent_count.alloc(l->n_groups + 1, s));
+  TRY(cudaMemsetAsync(row_count.p, 0, 4 * (nc + 1), s));
+  TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
+  so.row_count = row_count.p;
+  so.ent_count = ent_count.p;
+  if (l->n_groups > 0)
+    count_launch(), k_search<false><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->nreal.p,
+        grid->col_first.p, grid->cells, bx, r_list, so);
+  TRY(cudaGetLastError());
+  TRY(l->offsets.alloc(nc + 1, s));
+  TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
+  TRY(exclusive_scan_i32(row_count.p, l->offsets.p, nc + 1, s));
+  TRY(exclusive_scan_i32(ent_count.p, l->ent_offsets.p, l->n_groups + 1, s));
+  TRY(cudaMemcpyAsync(&h[0], l->offsets.p + nc, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaMemcpyAsync(&h[1], l->ent_offsets.p + l->n_groups, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaStreamSynchronize(s));
+  l->n_rows = h[0];
+  l->n_entries = h[1];
+  TRY(l->j.alloc(l->n_rows, s));
+  TRY(l->mask.alloc(l->n_rows, s));
+  TRY(l->delta.alloc(l->n_rows, s));
+  TRY(l->slack.alloc(l->n_rows, s));
+  TRY(l->row_entry.alloc(l->n_rows, s));
+  TRY(l->ent_j.alloc(l->n_entries, s));
+  TRY(l->ent_delta.alloc(l->n_entries, s));
+  TRY(l->ent_slack.alloc(l->n_entries, s));
+  TRY(l->ent_mask.alloc(l->n_entries * l->mask_words(), s));
+  so.offsets = l->offsets.p;
+  so.ent_offsets = l->ent_offsets.p;
+  so.j = l->j.p;
+  so.mask = l->mask.p;
+  so.delta = l->delta.p;
+  so.slack = l->slack.p;
+  so.row_entry = l->row_entry.p;
+  so.ent_j = l->ent_j.p;
+  so.ent_delta = l->ent_delta.p;
+  so.ent_slack = l->ent_slack.p;
+  so.ent_mask = l->ent_mask.p;
+  if (l->n_groups > 0)
+    count_launch(), k_search<true><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->nreal.p,
+        grid->col_first.p, grid->cells, bx, r_list, so);
+  TRY(cudaGetLastError());
+  TRY(order_entries(l, s));
+  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s);
+  *out = l;
+  return NBX_OK;
+fail:
+  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s);
+  nbx_list_free(l);
+  return NBX_ERR_CUDA;
+}
+
+extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
+                                  const double* pos, const double box[3], void* stream,
+                                  nbx_list_t** out) {
+  if (!in || !grid || !pos || !box || !out) {
+    set_error("nbx_pairlist_prune: null argument");
+    return NBX_ERR_PARAM;
+  }
+  if (grid->n_clusters != in->n_clusters || grid->m != in->m) {
+    set_error("nbx_pairlist_prune: grid does not match the list");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  nbx_list* l = new nbx_list();
+  *out = nullptr;
+  l->m = in->m;
+  l->G = in->G;
+  l->n_clusters = in->n_clusters;
+  l->n_groups = in->n_groups;
+  l->r_list = in->r_list;
+  for (int d = 0; d < 3; ++d) l->L[d] = in->L[d];
+  const int W = in->mask_words();
+  const int64_t nr = in->n_rows, ne = in->n_entries, nc = in->n_clusters;
+  Box bx = make_box(box);
+  DBuf<int32_t> keep, scan, alive, escan;
+  DBuf<uint64_t> emask;
+  int32_t h[2] = {0, 0};
+  TRY(keep.alloc(nr + 1, s));
+  TRY(scan.alloc(nr + 1, s));
+  TRY(alive.alloc(ne + 1, s));
+  TRY(escan.alloc(ne + 1, s));
+  TRY(emask.alloc(ne * W, s));
+  TRY(cudaMemsetAsync(keep.p, 0, 4 * (nr + 1), s));
+  TRY(cudaMemsetAsync(alive.p, 0, 4 * (ne + 1), s));
+  if (ne) TRY(cudaMemcpyAsync(emask.p, in->ent_mask.p, 8 * ne * W, cudaMemcpyDeviceToDevice, s));
+  if (nc > 0)
+    count_launch(), k_prune<<<nb(nc, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(
+        in->offsets.p, in->j.p, in->mask.p, in->row_entry.p, nc, in->m, in->G, pos, bx,
+        in->r_list * in->r_list, grid->cell_of_cluster.p, grid->col_first.p, keep.p, emask.p, alive.p);
+  TRY(cudaGetLastError());
+  TRY(exclusive_scan_i32(keep.p, scan.p, nr + 1, s));
+  TRY(exclusive_scan_i32(alive.p, escan.p, ne + 1, s));
+  TRY(cudaMemcpyAsync(&h[0], scan.p + nr, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaMemcpyAsync(&h[1], escan.p + ne, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaStreamSynchronize(s));
+  l->n_rows = h[0];
+  l->n_entries = h[1];
+  TRY(l->offsets.alloc(nc + 1, s));
+  TRY(l->j.alloc(l->n_rows, s));
+  TRY(l->mask.alloc(l->n_rows, s));
+  TRY(l->delta.alloc(l->n_rows, s));
+  TRY(l->slack.alloc(l->n_rows, s));
+  TRY(l->row_entry.alloc(l->n_rows, s));
+  TRY(l->group_first.alloc(l->n_groups, s));
+  TRY(l->group_nmem.alloc(l->n_groups, s));
+  TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
+  TRY(l->ent_j.alloc(l->n_entries, s));
+  TRY(l->ent_delta.alloc(l->n_entries, s));
+  TRY(l->ent_slack.alloc(l->n_entries, s));
+  TRY(l->ent_mask.alloc(l->n_entries * W, s));
+  count_launch(), k_new_offsets<<<nb(nc + 1, 256), 256, 0, s>>>(in->offsets.p, nc, scan.p, l->offsets.p);
+  count_launch(), k_new_offsets<<<nb(l->n_groups + 1, 256), 256, 0, s>>>(in->ent_offsets.p, l->n_groups, escan.p,
+                                                         l->ent_offsets.p);
+  if (l->n_groups) {
+    TRY(cudaMemcpyAsync(l->group_first.p, in->group_first.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
+    TRY(cudaMemcpyAsync(l->group_nmem.p, in->group_nmem.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
+  }
+  if (nr)
+    count_launch(), k_compact_rows<<<nb(nr, 256), 256, 0, s>>>(nr, keep.p, scan.p, escan.p, in->j.p, in->mask.p,
+                                               in->delta.p, in->slack.p, in->row_entry.p, l->j.p,
+                                               l->mask.p, l->delta.p, l->slack.p, l->row_entry.p);
+  if (ne)
+    count_launch(), k_compact_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, alive.p, escan.p, in->ent_j.p, in->ent_delta.p,
+                                                  in->ent_slack.p, emask.p, l->ent_j.p, l->ent_delta.p,
+                                                  l->ent_slack.p, l->ent_mask.p);
+  TRY(cudaGetLastError());
+  TRY(order_entries(l, s));
+  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s);
+  *out = l;
+  return NBX_OK;
+fail:
+  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s);
+  nbx_list_free(l);
+  return NBX_ERR_CUDA;
+}
+
+extern "C" int nbx_list_info(const nbx_list_t* l, int64_t out[5]) {
+  if (!l || !out) {
+    set_error("nbx_list_info: null argument");
+    return NBX_ERR_PARAM;
+  }
+  out[0] = l->n_clusters;
+  out[1] = l->n_rows;
+  out[2] = l->m;
+  out[3] = l->n_groups;
+  out[4] = l->n_entries;
+  return NBX_OK;
+}
+
+template <typename TD, typename TH>
+static cudaError_t dl(const TD* d, int64_t count, TH* h, cudaStream_t s) {
+  if (!h || count <= 0) return cudaSuccess;
+  TD* tmp = (TD*)malloc(sizeof(TD) * (size_t)count);
+  cudaError_t e = cudaMemcpyAsync(tmp, d, sizeof(TD) * (size_t)count, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (!e)
+    for (int64_t i = 0; i < count; ++i) h[i] = (TH)tmp[i];
+  free(tmp);
+  return e;
+}
+
+extern "C" int nbx_list_download(const nbx_list_t* l, int64_t* offsets, int64_t* j_idx,
+                                 uint64_t* masks, void* stream) {
+  if (!l) {
+    set_error("nbx_list_download: null list");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  cudaError_t e;
+  if ((e = dl(l->offsets.p, l->n_clusters + 1, offsets, s)) || (e = dl(l->j.p, l->n_rows, j_idx, s)) ||
+      (e = dl(l->mask.p, l->n_rows, masks, s))) {
+    set_error("nbx_list_download: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
+}
+
+extern "C" int nbx_count_within(const nbx_list_t* l, const double* pos, const double box[3],
+                                double r_cut, void* stream, int64_t out[2]) {
+  if (!l || !pos || !box || !out) {
+    set_error("nbx_count_within: null argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  DBuf<unsigned long long> cnt;
+  unsigned long long h[2] = {0, 0};
+  TRY(cnt.alloc(2, s));
+  TRY(cudaMemsetAsync(cnt.p, 0, 16, s));
+  if (l->n_clusters > 0)
+    count_launch(), k_count_within<<<nb(l->n_clusters, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(
+        l->offsets.p, l->j.p, l->mask.p, l->n_clusters, l->m, pos, make_box(box), r_cut * r_cut, cnt.p);
+  TRY(cudaGetLastError());
+  TRY(cudaMemcpyAsync(h, cnt.p, 16, cudaMemcpyDeviceToHost, s));
+  TRY(cudaStreamSynchronize(s));
+  cnt.release(s);
+  out[0] = (int64_t)h[0];
+  out[1] = (int64_t)h[1];
+  return NBX_OK;
+fail:
+  cnt.release(s);
+  return NBX_ERR_CUDA;
+}
+
+extern "C" int nbx_super_layout(const nbx_list_t* lc, int32_t size, void* stream, int64_t* n_entries) {
+  if (!lc || size < 1) {
+    set_error("nbx_super_layout: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  nbx_list* l = const_cast<nbx_list*>(static_cast<const nbx_list*>(lc));
+  cudaStream_t s = to_stream(stream);
+  const int64_t nr = l->n_rows, nc = l->n_clusters;
+  const int64_t ngr = (nc + size - 1) / size;
+  DBuf<int32_t> ci_of_row, vals, vals2, head, hscan, gcount;
+  DBuf<uint64_t> keys, keys2;
+  int32_t ne = 0;
+  size_t bytes = 0;
+  void* tmp = nullptr;
+  TRY(ci_of_row.alloc(nr, s));
+  TRY(vals.alloc(nr, s));
+  TRY(vals2.alloc(nr, s));
+  TRY(keys.alloc(nr, s));
+  TRY(keys2.alloc(nr, s));
+  TRY(head.alloc(nr + 1, s));
+  TRY(hscan.alloc(nr + 1, s));
+  TRY(gcount.alloc(ngr + 1, s));
+  TRY(cudaMemsetAsync(gcount.p, 0, 4 * (ngr + 1), s));
+  if (nc) count_launch(), k_row_ci<<<nb(nc, 256), 256, 0, s>>>(l->offsets.p, nc, ci_of_row.p);
+  if (nr) {
+    count_launch(), k_super_keys<<<nb(nr, 256), 256, 0, s>>>(ci_of_row.p, l->j.p, nr, size, nc, keys.p, vals.p);
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)nr, 0, 64, s));
+    TRY(cudaMallocAsync(&tmp, bytes, s));
+    TRY(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)nr, 0, 64, s));
+    cudaFreeAsync(tmp, s);
+  }
+  count_launch(), k_super_heads<<<nb(nr + 1, 256), 256, 0, s>>>(keys2.p, nr, head.p);
+  TRY(exclusive_scan_i32(head.p, hscan.p, nr + 1, s));
+  TRY(cudaMemcpyAsync(&ne, hscan.p + nr, 4, cudaMemcpyDeviceToHost, s));
+  TRY(cudaStreamSynchronize(s));
+  TRY(l->super_j.alloc(ne, s));
+  TRY(l->super_pair.alloc((int64_t)ne * size, s));
+  TRY(l->super_offsets.alloc(ngr + 1, s));
+  TRY(cudaMemsetAsync(l->super_pair.p, 0xff, 4 * (size_t)ne * size, s));
+  if (nr)
+    count_launch(), k_super_fill<<<nb(nr, 256), 256, 0, s>>>(keys2.p, vals2.p, hscan.p, ci_of_row.p, nr, size, nc,
+                                             l->super_j.p, l->super_pair.p, gcount.p);
+  TRY(exclusive_scan_i32(gcount.p, l->super_offsets.p, ngr + 1, s));
+  TRY(cudaGetLastError());
+  TRY(cudaStreamSynchronize(s));
+  l->super_size = size;
+  l->super_groups = ngr;
+  l->super_entries = ne;
+  *n_entries = ne;
+  ci_of_row.release(s); vals.release(s); vals2.release(s); keys.release(s); keys2.release(s);
+  head.release(s); hscan.release(s); gcount.release(s);
+  return NBX_OK;
+fail:
+  ci_of_row.release(s); vals.release(s); vals2.release(s); keys.release(s); keys2.release(s);
+  head.release(s); hscan.release(s); gcount.release(s);
+  return NBX_ERR_CUDA;
+}
+
+extern "C" int nbx_super_download(const nbx_list_t* l, int64_t* super_offsets, int64_t* super_j,
+                                  int64_t* super_pair_idx, void* stream) {
+  if (!l || l->super_size == 0) {
+    set_error("nbx_super_download: layout not built");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  cudaError_t e;
+  if ((e = dl(l->super_offsets.p, l->super_groups + 1, super_offsets, s)) ||
+      (e = dl(l->super_j.p, l->super_entries, super_j, s)) ||
+      (e = dl(l->super_pair.p, l->super_entries * l->super_size, super_pair_idx, s))) {
+    set_error("nbx_super_download: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
+}

@@ -1,0 +1,189 @@
+"""Gridding into fixed-size clusters -- drop-in for clustermd.gridder.
+
+Mirrors /root/reference/pkg/src/clustermd/gridder.py: same names, argument
+meaning and errors.  The grid itself is built and kept on the GPU
+(``nbx_grid_build``, csrc/grid.cu); the numpy fields of ``ClusterGrid`` are
+materialised from the device on first access and are bit-identical to the
+reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from .model import ParameterError, ParticleSystem, SimBox
+
+VALID_CLUSTER_SIZES = (1, 2, 4, 8)
+
+
+class DeviceArray:
+    """A library-owned device buffer (pointer + shape) kept alive by `owner`."""
+
+    def __init__(self, ptr: ctypes.c_void_p, shape: tuple, owner):
+        self.ptr = ptr
+        self.shape = shape
+        self.owner = owner
+
+
+def _ro(a: np.ndarray) -> np.ndarray:
+    a.setflags(write=False)
+    return a
+
+
+class ClusterGrid:
+    """Device-resident clustered layout (gridder.py:23-66).
+
+    Fields (numpy, read-only, materialised lazily): perm, inverse_perm,
+    fill_mask, cell_of_cluster, clustered_positions, bboxes; plus m,
+    n_clusters, cell_counts, n_slots, n, cluster_centers().
+    """
+
+    def __init__(self, handle: ctypes.c_void_p, box_lengths: np.ndarray):
+        self._h = handle
+        info = np.zeros(5, dtype=np.int64)
+        _lib.check(_lib.load().nbx_grid_info(handle, _lib.ptr(info)), "grid_info")
+        self._n, self.m, cells, self.n_clusters, _ = (int(v) for v in info)
+        self.cell_counts = (cells, cells)
+        self.box_lengths = np.array(box_lengths, dtype=np.float64)
+        self._host = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.nbx_grid_free(h)
+            self._h = None
+
+    # -- sizes
+    @property
+    def n_slots(self) -> int:
+        return self.n_clusters * self.m
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    # -- device views
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def clustered_positions_device_ptr(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(_lib.load().nbx_grid_clustered_positions(self._h))
+
+    @property
+    def clustered_positions_device(self) -> DeviceArray:
+        """The build-time clustered positions without leaving the device."""
+        return DeviceArray(self.clustered_positions_device_ptr(), (self.n_slots, 3), self)
+
+    # -- host materialisation
+    def _materialise(self) -> dict:
+        if self._host is None:
+            ns, nc, n = self.n_slots, self.n_clusters, self.n
+            perm = np.empty(ns, dtype=np.int64)
+            inv = np.empty(n, dtype=np.int64)
+            fill = np.empty(ns, dtype=np.uint8)
+            coc = np.empty(nc, dtype=np.int64)
+            cpos = np.empty((ns, 3), dtype=np.float64)
+            bb = np.empty((nc, 2, 3), dtype=np.float64)
+            torch.cuda.synchronize()
+            _lib.check(_lib.load().nbx_grid_download(
+                self._h, _lib.ptr(perm), _lib.ptr(inv), _lib.ptr(fill), _lib.ptr(coc),
+                _lib.ptr(cpos), _lib.ptr(bb), dev.stream()), "grid_download")
+            self._host = dict(perm=_ro(perm), inverse_perm=_ro(inv), fill_mask=_ro(fill.astype(bool)),
+                              cell_of_cluster=_ro(coc), clustered_positions=_ro(cpos), bboxes=_ro(bb))
+        return self._host
+
+    perm = property(lambda self: self._materialise()["perm"])
+    inverse_perm = property(lambda self: self._materialise()["inverse_perm"])
+    fill_mask = property(lambda self: self._materialise()["fill_mask"])
+    cell_of_cluster = property(lambda self: self._materialise()["cell_of_cluster"])
+    clustered_positions = property(lambda self: self._materialise()["clustered_positions"])
+    bboxes = property(lambda self: self._materialise()["bboxes"])
+
+    def cluster_centers(self) -> np.ndarray:
+        """Bounding-box midpoints (gridder.py:64-66)."""
+        return 0.5 * (self.bboxes[:, 0] + self.bboxes[:, 1])
+
+
+def grid_cells(n: int, m: int, target_occupancy=None) -> int:
+    """gridder.py:82-91."""
+    occ = 2.0 * m if target_occupancy is None else target_occupancy
+    return max(1, int(round(math.sqrt(n / occ))))
+
+
+def build_cluster_grid(system: ParticleSystem, m: int, target_occupancy: float | None = None,
+                       positions=None) -> ClusterGrid:
+    """Grid in x/y, order columns by z, pack into m-clusters (gridder.py:69-146).
+
+    ``positions`` optionally overrides system.positions with a CUDA tensor
+    (device-resident callers avoid the host->device copy)."""
+    if m not in VALID_CLUSTER_SIZES:
+        raise ParameterError(f"cluster size m must be one of {VALID_CLUSTER_SIZES}, got {m}")
+    if target_occupancy is None:
+        target_occupancy = 2.0 * m
+    if target_occupancy <= 0:
+        raise ParameterError(f"target occupancy must be positive, got {target_occupancy}")
+    n = system.n
+    cells = grid_cells(n, m, target_occupancy)
+    pos = dev.to_device(system.positions if positions is None else positions, torch.float64, (n, 3))
+    box = _lib.box3(system.box.lengths)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().nbx_grid_build(_lib.ptr(pos), n, _lib.ptr(box), m, cells, dev.stream(),
+                                          ctypes.byref(h)), "grid_build")
+    return ClusterGrid(h, system.box.lengths)
+
+
+def scatter_to_original(grid: ClusterGrid, clustered_values):
+    """Per-slot array back to particle order, fillers dropped (gridder.py:149-162).
+
+    CUDA tensors stay on the device (nbx_scatter_to_original); host arrays
+    are indexed on the host."""
+    if dev.is_device_tensor(clustered_values):
+        v = clustered_values
+        if v.shape[0] != grid.n_slots:
+            raise ParameterError(f"expected leading axis {grid.n_slots}, got {v.shape[0]}")
+        k = int(np.prod(v.shape[1:])) if v.dim() > 1 else 1
+        vin = v.to(torch.float64).contiguous().reshape(grid.n_slots, k)
+        out = torch.empty((grid.n, k), dtype=torch.float64, device=v.device)
+        _lib.check(_lib.load().nbx_scatter_to_original(grid.handle, _lib.ptr(vin), k, _lib.ptr(out),
+                                                       dev.stream()), "scatter")
+        return out.reshape((grid.n,) + tuple(v.shape[1:])).to(v.dtype)
+    values = np.asarray(clustered_values)
+    if values.shape[0] != grid.n_slots:
+        raise ParameterError(f"expected leading axis {grid.n_slots}, got {values.shape[0]}")
+    out = np.zeros((grid.n,) + values.shape[1:], dtype=values.dtype)
+    real = ~grid.fill_mask
+    out[grid.perm[real]] = values[real]
+    return out
+
+
+def bbox_gap_sq(lo_i, hi_i, lo_j, hi_j, lengths) -> np.ndarray:
+    """Periodic AABB gap^2 (gridder.py:165-185); the GPU search evaluates the
+    same expression in csrc/common.cuh (gap_sq)."""
+    lo_j = np.asarray(lo_j, dtype=np.float64)
+    hi_j = np.asarray(hi_j, dtype=np.float64)
+    out = np.zeros(lo_j.shape[:-1], dtype=np.float64)
+    for d in range(3):
+        L = lengths[d]
+        a = lo_j[..., d] - hi_i[d]
+        b = lo_i[d] - hi_j[..., d]
+        g = np.minimum(np.maximum(0.0, np.maximum(a, b)),
+                       np.minimum(np.maximum(0.0, np.maximum(a - L, b + L)),
+                                  np.maximum(0.0, np.maximum(a + L, b - L))))
+        out = out + g * g
+    return out
+
+
+def cluster_min_distance(grid: ClusterGrid, i: int, j: int, box: SimBox) -> float:
+    """Conservative AABB distance between clusters i and j (gridder.py:188-196)."""
+    if not (0 <= i < grid.n_clusters and 0 <= j < grid.n_clusters):
+        raise ParameterError(f"cluster indices ({i}, {j}) out of range [0, {grid.n_clusters})")
+    lo_i, hi_i = grid.bboxes[i]
+    lo_j, hi_j = grid.bboxes[j]
+    return float(np.sqrt(bbox_gap_sq(lo_i, hi_i, lo_j, hi_j, box.lengths)))

@@ -1,0 +1,241 @@
+"""Cluster-pair list: build, prune, diagnostics -- drop-in for clustermd.pairlist.
+
+Mirrors /root/reference/pkg/src/clustermd/pairlist.py.  Lists are built and
+pruned on the GPU (csrc/search.cu); ``ClusterPairList`` keeps the device
+handle and materialises the reference's numpy fields (offsets, j_idx, masks,
+super layout) on first access, set-identical to the reference.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from .gridder import ClusterGrid, DeviceArray, bbox_gap_sq
+from .model import ParameterError, SimBox
+
+VALID_SUPERCLUSTER_SIZES = (1, 8)
+
+
+def _ro(a):
+    a.setflags(write=False)
+    return a
+
+
+class ClusterPairList:
+    """CSR cluster-pair list + optional super-cluster layout (pairlist.py:27-94).
+
+    Device-resident; numpy views: offsets, j_idx, masks (n_pairs, m, m) bool,
+    super_offsets / super_j_idx / super_pair_idx (supercluster_size 8)."""
+
+    def __init__(self, handle, grid: ClusterGrid, r_list: float, n_lane: int, build_step: int,
+                 supercluster_size: int, build_positions=None):
+        self._h = handle
+        self.grid = grid
+        info = np.zeros(5, dtype=np.int64)
+        _lib.check(_lib.load().nbx_list_info(handle, _lib.ptr(info)), "list_info")
+        self._n_i, self._n_rows, self.m, self.n_groups, self.n_entries = (int(v) for v in info)
+        self.r_list = float(r_list)
+        self.n_lane = n_lane
+        self.build_step = build_step
+        self.supercluster_size = supercluster_size
+        self._build_positions = build_positions
+        self._host = None
+        self._super = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.nbx_list_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n_i_clusters(self) -> int:
+        return self._n_i
+
+    @property
+    def n_pairs(self) -> int:
+        return self._n_rows
+
+    @property
+    def build_positions(self) -> np.ndarray:
+        if self._build_positions is None:
+            return self.grid.clustered_positions
+        return self._build_positions
+
+    def _materialise(self):
+        if self._host is None:
+            off = np.empty(self._n_i + 1, dtype=np.int64)
+            jj = np.empty(self._n_rows, dtype=np.int64)
+            mk = np.empty(self._n_rows, dtype=np.uint64)
+            torch.cuda.synchronize()
+            _lib.check(_lib.load().nbx_list_download(self._h, _lib.ptr(off), _lib.ptr(jj), _lib.ptr(mk),
+                                                     dev.stream()), "list_download")
+            m = self.m
+            bits = ((mk[:, None] >> np.arange(m * m, dtype=np.uint64)) & np.uint64(1)).astype(bool)
+            self._host = dict(offsets=_ro(off), j_idx=_ro(jj), masks=_ro(bits.reshape(-1, m, m)),
+                              mask_bits=_ro(mk))
+        return self._host
+
+    offsets = property(lambda self: self._materialise()["offsets"])
+    j_idx = property(lambda self: self._materialise()["j_idx"])
+    masks = property(lambda self: self._materialise()["masks"])
+    mask_bits = property(lambda self: self._materialise()["mask_bits"])
+
+    def _super_layout(self):
+        if self.supercluster_size == 1:
+            return None
+        if self._super is None:
+            ne = ctypes.c_int64()
+            _lib.check(_lib.load().nbx_super_layout(self._h, self.supercluster_size, dev.stream(),
+                                                    ctypes.byref(ne)), "super_layout")
+            ngr = -(-self._n_i // self.supercluster_size)
+            so = np.empty(ngr + 1, dtype=np.int64)
+            sj = np.empty(ne.value, dtype=np.int64)
+            sp = np.empty((ne.value, self.supercluster_size), dtype=np.int64)
+            _lib.check(_lib.load().nbx_super_download(self._h, _lib.ptr(so), _lib.ptr(sj), _lib.ptr(sp),
+                                                      dev.stream()), "super_download")
+            self._super = (_ro(so), _ro(sj), _ro(sp))
+        return self._super
+
+    super_offsets = property(lambda self: None if self._super_layout() is None else self._super_layout()[0])
+    super_j_idx = property(lambda self: None if self._super_layout() is None else self._super_layout()[1])
+    super_pair_idx = property(lambda self: None if self._super_layout() is None else self._super_layout()[2])
+
+    @property
+    def n_super_groups(self) -> int:
+        return 0 if self.supercluster_size == 1 else -(-self._n_i // self.supercluster_size)
+
+    def entries(self, ci: int) -> np.ndarray:
+        return self.j_idx[self.offsets[ci]:self.offsets[ci + 1]]
+
+    def pair_i_clusters(self) -> np.ndarray:
+        return np.repeat(np.arange(self._n_i, dtype=np.int64), np.diff(self.offsets))
+
+    def super_flags(self):
+        sp = self.super_pair_idx
+        return None if sp is None else sp >= 0
+
+
+@dataclass(frozen=True)
+class InteractionStats:
+    """pairlist.py:97-103."""
+
+    n_admitted: int
+    n_within_cutoff: int
+    ratio: float
+
+
+def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, supercluster_size: int = 1,
+                    n_lane: int = 1, build_step: int = 0) -> ClusterPairList:
+    """All cluster pairs with AABB gap <= r_list, j >= i (pairlist.py:147-217)."""
+    if r_list <= 0.0:
+        raise ParameterError(f"r_list must be positive, got {r_list}")
+    if np.any(box.lengths < 2.0 * r_list):
+        raise ParameterError(f"every box edge must be >= 2*r_list={2.0 * r_list} "
+                             f"for the single-image convention, got {box.lengths}")
+    if supercluster_size not in VALID_SUPERCLUSTER_SIZES:
+        raise ParameterError(f"supercluster_size must be one of {VALID_SUPERCLUSTER_SIZES}, "
+                             f"got {supercluster_size}")
+    h = ctypes.c_void_p()
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_pairlist_build(grid.handle, _lib.ptr(L), float(r_list), dev.stream(),
+                                              ctypes.byref(h)), "pairlist_build")
+    return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+
+
+def _positions_ptr(plist: ClusterPairList, positions):
+    """Device pointer for clustered positions: the grid's own build snapshot
+    when that is what the caller passed, else an uploaded copy."""
+    g = plist.grid
+    if isinstance(positions, DeviceArray):
+        return positions.ptr, positions
+    if g._host is not None and positions is g._host["clustered_positions"]:
+        return g.clustered_positions_device_ptr(), None
+    if dev.is_device_tensor(positions):
+        t = positions.to(torch.float64).contiguous()
+        return _lib.ptr(t), t
+    arr = np.asarray(positions, dtype=np.float64)
+    t = dev.to_device(arr, torch.float64)
+    return _lib.ptr(t), t
+
+
+def prune_pair_list(plist: ClusterPairList, positions, box: SimBox) -> ClusterPairList:
+    """Drop rows whose exact min admitted-slot distance exceeds r_list
+    (pairlist.py:242-282); positions are clustered (n_slots, 3)."""
+    shape = tuple(positions.shape)
+    if shape != (plist.grid.n_slots, 3):
+        raise ParameterError(f"positions shape {shape} does not match the list's slot layout "
+                             f"{(plist.grid.n_slots, 3)}")
+    if plist.n_pairs == 0:
+        return plist
+    p, keep_alive = _positions_ptr(plist, positions)
+    h = ctypes.c_void_p()
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_pairlist_prune(plist.handle, plist.grid.handle, p, _lib.ptr(L), dev.stream(),
+                                              ctypes.byref(h)), "pairlist_prune")
+    del keep_alive
+    return ClusterPairList(h, plist.grid, plist.r_list, plist.n_lane, plist.build_step,
+                           plist.supercluster_size, plist._build_positions)
+
+
+def admitted_pairs(plist: ClusterPairList, grid: ClusterGrid) -> set:
+    """Admitted original-index pairs (lo, hi) (pairlist.py:285-300)."""
+    if plist.n_pairs == 0:
+        return set()
+    m = plist.m
+    p, a, b = np.nonzero(plist.masks)
+    ci = plist.pair_i_clusters()
+    oi = grid.perm[ci[p] * m + a]
+    oj = grid.perm[plist.j_idx[p] * m + b]
+    return set(zip(np.minimum(oi, oj).tolist(), np.maximum(oi, oj).tolist()))
+
+
+def interaction_stats(plist: ClusterPairList, grid: ClusterGrid, positions, box: SimBox,
+                      r_cut: float) -> InteractionStats:
+    """Admitted vs within-r_cut slot pairs (pairlist.py:323-346), counted on the GPU."""
+    if r_cut > plist.r_list:
+        raise ParameterError(f"r_cut={r_cut} must not exceed the list radius r_list={plist.r_list}")
+    if plist.n_pairs == 0:
+        return InteractionStats(0, 0, 1.0)
+    p, keep_alive = _positions_ptr(plist, positions)
+    out = np.zeros(2, dtype=np.int64)
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_count_within(plist.handle, p, _lib.ptr(L), float(r_cut), dev.stream(),
+                                            _lib.ptr(out)), "count_within")
+    del keep_alive
+    n_adm, n_win = int(out[0]), int(out[1])
+    ratio = float(n_adm) / float(n_win) if n_win else float("inf")
+    if n_adm == 0:
+        ratio = 1.0 if n_win == 0 else 0.0
+    return InteractionStats(n_admitted=n_adm, n_within_cutoff=n_win, ratio=ratio)
+
+
+def write_pairs_csv(plist: ClusterPairList, grid: ClusterGrid, box: SimBox, path) -> None:
+    """Per-row diagnostics CSV (pairlist.py:349-376): bbox vs exact distance."""
+    ci = plist.pair_i_clusters()
+    pos = plist.build_positions.reshape(-1, plist.m, 3)
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["i_cluster", "j_cluster", "bbox_distance_nm", "exact_min_distance_nm"])
+        for p in range(plist.n_pairs):
+            lo_i, hi_i = grid.bboxes[ci[p]]
+            lo_j, hi_j = grid.bboxes[plist.j_idx[p]]
+            gap = float(np.sqrt(bbox_gap_sq(lo_i, hi_i, lo_j, hi_j, box.lengths)))
+            dr = pos[ci[p]][:, None, :] - pos[plist.j_idx[p]][None, :, :]
+            dr = dr - np.floor(dr / box.lengths + 0.5) * box.lengths
+            d2 = np.einsum("abd,abd->ab", dr, dr)
+            d2[~plist.masks[p]] = np.inf
+            mn = float(d2.min())
+            w.writerow([int(ci[p]), int(plist.j_idx[p]), repr(gap),
+                        repr(float(np.sqrt(mn))) if np.isfinite(mn) else repr(float("nan"))])
