@@ -46,7 +46,6 @@ struct ForceArgs {
   const int32_t* ent_off;     // group -> entry range
   const int32_t* ent_j;
   const float4* ent_delta;    // j-local -> group-local offset (image included)
-  const float* ent_slack;
   const uint64_t* ent_mask;
   // per-slot inputs
   const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
@@ -101,16 +100,17 @@ __host__ __device__ constexpr uint64_t column_bits() {
   return c;
 }
 
-// Ewald real-space correction polynomials (host-fitted, force.cu
-// ewald_fit): with w = beta^2 r^2 and u = w * (2/w_max) - 1 in [-1, 1],
-//   Gf(u) ~ erf(z)/z^3 - 2/sqrt(pi) exp(-w)/w   (force)
-//   Gv(u) ~ erf(z)/z                            (energy),  z = beta r,
-// so that F_c/r = qq (1/r^3 - beta^3 Gf) and E_c = qq (1/r - beta Gv - shift):
-// no transcendental beyond the rsqrt every pair needs anyway.
+// Ewald real space without transcendentals beyond the per-pair rsqrt: with
+// z = beta r, w = z^2 and u = w (2 / w_max) - 1 in [-1, 1] (host-fitted
+// Chebyshev series of functions ANALYTIC in w, ew_fit below):
+//   Gf(u) ~ erf(z)/z^3 - 2 exp(-w) / (sqrt(pi) w)  ->  F_c/r = qq (1/r^3 - beta^3 Gf)
+//   Gv(u) ~ erf(z)/z                               ->  E_c = qq (1/r - beta Gv - shift)
+// (the GROMACS analytical-Ewald split).  The polynomial terms do not vanish
+// with rinv, so they are masked through qm = inc ? qq : 0.
 constexpr int EW_DEG = 12;
 
-// One pair: F/r, plus energies when requested.  `inc` masks everything:
-// rinv is zeroed, and qq too where a term does not carry rinv.
+// One pair: F/r, plus energies when requested.  `inc` zeroes rinv, which
+// masks every force term; energy shift terms are masked explicitly.
 template <int ELEC, bool KRF, bool ENERGY>
 __device__ __forceinline__ float pair_eval(const ForceArgs& A, const float4& xi, const float4& lj, float xjw,
                                            float r2, bool inc, float& elj, float& ec) {
@@ -120,27 +120,28 @@ __device__ __forceinline__ float pair_eval(const ForceArgs& A, const float4& xi,
   const float rinv6 = rinv2 * rinv2 * rinv2;
   const float qq = xi.w * xjw;
   const float flj = rinv6 * fmaf(lj.y, rinv6, -lj.x);  // 12 c12/r^12 - 6 c6/r^6
+  const float qr = qq * rinv;
   float fscal;
   if (ELEC == FE_RF) {
-    fscal = fmaf(qq, rinv, flj) * rinv2;
+    fscal = (flj + qr) * rinv2;
     if (KRF || ENERGY) {
       const float qm = inc ? qq : 0.f;
       if (KRF) fscal = fmaf(-qm, A.k2rf, fscal);
-      if (ENERGY) ec = qm * (rinv + fmaf(A.krf, r2, -A.crf));
+      if (ENERGY) ec = fmaf(qm, fmaf(A.krf, r2, -A.crf), qr);
     }
   } else {
     const float qm = inc ? qq : 0.f;
     const float u = fmaf(r2, A.ew_a, -1.f);
-    float pf = A.ew_f[0];
+    float gf = A.ew_f[0];
 #pragma unroll
-    for (int k = 1; k <= EW_DEG; ++k) pf = fmaf(pf, u, A.ew_f[k]);
-    const float t = fmaf(-A.beta3, pf, rinv * rinv2);
+    for (int k = 1; k <= EW_DEG; ++k) gf = fmaf(gf, u, A.ew_f[k]);
+    const float t = fmaf(-A.beta3, gf, rinv * rinv2);
     fscal = fmaf(qm, t, flj * rinv2);
     if (ENERGY) {
-      float pv = A.ew_v[0];
+      float gv = A.ew_v[0];
 #pragma unroll
-      for (int k = 1; k <= EW_DEG; ++k) pv = fmaf(pv, u, A.ew_v[k]);
-      ec = qm * (rinv - fmaf(A.beta, pv, A.ew_shift));
+      for (int k = 1; k <= EW_DEG; ++k) gv = fmaf(gv, u, A.ew_v[k]);
+      ec = qm * (rinv - fmaf(A.beta, gv, A.ew_shift));
     }
   }
   if (ENERGY) elj = inc ? fmaf(rinv6, fmaf(lj.y * (1.f / 12.f), rinv6, -lj.x * (1.f / 6.f)), -lj.z) : 0.f;
@@ -161,22 +162,61 @@ __device__ __forceinline__ float pair_geom(const ForceArgs& A, const float4& xi,
   return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
 }
 
-// One iteration body: this lane's entry (j-atom xj, pre-shifted masks mk)
-// against the group's i-atoms.  MI = per-pair minimum image.
-template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND, bool MI>
+// Lane-view of one entry: its j-cluster, the lane's j-atom (shifted into the
+// group frame), and the entry masks pre-shifted by the lane's j-slot b and
+// split into 32-bit words (bit k*m*m + a*m tests pair (member k, atom a)).
+template <int W>
+struct Entry {
+  int32_t cj;
+  float4 d;          // xyz: j-local -> group-local offset, w: slack
+  uint32_t w[2 * W];
+};
+
+template <int M, int W>
+__device__ __forceinline__ void load_entry(const ForceArgs& A, int32_t e, bool valid, int b, Entry<W>& E) {
+  if (valid) {
+    E.cj = __ldg(A.ent_j + e);
+    E.d = __ldg(A.ent_delta + e);
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const uint64_t mw = __ldg(A.ent_mask + (int64_t)e * W + q) >> b;
+      E.w[2 * q] = (uint32_t)mw;
+      E.w[2 * q + 1] = (uint32_t)(mw >> 32);
+    }
+  } else {
+    E.cj = 0;
+    E.d = make_float4(0.f, 0.f, 0.f, 3.0e38f);
+#pragma unroll
+    for (int q = 0; q < 2 * W; ++q) E.w[q] = 0u;
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void load_jatom(const ForceArgs& A, int32_t cj, int b, const float4& d, float4& xj,
+                                           int& tj) {
+  xj = __ldg(A.xyzq + (int64_t)cj * M + b);
+  tj = __ldg(A.type + (int64_t)cj * M + b);
+  xj.x += d.x;
+  xj.y += d.y;
+  xj.z += d.z;
+}
+
+template <int M, int W>
+__device__ __forceinline__ bool entry_bit(const Entry<W>& E, int p) {
+  return (E.w[p >> 5] >> (p & 31)) & 1u;
+}
+
+// One iteration: this lane's entry against the group's i-atoms.  MI =
+// per-pair minimum image (entries whose slack cannot guarantee one image).
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND, bool MI, int W>
 __device__ __forceinline__ void sweep(const ForceArgs& A, const float4* __restrict__ s_xi,
-                                      const float4* __restrict__ s_ljt, const uint64_t* mk, unsigned wpres,
+                                      const float4* __restrict__ s_ljt, const Entry<W>& E, unsigned wpres,
                                       const float4& xj, float (&fi)[G * M][3], float& fjx, float& fjy,
                                       float& fjz, float& elj, float& ec, uint32_t& near) {
   constexpr int MM = M * M;
-  constexpr int W = (G * M * M > 64) ? 2 : 1;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     if (!((wpres >> k) & 1u)) continue;
-    // this member's m x m bits (pre-shifted by b): 32-bit for m <= 4
-    uint64_t word64;
-    if constexpr (W == 2) word64 = mk[k];
-    else word64 = mk[0] >> (k * MM);
 #pragma unroll
     for (int a = 0; a < M; ++a) {
       const int ia = k * M + a;
@@ -184,9 +224,7 @@ __device__ __forceinline__ void sweep(const ForceArgs& A, const float4* __restri
       const float4 lj = s_ljt[ia];
       float dx, dy, dz;
       const float r2 = pair_geom<MI>(A, xi, xj, dx, dy, dz);
-      bool adm;
-      if constexpr (M <= 4) adm = ((uint32_t)word64 >> (a * M)) & 1u;
-      else adm = (a < 4) ? (((uint32_t)word64 >> (a * M)) & 1u) : (((uint32_t)(word64 >> 32) >> ((a - 4) * M)) & 1u);
+      const bool adm = entry_bit<M, W>(E, k * MM + a * M);
       const bool inc = adm && (r2 <= A.rc2);
       if (BAND) near |= (adm && fabsf(r2 - A.rc2) < A.band) ? (1u << ia) : 0u;
       float pe_lj = 0.f, pe_c = 0.f;
@@ -262,11 +300,18 @@ k_force(const ForceArgs A) {
   const int32_t e_beg = A.ent_off[g], e_end = A.ent_off[g + 1];
   float4* s_lj = s_dyn + (size_t)w * IA * A.nt;
 
-  // stage the group's i-atoms and their LJ parameters per j-type
+  // software pipeline: entry data two iterations ahead, j-atom one ahead
+  Entry<W> cur, nxt;
+  float4 xj;
+  int tj;
+  load_entry<M, W>(A, e_beg + r, e_beg + r < e_end, b, cur);
+  load_entry<M, W>(A, e_beg + R + r, e_beg + R + r < e_end, b, nxt);
+  load_jatom<M>(A, cur.cj, b, cur.d, xj, tj);
+
+  // stage the group's i-atoms (group frame) and their LJ parameters per j-type
   for (int ia = lane; ia < IA; ia += 32) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (ia < nmem * M) {
-      // member-local -> group-local (origin: first member's bbox low corner), FP64 offset
       v = A.xyzq[(int64_t)first * M + ia];
       const int64_t c = first + ia / M;
       v.x = (float)((A.bbox[6 * c + 0] - A.bbox[6 * (int64_t)first + 0]) + (double)v.x);
@@ -295,50 +340,37 @@ k_force(const ForceArgs A) {
   for (int32_t e0 = e_beg; e0 < e_end; e0 += R) {
     const int32_t e = e0 + r;
     const bool valid = e < e_end;
-    uint64_t mk[W];
-    float4 xj = make_float4(0.f, 0.f, 0.f, 0.f);
-    int tj = 0;
-    bool unsafe = false;
-    int32_t cj = 0;
-    if (valid) {
-      cj = A.ent_j[e];
-      const float4 S = A.ent_delta[e];
-#pragma unroll
-      for (int q = 0; q < W; ++q) mk[q] = A.ent_mask[(int64_t)e * W + q] >> b;
-      xj = A.xyzq[(int64_t)cj * M + b];
-      tj = A.type[(int64_t)cj * M + b];
-      xj.x += S.x;
-      xj.y += S.y;
-      xj.z += S.z;
-      unsafe = A.ent_slack[e] < slack_thr;
-    } else {
-#pragma unroll
-      for (int q = 0; q < W; ++q) mk[q] = 0ull;
-    }
+    // prefetch: entry data for e0 + 2R, j-atom for e0 + R
+    Entry<W> nx2;
+    load_entry<M, W>(A, e + 2 * R, e + 2 * R < e_end, b, nx2);
+    float4 xj_n;
+    int tj_n;
+    load_jatom<M>(A, nxt.cj, b, nxt.d, xj_n, tj_n);
+
     unsigned pres = 0;
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       uint64_t word;
-      if constexpr (W == 2) word = mk[k];
-      else word = mk[0] >> (k * MM);
+      if constexpr (W == 2) word = ((uint64_t)cur.w[2 * k + 1] << 32) | cur.w[2 * k];
+      else word = (((uint64_t)cur.w[1] << 32) | cur.w[0]) >> (k * MM);
       pres |= ((word & colmask) != 0ull) ? (1u << k) : 0u;
     }
     const unsigned wpres = __reduce_or_sync(0xffffffffu, pres);
-    const bool wunsafe = __any_sync(0xffffffffu, unsafe);
+    const bool wunsafe = __any_sync(0xffffffffu, valid && cur.d.w < slack_thr);
     const float4* s_ljt = s_lj + tj * IA;
     float fjx = 0.f, fjy = 0.f, fjz = 0.f;
     float elj = 0.f, ec = 0.f;
     uint32_t near = 0;
     if (!wunsafe)
-      sweep<M, G, ELEC, KRF, ENERGY, BAND, false>(A, s_xi[w], s_ljt, mk, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+      sweep<M, G, ELEC, KRF, ENERGY, BAND, false, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
     else
-      sweep<M, G, ELEC, KRF, ENERGY, BAND, true>(A, s_xi[w], s_ljt, mk, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+      sweep<M, G, ELEC, KRF, ENERGY, BAND, true, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
     if (BAND && __any_sync(0xffffffffu, near != 0)) {
       if (near) {
         if (!wunsafe)
-          band_fix<M, G, ELEC, KRF, ENERGY, false>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cj, b, fjx, fjy, fjz, elj, ec);
+          band_fix<M, G, ELEC, KRF, ENERGY, false>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cur.cj, b, fjx, fjy, fjz, elj, ec);
         else
-          band_fix<M, G, ELEC, KRF, ENERGY, true>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cj, b, fjx, fjy, fjz, elj, ec);
+          band_fix<M, G, ELEC, KRF, ENERGY, true>(A, s_xi[w], s_ljt, s_corr[w], near, xj, first, cur.cj, b, fjx, fjy, fjz, elj, ec);
       }
       __syncwarp();
     }
@@ -347,6 +379,10 @@ k_force(const ForceArgs A) {
       elj_acc += (double)elj;
       ec_acc += (double)ec;
     }
+    cur = nxt;
+    nxt = nx2;
+    xj = xj_n;
+    tj = tj_n;
   }
 
   // i-force transpose-reduce through shared memory
@@ -410,23 +446,38 @@ __global__ void k_gather(const double* __restrict__ pos, const double* __restric
 }
 
 // Final per-atom forces: own i-partial + j-partials of every entry whose
-// j-cluster holds the atom, summed in FP64 in ascending entry order.
+// j-cluster holds the atom.  One warp per cluster, lane = (stride s of 32/m,
+// j-slot b): lane sums items s, s + 32/m, ... in FP64, then a fixed shuffle
+// tree combines the strides -- the same order on every run (deterministic).
 __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __restrict__ part_j,
                          const int32_t* __restrict__ t_first, const int32_t* __restrict__ t_items,
                          const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
-                         int64_t n_slots, int m, int flags, double* __restrict__ f_out,
+                         int64_t n_clusters, int m, int flags, double* __restrict__ f_out,
                          unsigned int* __restrict__ flag) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= n_slots) return;
-  const int64_t c = s / m, b = s - c * m;
-  const float4 pi = part_i[s];
-  double fx = pi.x, fy = pi.y, fz = pi.z;
-  for (int32_t t = t_first[c]; t < t_first[c + 1]; ++t) {
-    const float4 pj = part_j[(int64_t)t_items[t] * m + b];
+  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= n_clusters) return;
+  const int S = 32 / m;
+  const int sidx = lane / m, b = lane - sidx * m;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  const int32_t t1 = t_first[c + 1];
+  for (int32_t t = t_first[c] + sidx; t < t1; t += S) {
+    const float4 pj = __ldg(part_j + (int64_t)__ldg(t_items + t) * m + b);
     fx += pj.x;
     fy += pj.y;
     fz += pj.z;
   }
+  for (int o = 16; o >= m; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+    fz += __shfl_xor_sync(0xffffffffu, fz, o);
+  }
+  if (sidx != 0) return;
+  const int64_t s = c * m + b;
+  const float4 pi = part_i[s];
+  fx += pi.x;
+  fy += pi.y;
+  fz += pi.z;
   if (!isfinite(fx) || !isfinite(fy) || !isfinite(fz)) atomicOr(flag, 1u);
   int64_t o;
   if (flags & NBX_FORCE_CLUSTERED) {
@@ -481,6 +532,10 @@ __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __
       }
     }
   }
+}
+
+__global__ void k_init_scalars(unsigned int* scalars) {
+  if (threadIdx.x < 4) scalars[threadIdx.x] = threadIdx.x < 2 ? 0u : 0xffffffffu;
 }
 
 __global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, int shift,
@@ -554,9 +609,9 @@ static cudaError_t launch_force(int m, bool grouped, const ForceArgs& A, int ele
 
 // Chebyshev fit of the Ewald correction functions (see EW_DEG above), in
 // double precision on the host, converted to a power series in u.
-static double ew_gf(double w) {
+static double ew_gf(double w) {  // erf(z)/z^3 - 2 exp(-w) / (sqrt(pi) w)
   if (w < 0.5) {  // series: (2/sqrt(pi)) sum_{n>=1} (-1)^(n+1) w^(n-1) 2n / (n! (2n+1))
-    double s = 0.0, term = 1.0;  // term = w^(n-1)/n!
+    double s = 0.0, term = 1.0;  // term = w^(n-1) / n!
     for (int n = 1; n < 30; ++n) {
       term = (n == 1) ? 1.0 : term * w / n;
       s += ((n & 1) ? 1.0 : -1.0) * term * (2.0 * n) / (2.0 * n + 1.0);
@@ -566,7 +621,7 @@ static double ew_gf(double w) {
   const double z = sqrt(w);
   return erf(z) / (z * w) - 2.0 / sqrt(M_PI) * exp(-w) / w;
 }
-static double ew_gv(double w) {
+static double ew_gv(double w) {  // erf(z)/z
   if (w < 1e-12) return 2.0 / sqrt(M_PI);
   const double z = sqrt(w);
   return erf(z) / z;
@@ -691,6 +746,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
   if (wk.scalars.n < 4) { if ((e = wk.scalars.alloc(4, s))) goto cuda_fail; }
   if (wk.lj.n < (int64_t)p->n_types * p->n_types) {
     if ((e = wk.lj.alloc((int64_t)p->n_types * p->n_types, s))) goto cuda_fail;
+    wk.lj_key.clear();
   }
   if (!canonical && !wk.t_ready) {
     if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s))) goto cuda_fail;
@@ -701,16 +757,23 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     wk.tc_ready = true;
   }
   {
-    // LJ table -> device (tiny; stream-ordered through a temporary)
+    // LJ table -> device only when it changed (no per-call host copies)
     const int nt = p->n_types;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&dtab), sizeof(double) * 2 * nt * nt, s))) goto cuda_fail;
-    if ((e = cudaMemcpyAsync(dtab, p->lj_table, sizeof(double) * 2 * nt * nt, cudaMemcpyHostToDevice, s))) goto cuda_fail;
-    count_launch(), k_build_lj<<<nb(nt * nt, 64), 64, 0, s>>>(dtab, nt, p->r_cut * p->r_cut, p->shift_potential, wk.lj.p);
-    cudaFreeAsync(dtab, s);
-    dtab = nullptr;
-    // scalars: [0] = 0 (max displacement), [2..3] = ~0 (bad key)
-    const unsigned int init[4] = {0u, 0u, 0xffffffffu, 0xffffffffu};
-    if ((e = cudaMemcpyAsync(wk.scalars.p, init, sizeof(init), cudaMemcpyHostToDevice, s))) goto cuda_fail;
+    std::vector<double> key(p->lj_table, p->lj_table + 2 * nt * nt);
+    key.push_back(p->r_cut);
+    key.push_back((double)p->shift_potential);
+    if (key != wk.lj_key) {
+      if ((e = cudaMallocAsync(reinterpret_cast<void**>(&dtab), sizeof(double) * 2 * nt * nt, s))) goto cuda_fail;
+      if ((e = cudaMemcpyAsync(dtab, p->lj_table, sizeof(double) * 2 * nt * nt, cudaMemcpyHostToDevice, s))) goto cuda_fail;
+      count_launch();
+      k_build_lj<<<nb(nt * nt, 64), 64, 0, s>>>(dtab, nt, p->r_cut * p->r_cut, p->shift_potential, wk.lj.p);
+      cudaFreeAsync(dtab, s);
+      dtab = nullptr;
+      wk.lj_key = key;
+    }
+    // scalars: [0] = 0 (max displacement), [1] = 0 (non-finite flag), [2..3] = ~0 (bad key)
+    count_launch();
+    k_init_scalars<<<1, 32, 0, s>>>(wk.scalars.p);
     if (ns > 0)
       count_launch(), k_gather<<<nb(ns, 256), 256, 0, s>>>(positions, charges, lj_type, grid->perm.p, grid->fill.p,
                                            grid->cpos.p, grid->bbox.p, m, ns, bx, wk.xyzq.p, wk.type.p,
@@ -727,7 +790,6 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.ent_off = canonical ? l->offsets.p : l->ent_offsets.p;
     A.ent_j = canonical ? l->j.p : l->ent_j.p;
     A.ent_delta = canonical ? l->delta.p : l->ent_delta.p;
-    A.ent_slack = canonical ? l->slack.p : l->ent_slack.p;
     A.ent_mask = canonical ? l->mask.p : l->ent_mask.p;
     A.xyzq = wk.xyzq.p;
     A.bbox = grid->bbox.p;
@@ -778,9 +840,9 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     if ((e = launch_force(m, !canonical, A, ewald ? FE_EWALD : FE_RF, use_krf, (flags & NBX_FORCE_ENERGY) != 0, band, s)))
       goto cuda_fail;
     if (ns > 0)
-      count_launch(), k_reduce<<<nb(ns, 256), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
+      count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
                                            canonical ? wk.tc_items.p : wk.t_items.p, grid->perm.p,
-                                           grid->fill.p, ns, m, flags, f_out, wk.scalars.p + 1);
+                                           grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1);
     if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
       // nothing else to produce
     } else {

@@ -115,8 +115,8 @@ k_colsort(const int32_t* __restrict__ sorted, const int32_t* __restrict__ col_at
 }
 
 __global__ void k_bbox(const double* __restrict__ cpos, const uint8_t* __restrict__ fill,
-                       int64_t n_clusters, int m, double* __restrict__ bbox,
-                       int8_t* __restrict__ nreal) {
+                       int64_t n_clusters, int m, double* __restrict__ bbox, float2* __restrict__ zr,
+                       float4* __restrict__ bbf, int8_t* __restrict__ nreal) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n_clusters) return;
   double lo[3], hi[3];
@@ -136,6 +136,9 @@ __global__ void k_bbox(const double* __restrict__ cpos, const uint8_t* __restric
     bbox[6 * c + 3 + d] = hi[d];
   }
   nreal[c] = (int8_t)nr;
+  zr[c] = make_float2(__double2float_rd(lo[2]), __double2float_ru(hi[2]));  // outward-rounded z range
+  bbf[2 * c] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]), 0.f);
+  bbf[2 * c + 1] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), 0.f);
 }
 
 __global__ void k_scatter_original(const double* __restrict__ in, const int32_t* __restrict__ perm,
@@ -163,6 +166,22 @@ void nbx::set_error(const char* fmt, ...) {
 }
 extern "C" const char* nbx_last_error(void) { return g_err; }
 extern "C" int nbx_version(void) { return 1; }
+
+void nbx::ensure_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // pre-grow the pool once (kept: threshold = max) so rebuilds do not map
+    // new pages in the middle of a step
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, size_t(2) << 30, 0) == cudaSuccess) cudaFreeAsync(p, 0);
+  }
+  done_dev = dev;
+}
 
 static std::atomic<int64_t> g_launches{0};
 void nbx::count_launch(int64_t k) { g_launches += k; }
@@ -264,6 +283,7 @@ extern "C" int nbx_grid_build(const double* positions, int64_t n, const double b
   const int64_t ns = (int64_t)nc * m;
   if ((e = g->perm.alloc(ns, s)) || (e = g->fill.alloc(ns, s)) || (e = g->cpos.alloc(3 * ns, s)) ||
       (e = g->cell_of_cluster.alloc(nc, s)) || (e = g->bbox.alloc(6 * (int64_t)nc, s)) ||
+      (e = g->zr.alloc(nc, s)) || (e = g->bbf.alloc(2 * (int64_t)nc, s)) ||
       (e = g->nreal.alloc(nc, s)))
     return fail(e);
   if (n > 0) {
@@ -272,7 +292,7 @@ extern "C" int nbx_grid_build(const double* positions, int64_t n, const double b
     k_colsort<<<blocks(n_cols, COLSORT_WARPS), COLSORT_WARPS * 32, 0, s>>>(
         sorted.p, col_atom_first.p, g->col_first.p, n_cols, m, wpos.p, g->perm.p, g->fill.p,
         g->cpos.p, g->inverse_perm.p, g->cell_of_cluster.p);
-    k_bbox<<<blocks(nc, 128), 128, 0, s>>>(g->cpos.p, g->fill.p, nc, m, g->bbox.p, g->nreal.p);
+    k_bbox<<<blocks(nc, 128), 128, 0, s>>>(g->cpos.p, g->fill.p, nc, m, g->bbox.p, g->zr.p, g->bbf.p, g->nreal.p);
   }
   if ((e = cudaGetLastError())) return fail(e);
   wpos.release(s); cell.release(s); col_count.release(s); col_atom_first.release(s);
@@ -354,6 +374,6 @@ extern "C" void nbx_grid_free(nbx_grid_t* g) {
   cudaStream_t s = 0;
   g->perm.release(s); g->inverse_perm.release(s); g->fill.release(s);
   g->cell_of_cluster.release(s); g->col_first.release(s); g->cpos.release(s);
-  g->bbox.release(s); g->nreal.release(s);
+  g->bbox.release(s); g->zr.release(s); g->bbf.release(s); g->nreal.release(s);
   delete g;
 }

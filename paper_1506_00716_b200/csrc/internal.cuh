@@ -3,10 +3,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 #include "nbx.h"
 
 namespace nbx {
+
+// Keep freed stream-ordered memory in the device pool across syncs (the
+// default release threshold of 0 returns it to the driver at every sync and
+// makes the next cudaMallocAsync re-map pages -- milliseconds per rebuild).
+void ensure_pool();
 
 // Device buffer with stream-ordered allocation.
 template <typename T>
@@ -17,6 +24,7 @@ struct DBuf {
     release(s);
     n = count;
     if (count <= 0) return cudaSuccess;
+    ensure_pool();
     return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, s);
   }
   void release(cudaStream_t s) {
@@ -40,6 +48,8 @@ struct Grid {
   DBuf<int32_t> col_first;      // (cells^2 + 1) first cluster of each column
   DBuf<double> cpos;            // (n_slots, 3) wrapped build-time positions
   DBuf<double> bbox;            // (n_clusters, 6) lo xyz, hi xyz
+  DBuf<float2> zr;              // (n_clusters) z range rounded outward (search prefilter)
+  DBuf<float4> bbf;             // (n_clusters, 2) FP32 box rounded outward (search)
   DBuf<int8_t> nreal;           // (n_clusters) real (non-filler) slots
   int64_t n_slots() const { return n_clusters * m; }
 };
@@ -53,7 +63,7 @@ struct ForceWork {
   DBuf<double> e_grp;     // (2 * n_work_groups) per-group energies
   DBuf<unsigned int> scalars;   // [0] max displacement bits, [1..2] bad key (u64)
   DBuf<float4> lj;        // (t*t) {6 c6, 12 c12, shift_lj, 0}
-  int64_t lj_types = -1;
+  std::vector<double> lj_key;  // host copy of what `lj` was built from (skip re-uploads)
   // transposed index: entries (or rows) sorted by j-cluster
   DBuf<int32_t> t_first;  // (n_clusters + 1)
   DBuf<int32_t> t_items;  // (n_entries)

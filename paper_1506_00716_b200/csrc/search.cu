@@ -51,6 +51,12 @@ __device__ __forceinline__ Ranges col_ranges(double lo, double hi, double r, dou
   return R;
 }
 
+__host__ __device__ constexpr uint64_t column_mask_u64(int m) {
+  uint64_t c = 0;
+  for (int a = 0; a < m; ++a) c |= 1ull << (a * m);
+  return c;
+}
+
 __device__ __forceinline__ uint64_t row_mask(int m, int nr_i, int nr_j, bool diag) {
   uint64_t jb = (nr_j >= 64) ? ~0ull : ((1ull << nr_j) - 1ull);
   uint64_t mk = 0;
@@ -80,18 +86,20 @@ __device__ __forceinline__ void image_delta(const double* bi, const double* oi, 
     const double s = box.L[d] - (bi[3 + d] - bi[d]) - (bj[3 + d] - bj[d]);
     sl = fmin(sl, s);
   }
-  *delta = make_float4((float)dl[0], (float)dl[1], (float)dl[2], 0.f);
+  *delta = make_float4((float)dl[0], (float)dl[1], (float)dl[2], (float)sl);
   *slack = (float)sl;
 }
 
 constexpr int SEARCH_WARPS = 4;
 constexpr int GMAX = 16;
+constexpr int STASH = 1024;  // hits kept per group between the two passes
 
 struct SearchOut {
-  // counting pass
+  // pass 1
   int32_t* row_count;   // (n_clusters)
   int32_t* ent_count;   // (n_groups)
-  // writing pass
+  int2* stash;          // (n_groups * STASH) {cj, member bits}
+  // pass 2
   const int32_t* offsets;
   const int32_t* ent_offsets;
   int32_t* j;
@@ -105,116 +113,210 @@ struct SearchOut {
   uint64_t* ent_mask;
 };
 
-template <bool WRITE>
+// FP32 periodic gap of one dimension (same formula as gap_1d)
+__device__ __forceinline__ float gap1f(float lo_i, float hi_i, float lo_j, float hi_j, float L) {
+  const float a = lo_j - hi_i, b = lo_i - hi_j;
+  const float g0 = fmaxf(0.f, fmaxf(a, b));
+  const float gm = fmaxf(0.f, fmaxf(a - L, b + L));
+  const float gp = fmaxf(0.f, fmaxf(a + L, b - L));
+  return fminf(g0, fminf(gm, gp));
+}
+
+struct SearchCtx {
+  int32_t first;
+  int nmem;
+  double r2;
+  float r2_lo, r2_hi;          // FP32 decision band around r_list^2
+  float Lf[3];
+  const double* bbox;
+  const float4* bbf;            // (n_clusters * 2) outward-rounded FP32 boxes
+};
+
+// Member bits of candidate cj: FP32 gap^2 decides outside +-1e-4 r^2 (boxes
+// rounded outward; the band covers FP32 rounding), the exact FP64 replay of
+// gridder.py:165-185 decides inside it.
+__device__ __forceinline__ uint32_t member_bits(const SearchCtx& C, const float4 (*s_bf)[2],
+                                                const double (*s_bb)[6], int32_t cj, const Box& box) {
+  const float4 lo = __ldg(C.bbf + 2 * (int64_t)cj), hi = __ldg(C.bbf + 2 * (int64_t)cj + 1);
+  uint32_t bits = 0;
+  for (int k = 0; k < C.nmem; ++k) {
+    if (cj < C.first + k) break;
+    const float gx = gap1f(s_bf[k][0].x, s_bf[k][1].x, lo.x, hi.x, C.Lf[0]);
+    const float gy = gap1f(s_bf[k][0].y, s_bf[k][1].y, lo.y, hi.y, C.Lf[1]);
+    const float gz = gap1f(s_bf[k][0].z, s_bf[k][1].z, lo.z, hi.z, C.Lf[2]);
+    const float g2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+    bool in;
+    if (g2 < C.r2_lo) in = true;
+    else if (g2 > C.r2_hi) in = false;
+    else {
+      double bj[6];
+      for (int d = 0; d < 6; ++d) bj[d] = C.bbox[6 * (int64_t)cj + d];
+      in = gap_sq(s_bb[k], bj, box) <= C.r2;
+    }
+    bits |= (in ? 1u : 0u) << k;
+  }
+  return bits;
+}
+
+// Emit one batch of hits (ascending cj across lanes): canonical rows of every
+// member (CSR position = member offset + running count) and the group entry.
+__device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx& C, const double (*s_bb)[6],
+                                           const double* gb, int32_t cj, uint32_t bits, int lane,
+                                           int32_t& cnt, int32_t& ecnt, int32_t row_base, int32_t ent_base,
+                                           int m, const int8_t* nreal, const Box& box) {
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
+  if (!eb) return;
+  const int ent_pos = ent_base + ecnt + __popc(eb & lt);
+  const int W = (m == 8) ? 2 : 1;
+  uint64_t emask[2] = {0ull, 0ull};
+  double bj[6];
+  if (bits)
+    for (int d = 0; d < 6; ++d) bj[d] = C.bbox[6 * (int64_t)cj + d];
+  for (int k = 0; k < C.nmem; ++k) {
+    const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+    if (!b) continue;
+    const int32_t before = __shfl_sync(0xffffffffu, cnt, k);
+    const int32_t rbase = __shfl_sync(0xffffffffu, row_base, k);
+    if ((bits >> k) & 1u) {
+      const int32_t ci = C.first + k;
+      const int64_t row = (int64_t)rbase + before + __popc(b & lt);
+      const uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
+      out.j[row] = cj;
+      out.mask[row] = mk;
+      float4 rdelta;
+      float rslack;
+      image_delta(s_bb[k], s_bb[k], bj, box, &rdelta, &rslack);
+      out.delta[row] = rdelta;
+      out.slack[row] = rslack;
+      out.row_entry[row] = ent_pos;
+      if (W == 2) emask[k] = mk;
+      else emask[0] |= mk << (k * m * m);
+    }
+    if (lane == k) cnt += __popc(b);
+  }
+  if (bits) {
+    float4 e_delta;
+    float e_slack;
+    image_delta(gb, s_bb[0], bj, box, &e_delta, &e_slack);
+    out.ent_j[ent_pos] = cj;
+    out.ent_delta[ent_pos] = e_delta;
+    out.ent_slack[ent_pos] = e_slack;
+    out.ent_mask[(int64_t)ent_pos * W] = emask[0];
+    if (W == 2) out.ent_mask[(int64_t)ent_pos * W + 1] = emask[1];
+  }
+  ecnt += __popc(eb);
+}
+
+// MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
+// by re-running the search for groups whose hits overflowed it).
+template <int MODE>
 __global__ void __launch_bounds__(SEARCH_WARPS * 32)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
-         int64_t n_groups, int m, int G, const double* __restrict__ bbox,
-         const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first, int64_t cells,
-         Box box, double r_list, SearchOut out) {
+         int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
+         const float2* __restrict__ zr, const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first,
+         int64_t cells, Box box, double r_list, SearchOut out) {
   __shared__ double s_bb[SEARCH_WARPS][GMAX][6];
+  __shared__ float4 s_bf[SEARCH_WARPS][GMAX][2];
+  __shared__ int32_t s_q[SEARCH_WARPS][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = blockIdx.x * (int64_t)SEARCH_WARPS + w;
   if (g >= n_groups) return;
-  const int32_t first = group_first[g];
-  const int nmem = group_nmem[g];
-  if (lane < nmem)
-    for (int d = 0; d < 6; ++d) s_bb[w][lane][d] = bbox[6 * (int64_t)(first + lane) + d];
+  SearchCtx C;
+  C.first = group_first[g];
+  C.nmem = group_nmem[g];
+  C.r2 = __dmul_rn(r_list, r_list);
+  C.r2_lo = (float)(C.r2 * (1.0 - 1e-4));
+  C.r2_hi = (float)(C.r2 * (1.0 + 1e-4));
+  for (int d = 0; d < 3; ++d) C.Lf[d] = (float)box.L[d];
+  C.bbox = bbox;
+  C.bbf = bbf;
+  if (lane < C.nmem) {
+    for (int d = 0; d < 6; ++d) s_bb[w][lane][d] = bbox[6 * (int64_t)(C.first + lane) + d];
+    s_bf[w][lane][0] = bbf[2 * (int64_t)(C.first + lane)];
+    s_bf[w][lane][1] = bbf[2 * (int64_t)(C.first + lane) + 1];
+  }
   __syncwarp();
   double gb[6];  // group AABB
   for (int d = 0; d < 3; ++d) {
     gb[d] = s_bb[w][0][d];
     gb[3 + d] = s_bb[w][0][3 + d];
-    for (int k = 1; k < nmem; ++k) {
+    for (int k = 1; k < C.nmem; ++k) {
       gb[d] = fmin(gb[d], s_bb[w][k][d]);
       gb[3 + d] = fmax(gb[3 + d], s_bb[w][k][3 + d]);
     }
   }
-  const double r2 = __dmul_rn(r_list, r_list);
-  // conservative FP64-free prefilter margin (exact test follows)
-  const float r2_pre = (float)(r2 * (1.0 + 1e-4)) + 1e-6f;
+  int32_t cnt = 0, ecnt = 0, row_base = 0, ent_base = 0;
+  int2* stash = out.stash + g * (int64_t)STASH;
+  if (MODE == 1) {
+    if (lane < C.nmem) row_base = out.offsets[C.first + lane];
+    ent_base = out.ent_offsets[g];
+    const int32_t nst = out.ent_count[g];  // hits of this group (== its entry count)
+    if (nst <= STASH) {
+      for (int32_t base = 0; base < nst; base += 32) {
+        int2 h = make_int2(0, 0);
+        if (base + lane < nst) h = stash[base + lane];
+        emit_batch(out, C, s_bb[w], gb, h.x, (uint32_t)h.y, lane, cnt, ecnt, row_base, ent_base, m, nreal, box);
+      }
+      return;
+    }
+  }
+  const float r2_pre = (float)(C.r2 * (1.0 + 1e-4)) + 1e-5f;
+  const float gzlo = __double2float_rd(gb[2]), gzhi = __double2float_ru(gb[5]);
   const double wx = box.L[0] / (double)cells, wy = box.L[1] / (double)cells;
   Ranges RX = col_ranges(gb[0], gb[3], r_list, wx, cells);
   Ranges RY = col_ranges(gb[1], gb[4], r_list, wy, cells);
-
-  int32_t cnt = 0;   // lane k < nmem: rows emitted for member k
-  int32_t ecnt = 0;  // entries emitted (uniform)
-  int32_t row_base = 0, ent_base = 0;
-  if (WRITE) {
-    if (lane < nmem) row_base = out.offsets[first + lane];
-    ent_base = out.ent_offsets[g];
-  }
   const unsigned lt = (1u << lane) - 1u;
-  const int W = (m == 8) ? 2 : 1;
+  int qn = 0;  // queued z-survivors (warp-uniform)
+
+  auto process = [&](int n_items) {  // the first n_items of the queue
+    const int32_t cj = lane < n_items ? s_q[w][lane] : 0;
+    const uint32_t bits = lane < n_items ? member_bits(C, s_bf[w], s_bb[w], cj, box) : 0u;
+    if (MODE == 0) {
+      const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
+      for (int k = 0; k < C.nmem; ++k) {
+        const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+        if (lane == k) cnt += __popc(b);
+      }
+      if (bits && ecnt + __popc(eb & lt) < STASH) stash[ecnt + __popc(eb & lt)] = make_int2(cj, (int)bits);
+      ecnt += __popc(eb);
+    } else {
+      emit_batch(out, C, s_bb[w], gb, cj, bits, lane, cnt, ecnt, row_base, ent_base, m, nreal, box);
+    }
+  };
 
   for (int sx = 0; sx < RX.n; ++sx) {
     for (int64_t ix = RX.lo[sx]; ix <= RX.hi[sx]; ++ix) {
       for (int sy = 0; sy < RY.n; ++sy) {
         const int32_t c0 = col_first[ix * cells + RY.lo[sy]];
         const int32_t c1 = col_first[ix * cells + RY.hi[sy] + 1];
-        int32_t start = c0 > first ? c0 : first;
+        const int32_t start = c0 > C.first ? c0 : C.first;
         for (int32_t base = start; base < c1; base += 32) {
           const int32_t cj = base + lane;
-          uint32_t bits = 0;
-          double bj[6];
-          if (cj < c1) {
-            for (int d = 0; d < 6; ++d) bj[d] = bbox[6 * (int64_t)cj + d];
-            // prefilter on the group box (FP32, conservative)
-            float pre = 0.f;
-            for (int d = 0; d < 3; ++d) {
-              float gg = (float)gap_1d(gb[d], gb[3 + d], bj[d], bj[3 + d], box.L[d]);
-              pre += gg * gg;
-            }
-            if (pre <= r2_pre) {
-              for (int k = 0; k < nmem; ++k) {
-                if (cj >= first + k && gap_sq(s_bb[w][k], bj, box) <= r2) bits |= 1u << k;
-              }
-            }
+          bool keep = false;
+          if (cj < c1) {  // conservative FP32 z prefilter against the whole group
+            const float2 z = __ldg(zr + cj);
+            const float gz = gap1f(gzlo, gzhi, z.x, z.y, C.Lf[2]);
+            keep = gz * gz <= r2_pre;
           }
-          const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
-          if (eb == 0) continue;
-          int ent_pos = ent_base + ecnt + __popc(eb & lt);
-          uint64_t emask[2] = {0ull, 0ull};
-          float4 e_delta = make_float4(0.f, 0.f, 0.f, 0.f);
-          float e_slack = 0.f;
-          if (WRITE && bits) image_delta(gb, s_bb[w][0], bj, box, &e_delta, &e_slack);
-          for (int k = 0; k < nmem; ++k) {
-            const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
-            if (!b) continue;
-            if (WRITE) {
-              const int32_t before = __shfl_sync(0xffffffffu, cnt, k);
-              const int32_t rbase = __shfl_sync(0xffffffffu, row_base, k);
-              if ((bits >> k) & 1u) {
-                const int32_t ci = first + k;
-                const int64_t row = (int64_t)rbase + before + __popc(b & lt);
-                const uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
-                out.j[row] = cj;
-                out.mask[row] = mk;
-                float4 rdelta;
-                float rslack;
-                image_delta(s_bb[w][k], s_bb[w][k], bj, box, &rdelta, &rslack);
-                out.delta[row] = rdelta;
-                out.slack[row] = rslack;
-                out.row_entry[row] = ent_pos;
-                if (W == 2) emask[k] = mk;
-                else emask[0] |= mk << (k * m * m);
-              }
-            }
-            if (lane == k) cnt += __popc(b);
+          const unsigned kb = __ballot_sync(0xffffffffu, keep);
+          if (keep) s_q[w][qn + __popc(kb & lt)] = cj;
+          qn += __popc(kb);
+          __syncwarp();
+          if (qn >= 32) {
+            process(32);
+            __syncwarp();
+            if (lane < qn - 32) s_q[w][lane] = s_q[w][32 + lane];
+            qn -= 32;
+            __syncwarp();
           }
-          if (WRITE && bits) {
-            out.ent_j[ent_pos] = cj;
-            out.ent_delta[ent_pos] = e_delta;
-            out.ent_slack[ent_pos] = e_slack;
-            out.ent_mask[(int64_t)ent_pos * W] = emask[0];
-            if (W == 2) out.ent_mask[(int64_t)ent_pos * W + 1] = emask[1];
-          }
-          ecnt += __popc(eb);
         }
       }
     }
   }
-  if (!WRITE) {
-    if (lane < nmem) out.row_count[first + lane] = cnt;
+  if (qn > 0) process(qn);
+  if (MODE == 0) {
+    if (lane < C.nmem) out.row_count[C.first + lane] = cnt;
     if (lane == 0) out.ent_count[g] = ecnt;
   }
 }
@@ -276,81 +378,130 @@ __device__ __forceinline__ bool within_exact(const double* __restrict__ pos, int
 
 constexpr int ROWS_WARPS = 4;
 
-// Prune (pairlist.py:242-282): one warp per i-cluster, lanes over its rows.
-// Removed rows clear their member bits in the (copied) entry masks; kept rows
-// mark their entry alive.
+// Positions for the row kernels: FP32, relative to the cluster's first slot
+// (small magnitudes -> ~1e-7 nm resolution; the origin offsets between two
+// clusters are formed in FP64).
+__global__ void k_local_coords(const double* __restrict__ pos, int64_t n_slots, int m, float4* __restrict__ xl) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  const int64_t o = (s / m) * m;
+  xl[s] = make_float4((float)(pos[3 * s] - pos[3 * o]), (float)(pos[3 * s + 1] - pos[3 * o + 1]),
+                      (float)(pos[3 * s + 2] - pos[3 * o + 2]), 0.f);
+}
+
+// Row kernels (prune: pairlist.py:242-282, count: pairlist.py:303-320): one
+// warp per i-cluster, lane = (row slot r of 32/m, j-atom b).  i-atoms live in
+// registers, j-atoms are coalesced float4 loads.  Each admitted pair's
+// d^2 <= r^2 is decided by the FP32 estimate outside +-1e-4 relative of r^2
+// and by the exact FP64 replay (min_image_np + einsum order) inside it.
+template <int M, int MODE>  // MODE 0: prune, 1: count within
 __global__ void __launch_bounds__(ROWS_WARPS * 32)
-k_prune(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv,
-        const uint64_t* __restrict__ mask, const int32_t* __restrict__ row_entry,
-        int64_t n_clusters, int m, int G, const double* __restrict__ pos, Box box, double r2,
-        const int32_t* __restrict__ cell_of_cluster, const int32_t* __restrict__ col_first,
-        int32_t* __restrict__ keep, uint64_t* __restrict__ ent_mask, int32_t* __restrict__ ent_alive) {
+k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, const uint64_t* __restrict__ mask,
+       const int32_t* __restrict__ row_entry, int64_t n_clusters, int G, const double* __restrict__ pos,
+       const float4* __restrict__ xl, Box box, double r2,
+       const int32_t* __restrict__ cell_of_cluster, const int32_t* __restrict__ col_first,
+       int32_t* __restrict__ keep, uint64_t* __restrict__ ent_mask, int32_t* __restrict__ ent_alive,
+       unsigned long long* __restrict__ counts) {
+  constexpr int R = 32 / M;
   const int64_t ci = blockIdx.x * (int64_t)ROWS_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (ci >= n_clusters) return;
+  const int r = lane / M, b = lane % M;
+  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
   const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
   const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
-  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
-  const int k = (int)((ci - col_first[cell_of_cluster[ci]]) % G);
-  const int W = (m == 8) ? 2 : 1;
-  for (int32_t row = offsets[ci] + lane; row < offsets[ci + 1]; row += 32) {
-    const int32_t cj = jv[row];
-    const uint64_t mk = mask[row];
-    bool kp = (cj == ci);
-    if (!kp) {
-      for (int a = 0; a < m && !kp; ++a)
-        for (int b = 0; b < m; ++b) {
-          if (!((mk >> (a * m + b)) & 1ull)) continue;
-          if (within_exact(pos, ci * m + a, (int64_t)cj * m + b, box, r2, lo, hi, Lf, iLf)) {
-            kp = true;
-            break;
-          }
+  float4 xi[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) xi[a] = __ldg(xl + ci * M + a);
+  const double oi[3] = {pos[3 * ci * M], pos[3 * ci * M + 1], pos[3 * ci * M + 2]};
+  const int W = (M == 8) ? 2 : 1;
+  const int k = MODE == 0 ? (int)((ci - col_first[cell_of_cluster[ci]]) % G) : 0;
+  unsigned long long adm = 0, win = 0;
+  const int32_t r0 = offsets[ci], r1 = offsets[ci + 1];
+  for (int32_t base = r0; base < r1; base += R) {
+    const int32_t row = base + r;
+    const bool valid = row < r1;
+    bool any = false;
+    int32_t cj = -1;
+    uint64_t mk = 0;
+    if (valid) {
+      cj = jv[row];
+      mk = mask[row];
+      const float4 xj = __ldg(xl + (int64_t)cj * M + b);
+      const int64_t oj = 3 * (int64_t)cj * M;
+      const float ox = (float)(oi[0] - pos[oj]);
+      const float oy = (float)(oi[1] - pos[oj + 1]);
+      const float oz = (float)(oi[2] - pos[oj + 2]);
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        if (!((mk >> (a * M + b)) & 1ull)) continue;
+        if (MODE == 0 && any) break;
+        float dx = xi[a].x - xj.x + ox, dy = xi[a].y - xj.y + oy, dz = xi[a].z - xj.z + oz;
+        dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
+        dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
+        dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
+        const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        bool in;
+        if (f < lo) in = true;
+        else if (f > hi) in = false;
+        else {
+          const int64_t si = ci * M + a, sj = (int64_t)cj * M + b;
+          const double ex = min_image_np(__dsub_rn(pos[3 * si], pos[3 * sj]), box.L[0], box.invL[0]);
+          const double ey = min_image_np(__dsub_rn(pos[3 * si + 1], pos[3 * sj + 1]), box.L[1], box.invL[1]);
+          const double ez = min_image_np(__dsub_rn(pos[3 * si + 2], pos[3 * sj + 2]), box.L[2], box.invL[2]);
+          in = d2_einsum(ex, ey, ez) <= r2;
         }
-    }
-    keep[row] = kp ? 1 : 0;
-    const int32_t e = row_entry[row];
-    if (kp) {
-      ent_alive[e] = 1;
-    } else if (mk) {
-      if (W == 2) {
-        atomicAnd((unsigned long long*)&ent_mask[(int64_t)e * 2 + k], 0ull);
-      } else {
-        atomicAnd((unsigned long long*)&ent_mask[e], ~(unsigned long long)(mk << (k * m * m)));
+        any |= in;
+        if (MODE == 1) win += in;
       }
+      if (MODE == 1) adm += __popcll(mk & (column_mask_u64(M) << b));
+    }
+    if (MODE == 0) {
+      // row decision: any pair of the row's m lanes within r_list (or diagonal)
+      const unsigned bal = __ballot_sync(0xffffffffu, any);
+      const unsigned seg = ((M == 32) ? 0xffffffffu : ((1u << M) - 1u)) << (r * M);
+      const bool kp = (cj == ci) || (bal & seg) != 0u;
+      if (valid && b == 0) {
+        keep[row] = kp ? 1 : 0;
+        const int32_t e = row_entry[row];
+        if (kp) {
+          ent_alive[e] = 1;
+        } else if (mk) {
+          if (W == 2) atomicAnd((unsigned long long*)&ent_mask[(int64_t)e * 2 + k], 0ull);
+          else atomicAnd((unsigned long long*)&ent_mask[e], ~(unsigned long long)(mk << (k * M * M)));
+        }
+      }
+    }
+  }
+  if (MODE == 1) {
+    for (int o = 16; o; o >>= 1) {
+      adm += __shfl_xor_sync(0xffffffffu, adm, o);
+      win += __shfl_xor_sync(0xffffffffu, win, o);
+    }
+    if (lane == 0 && (adm || win)) {
+      atomicAdd(&counts[0], adm);
+      atomicAdd(&counts[1], win);
     }
   }
 }
 
-// interaction_stats (pairlist.py:323-346): admitted + within-r_cut counts.
-__global__ void __launch_bounds__(ROWS_WARPS * 32)
-k_count_within(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv,
-               const uint64_t* __restrict__ mask, int64_t n_clusters, int m,
-               const double* __restrict__ pos, Box box, double r2,
-               unsigned long long* __restrict__ counts) {
-  const int64_t ci = blockIdx.x * (int64_t)ROWS_WARPS + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (ci >= n_clusters) return;
-  const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
-  const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
-  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
-  unsigned long long adm = 0, win = 0;
-  for (int32_t row = offsets[ci] + lane; row < offsets[ci + 1]; row += 32) {
-    const int32_t cj = jv[row];
-    const uint64_t mk = mask[row];
-    adm += __popcll(mk);
-    for (int a = 0; a < m; ++a)
-      for (int b = 0; b < m; ++b)
-        if ((mk >> (a * m + b)) & 1ull)
-          win += within_exact(pos, ci * m + a, (int64_t)cj * m + b, box, r2, lo, hi, Lf, iLf);
+template <int MODE>
+static void launch_rows(int m, int64_t nc, cudaStream_t s, const int32_t* offsets, const int32_t* jv,
+                        const uint64_t* mask, const int32_t* row_entry, int G, const double* pos, const float4* xl,
+                        Box box, double r2, const int32_t* coc, const int32_t* col_first,
+                        int32_t* keep, uint64_t* ent_mask, int32_t* ent_alive, unsigned long long* counts) {
+  const int blocks = (int)((nc + ROWS_WARPS - 1) / ROWS_WARPS);
+  count_launch();
+#define NBX_ROWS(MM)                                                                                         \
+  k_rows<MM, MODE><<<blocks, ROWS_WARPS * 32, 0, s>>>(offsets, jv, mask, row_entry, nc, G, pos, xl, box, r2, \
+                                                      coc, col_first, keep, ent_mask, ent_alive, counts)
+  switch (m) {
+    case 1: NBX_ROWS(1); break;
+    case 2: NBX_ROWS(2); break;
+    case 4: NBX_ROWS(4); break;
+    default: NBX_ROWS(8); break;
   }
-  for (int o = 16; o; o >>= 1) {
-    adm += __shfl_xor_sync(0xffffffffu, adm, o);
-    win += __shfl_xor_sync(0xffffffffu, win, o);
-  }
-  if (lane == 0 && (adm || win)) {
-    atomicAdd(&counts[0], adm);
-    atomicAdd(&counts[1], win);
-  }
+#undef NBX_ROWS
 }
 
 // ---------------------------------------------------------------- compaction helpers
@@ -472,14 +623,26 @@ k_entry_order(const int32_t* __restrict__ ent_off, int64_t n_groups, const uint6
   }
   for (int t = lane; t < n; t += 32) s_key[w][t] = entry_pattern(emask, e0 + t, m, G);
   __syncwarp();
-  for (int t = lane; t < n; t += 32) {
-    const uint32_t k = s_key[w][t];
-    int32_t rank = 0;
-    for (int u = 0; u < n; ++u) {
-      const uint32_t ku = s_key[w][u];
-      rank += (ku < k) || (ku == k && u < t);
+  // stable counting order: repeatedly extract the smallest remaining key and
+  // place its entries in index order (iterations = distinct patterns)
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t placed = 0;
+  int64_t prev = -1;
+  while (placed < n) {
+    uint32_t mn = 0xffffffffu;
+    for (int t = lane; t < n; t += 32) {
+      const uint32_t k = s_key[w][t];
+      if ((int64_t)k > prev && k < mn) mn = k;
     }
-    newpos[e0 + t] = e0 + rank;
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    for (int base = 0; base < n; base += 32) {
+      const int t = base + lane;
+      const bool hit = t < n && s_key[w][t] == mn;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) newpos[e0 + t] = e0 + placed + __popc(bal & lt);
+      placed += __popc(bal);
+    }
+    prev = mn;
   }
 }
 
@@ -596,6 +759,7 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   for (int d = 0; d < 3; ++d) l->L[d] = box[d];
   Box bx = make_box(box);
   DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
+  DBuf<int2> stash;
   int32_t h[2] = {0, 0};
   SearchOut so{};
   TRY(ng.alloc(n_cols + 1, s));
@@ -614,17 +778,20 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   TRY(ent_count.alloc(l->n_groups + 1, s));
   TRY(cudaMemsetAsync(row_count.p, 0, 4 * (nc + 1), s));
   TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
+  TRY(stash.alloc(l->n_groups * (int64_t)STASH, s));
   so.row_count = row_count.p;
   so.ent_count = ent_count.p;
+  so.stash = stash.p;
   if (l->n_groups > 0)
-    count_launch(), k_search<false><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
-        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->nreal.p,
-        grid->col_first.p, grid->cells, bx, r_list, so);
+    count_launch(), k_search<0><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
+        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so);
   TRY(cudaGetLastError());
   TRY(l->offsets.alloc(nc + 1, s));
   TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
   TRY(exclusive_scan_i32(row_count.p, l->offsets.p, nc + 1, s));
   TRY(exclusive_scan_i32(ent_count.p, l->ent_offsets.p, l->n_groups + 1, s));
+  so.ent_count = ent_count.p;  // per-group hit counts (read by the emit pass)
   TRY(cudaMemcpyAsync(&h[0], l->offsets.p + nc, 4, cudaMemcpyDeviceToHost, s));
   TRY(cudaMemcpyAsync(&h[1], l->ent_offsets.p + l->n_groups, 4, cudaMemcpyDeviceToHost, s));
   TRY(cudaStreamSynchronize(s));
@@ -651,16 +818,16 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   so.ent_slack = l->ent_slack.p;
   so.ent_mask = l->ent_mask.p;
   if (l->n_groups > 0)
-    count_launch(), k_search<true><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
-        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->nreal.p,
-        grid->col_first.p, grid->cells, bx, r_list, so);
+    count_launch(), k_search<1><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+        l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
+        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so);
   TRY(cudaGetLastError());
   TRY(order_entries(l, s));
-  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s);
+  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s);
+  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }
@@ -690,6 +857,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   Box bx = make_box(box);
   DBuf<int32_t> keep, scan, alive, escan;
   DBuf<uint64_t> emask;
+  DBuf<float4> xl;
   int32_t h[2] = {0, 0};
   TRY(keep.alloc(nr + 1, s));
   TRY(scan.alloc(nr + 1, s));
@@ -699,10 +867,14 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(cudaMemsetAsync(keep.p, 0, 4 * (nr + 1), s));
   TRY(cudaMemsetAsync(alive.p, 0, 4 * (ne + 1), s));
   if (ne) TRY(cudaMemcpyAsync(emask.p, in->ent_mask.p, 8 * ne * W, cudaMemcpyDeviceToDevice, s));
-  if (nc > 0)
-    count_launch(), k_prune<<<nb(nc, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(
-        in->offsets.p, in->j.p, in->mask.p, in->row_entry.p, nc, in->m, in->G, pos, bx,
-        in->r_list * in->r_list, grid->cell_of_cluster.p, grid->col_first.p, keep.p, emask.p, alive.p);
+  TRY(xl.alloc(nc * in->m, s));
+  if (nc > 0) {
+    count_launch();
+    k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, nc * in->m, in->m, xl.p);
+    launch_rows<0>(in->m, nc, s, in->offsets.p, in->j.p, in->mask.p, in->row_entry.p, in->G, pos, xl.p,
+                   bx, in->r_list * in->r_list, grid->cell_of_cluster.p, grid->col_first.p, keep.p,
+                   emask.p, alive.p, nullptr);
+  }
   TRY(cudaGetLastError());
   TRY(exclusive_scan_i32(keep.p, scan.p, nr + 1, s));
   TRY(exclusive_scan_i32(alive.p, escan.p, ne + 1, s));
@@ -741,11 +913,11 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
                                                   l->ent_slack.p, l->ent_mask.p);
   TRY(cudaGetLastError());
   TRY(order_entries(l, s));
-  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s);
+  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s);
+  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }
@@ -799,21 +971,28 @@ extern "C" int nbx_count_within(const nbx_list_t* l, const double* pos, const do
   }
   cudaStream_t s = to_stream(stream);
   DBuf<unsigned long long> cnt;
+  DBuf<float4> xl;
   unsigned long long h[2] = {0, 0};
   TRY(cnt.alloc(2, s));
+  TRY(xl.alloc(l->n_clusters * l->m, s));
   TRY(cudaMemsetAsync(cnt.p, 0, 16, s));
-  if (l->n_clusters > 0)
-    count_launch(), k_count_within<<<nb(l->n_clusters, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(
-        l->offsets.p, l->j.p, l->mask.p, l->n_clusters, l->m, pos, make_box(box), r_cut * r_cut, cnt.p);
+  if (l->n_clusters > 0) {
+    count_launch();
+    k_local_coords<<<nb(l->n_clusters * l->m, 256), 256, 0, s>>>(pos, l->n_clusters * l->m, l->m, xl.p);
+    launch_rows<1>(l->m, l->n_clusters, s, l->offsets.p, l->j.p, l->mask.p, nullptr, l->G, pos, xl.p,
+                   make_box(box), r_cut * r_cut, nullptr, nullptr, nullptr, nullptr, nullptr, cnt.p);
+  }
   TRY(cudaGetLastError());
   TRY(cudaMemcpyAsync(h, cnt.p, 16, cudaMemcpyDeviceToHost, s));
   TRY(cudaStreamSynchronize(s));
   cnt.release(s);
+  xl.release(s);
   out[0] = (int64_t)h[0];
   out[1] = (int64_t)h[1];
   return NBX_OK;
 fail:
   cnt.release(s);
+  xl.release(s);
   return NBX_ERR_CUDA;
 }
 
