@@ -24,7 +24,10 @@ def to_device(a, dtype: torch.dtype, shape=None) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         t = a.to(device=dev, dtype=dtype)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=_np_dtype(dtype))))
+        arr = np.ascontiguousarray(np.asarray(a, dtype=_np_dtype(dtype)))
+        if not arr.flags.writeable:
+            arr = arr.copy()
+        t = torch.from_numpy(arr)
         t = t.to(device=dev, non_blocking=False)
     if shape is not None:
         t = t.reshape(shape)

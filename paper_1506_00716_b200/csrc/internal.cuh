@@ -85,6 +85,7 @@ struct List {
   int64_t n_entries = 0;
   double r_list = 0.0;
   double L[3] = {0, 0, 0};
+  const double* bbox = nullptr;  // the grid's boxes (frame of `delta`); the grid outlives its lists
   // canonical CSR
   DBuf<int32_t> offsets;    // (n_clusters + 1)
   DBuf<int32_t> j;          // (n_rows)

@@ -132,6 +132,14 @@ struct SearchCtx {
   const float4* bbf;            // (n_clusters * 2) outward-rounded FP32 boxes
 };
 
+// exact FP64 AABB test of gridder.py:165-185 (rare: FP32 ambiguity band)
+__device__ __noinline__ bool exact_gap_within(const double* bi, const double* __restrict__ bbox, int32_t cj,
+                                              Box box, double r2) {
+  double bj[6];
+  for (int d = 0; d < 6; ++d) bj[d] = bbox[6 * (int64_t)cj + d];
+  return gap_sq(bi, bj, box) <= r2;
+}
+
 // Member bits of candidate cj: FP32 gap^2 decides outside +-1e-4 r^2 (boxes
 // rounded outward; the band covers FP32 rounding), the exact FP64 replay of
 // gridder.py:165-185 decides inside it.
@@ -148,11 +156,7 @@ __device__ __forceinline__ uint32_t member_bits(const SearchCtx& C, const float4
     bool in;
     if (g2 < C.r2_lo) in = true;
     else if (g2 > C.r2_hi) in = false;
-    else {
-      double bj[6];
-      for (int d = 0; d < 6; ++d) bj[d] = C.bbox[6 * (int64_t)cj + d];
-      in = gap_sq(s_bb[k], bj, box) <= C.r2;
-    }
+    else in = exact_gap_within(s_bb[k], C.bbox, cj, box, C.r2);
     bits |= (in ? 1u : 0u) << k;
   }
   return bits;
@@ -211,7 +215,7 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
 // MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
 // by re-running the search for groups whose hits overflowed it).
 template <int MODE>
-__global__ void __launch_bounds__(SEARCH_WARPS * 32)
+__global__ void __launch_bounds__(SEARCH_WARPS * 32, 6)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
          int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
          const float2* __restrict__ zr, const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first,
@@ -378,15 +382,25 @@ __device__ __forceinline__ bool within_exact(const double* __restrict__ pos, int
 
 constexpr int ROWS_WARPS = 4;
 
-// Positions for the row kernels: FP32, relative to the cluster's first slot
-// (small magnitudes -> ~1e-7 nm resolution; the origin offsets between two
-// clusters are formed in FP64).
-__global__ void k_local_coords(const double* __restrict__ pos, int64_t n_slots, int m, float4* __restrict__ xl) {
+// Positions for the row kernels: FP32, relative to the cluster's build-time
+// box corner (the frame of the per-row `delta` offsets), ~1e-7 nm resolution.
+__global__ void k_local_coords(const double* __restrict__ pos, const double* __restrict__ bbox, int64_t n_slots,
+                               int m, float4* __restrict__ xl) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n_slots) return;
-  const int64_t o = (s / m) * m;
-  xl[s] = make_float4((float)(pos[3 * s] - pos[3 * o]), (float)(pos[3 * s + 1] - pos[3 * o + 1]),
-                      (float)(pos[3 * s + 2] - pos[3 * o + 2]), 0.f);
+  const int64_t c = s / m;
+  xl[s] = make_float4((float)(pos[3 * s] - bbox[6 * c]), (float)(pos[3 * s + 1] - bbox[6 * c + 1]),
+                      (float)(pos[3 * s + 2] - bbox[6 * c + 2]), 0.f);
+}
+
+// Exact replay of the reference decision d^2 <= r^2 for slots (si, sj)
+// (model.py:159-172 minimum image, pairlist.py:236 einsum order).  Rare.
+__device__ __noinline__ bool exact_within(const double* __restrict__ pos, int64_t si, int64_t sj, Box box,
+                                          double r2) {
+  const double ex = min_image_np(__dsub_rn(pos[3 * si], pos[3 * sj]), box.L[0], box.invL[0]);
+  const double ey = min_image_np(__dsub_rn(pos[3 * si + 1], pos[3 * sj + 1]), box.L[1], box.invL[1]);
+  const double ez = min_image_np(__dsub_rn(pos[3 * si + 2], pos[3 * sj + 2]), box.L[2], box.invL[2]);
+  return d2_einsum(ex, ey, ez) <= r2;
 }
 
 // Row kernels (prune: pairlist.py:242-282, count: pairlist.py:303-320): one
@@ -395,9 +409,9 @@ __global__ void k_local_coords(const double* __restrict__ pos, int64_t n_slots, 
 // d^2 <= r^2 is decided by the FP32 estimate outside +-1e-4 relative of r^2
 // and by the exact FP64 replay (min_image_np + einsum order) inside it.
 template <int M, int MODE>  // MODE 0: prune, 1: count within
-__global__ void __launch_bounds__(ROWS_WARPS * 32)
+__global__ void __launch_bounds__(ROWS_WARPS * 32, 8)
 k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, const uint64_t* __restrict__ mask,
-       const int32_t* __restrict__ row_entry, int64_t n_clusters, int G, const double* __restrict__ pos,
+       const float4* __restrict__ rdelta, const int32_t* __restrict__ row_entry, int64_t n_clusters, int G, const double* __restrict__ pos,
        const float4* __restrict__ xl, Box box, double r2,
        const int32_t* __restrict__ cell_of_cluster, const int32_t* __restrict__ col_first,
        int32_t* __restrict__ keep, uint64_t* __restrict__ ent_mask, int32_t* __restrict__ ent_alive,
@@ -413,44 +427,75 @@ k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, cons
   float4 xi[M];
 #pragma unroll
   for (int a = 0; a < M; ++a) xi[a] = __ldg(xl + ci * M + a);
-  const double oi[3] = {pos[3 * ci * M], pos[3 * ci * M + 1], pos[3 * ci * M + 2]};
   const int W = (M == 8) ? 2 : 1;
   const int k = MODE == 0 ? (int)((ci - col_first[cell_of_cluster[ci]]) % G) : 0;
   unsigned long long adm = 0, win = 0;
   const int32_t r0 = offsets[ci], r1 = offsets[ci + 1];
+  // two-deep software pipeline: row words of batch k+2 and the j-atom of
+  // batch k+1 are in flight while batch k is evaluated
+  int32_t c1 = -1, c2 = -1;       // cj of batches k+1, k+2
+  uint64_t m1 = 0, m2 = 0;
+  float4 d1 = make_float4(0.f, 0.f, 0.f, 0.f), d2 = d1, x0 = d1;
+  auto load_row = [&](int32_t row, int32_t& c, uint64_t& mm, float4& d) {
+    if (row < r1) {
+      c = __ldg(jv + row);
+      mm = __ldg(mask + row);
+      d = __ldg(rdelta + row);
+    }
+  };
+  int32_t c0 = -1;
+  uint64_t m0 = 0;
+  float4 dd0 = d1;
+  load_row(r0 + r, c0, m0, dd0);
+  load_row(r0 + R + r, c1, m1, d1);
+  if (r0 + r < r1) {
+    x0 = __ldg(xl + (int64_t)c0 * M + b);
+    x0.x += dd0.x;
+    x0.y += dd0.y;
+    x0.z += dd0.z;
+  }
   for (int32_t base = r0; base < r1; base += R) {
     const int32_t row = base + r;
     const bool valid = row < r1;
     bool any = false;
-    int32_t cj = -1;
-    uint64_t mk = 0;
+    const int32_t cj = c0;
+    const uint64_t mk = m0;
+    const float4 xj = x0;
+    load_row(row + 2 * R, c2, m2, d2);
+    if (row + R < r1) {
+      x0 = __ldg(xl + (int64_t)c1 * M + b);
+      x0.x += d1.x;
+      x0.y += d1.y;
+      x0.z += d1.z;
+    }
+    c0 = c1;
+    m0 = m1;
+    c1 = c2;
+    m1 = m2;
+    d1 = d2;
     if (valid) {
-      cj = jv[row];
-      mk = mask[row];
-      const float4 xj = __ldg(xl + (int64_t)cj * M + b);
-      const int64_t oj = 3 * (int64_t)cj * M;
-      const float ox = (float)(oi[0] - pos[oj]);
-      const float oy = (float)(oi[1] - pos[oj + 1]);
-      const float oz = (float)(oi[2] - pos[oj + 2]);
+      // FP32 decisions for this lane's M pairs; pairs inside the ambiguity
+      // band are collected and decided exactly afterwards (rare, out of line)
+      const uint32_t cm = (uint32_t)(mk >> b);
+      uint32_t amb = 0;
 #pragma unroll
       for (int a = 0; a < M; ++a) {
-        if (!((mk >> (a * M + b)) & 1ull)) continue;
-        if (MODE == 0 && any) break;
-        float dx = xi[a].x - xj.x + ox, dy = xi[a].y - xj.y + oy, dz = xi[a].z - xj.z + oz;
+        float dx = xi[a].x - xj.x, dy = xi[a].y - xj.y, dz = xi[a].z - xj.z;
         dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
         dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
         dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
         const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        bool in;
-        if (f < lo) in = true;
-        else if (f > hi) in = false;
-        else {
-          const int64_t si = ci * M + a, sj = (int64_t)cj * M + b;
-          const double ex = min_image_np(__dsub_rn(pos[3 * si], pos[3 * sj]), box.L[0], box.invL[0]);
-          const double ey = min_image_np(__dsub_rn(pos[3 * si + 1], pos[3 * sj + 1]), box.L[1], box.invL[1]);
-          const double ez = min_image_np(__dsub_rn(pos[3 * si + 2], pos[3 * sj + 2]), box.L[2], box.invL[2]);
-          in = d2_einsum(ex, ey, ez) <= r2;
-        }
+        const bool adm = (M == 8 && a >= 4) ? (((uint32_t)(mk >> (32 + b)) >> ((a - 4) * M)) & 1u)
+                                            : ((cm >> (a * M)) & 1u);
+        const bool in = adm && f < lo;
+        amb |= (adm && f >= lo && f <= hi) ? (1u << a) : 0u;
+        any |= in;
+        if (MODE == 1) win += in;
+      }
+      while (amb) {
+        const int a = __ffs(amb) - 1;
+        amb &= amb - 1;
+        const bool in = exact_within(pos, ci * M + a, (int64_t)cj * M + b, box, r2);
         any |= in;
         if (MODE == 1) win += in;
       }
@@ -487,13 +532,13 @@ k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, cons
 
 template <int MODE>
 static void launch_rows(int m, int64_t nc, cudaStream_t s, const int32_t* offsets, const int32_t* jv,
-                        const uint64_t* mask, const int32_t* row_entry, int G, const double* pos, const float4* xl,
+                        const uint64_t* mask, const float4* rdelta, const int32_t* row_entry, int G, const double* pos, const float4* xl,
                         Box box, double r2, const int32_t* coc, const int32_t* col_first,
                         int32_t* keep, uint64_t* ent_mask, int32_t* ent_alive, unsigned long long* counts) {
   const int blocks = (int)((nc + ROWS_WARPS - 1) / ROWS_WARPS);
   count_launch();
 #define NBX_ROWS(MM)                                                                                         \
-  k_rows<MM, MODE><<<blocks, ROWS_WARPS * 32, 0, s>>>(offsets, jv, mask, row_entry, nc, G, pos, xl, box, r2, \
+  k_rows<MM, MODE><<<blocks, ROWS_WARPS * 32, 0, s>>>(offsets, jv, mask, rdelta, row_entry, nc, G, pos, xl, box, r2, \
                                                       coc, col_first, keep, ent_mask, ent_alive, counts)
   switch (m) {
     case 1: NBX_ROWS(1); break;
@@ -756,6 +801,7 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   l->G = G;
   l->n_clusters = nc;
   l->r_list = r_list;
+  l->bbox = grid->bbox.p;
   for (int d = 0; d < 3; ++d) l->L[d] = box[d];
   Box bx = make_box(box);
   DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
@@ -851,6 +897,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   l->n_clusters = in->n_clusters;
   l->n_groups = in->n_groups;
   l->r_list = in->r_list;
+  l->bbox = in->bbox;
   for (int d = 0; d < 3; ++d) l->L[d] = in->L[d];
   const int W = in->mask_words();
   const int64_t nr = in->n_rows, ne = in->n_entries, nc = in->n_clusters;
@@ -870,8 +917,8 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(xl.alloc(nc * in->m, s));
   if (nc > 0) {
     count_launch();
-    k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, nc * in->m, in->m, xl.p);
-    launch_rows<0>(in->m, nc, s, in->offsets.p, in->j.p, in->mask.p, in->row_entry.p, in->G, pos, xl.p,
+    k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, grid->bbox.p, nc * in->m, in->m, xl.p);
+    launch_rows<0>(in->m, nc, s, in->offsets.p, in->j.p, in->mask.p, in->delta.p, in->row_entry.p, in->G, pos, xl.p,
                    bx, in->r_list * in->r_list, grid->cell_of_cluster.p, grid->col_first.p, keep.p,
                    emask.p, alive.p, nullptr);
   }
@@ -978,8 +1025,8 @@ extern "C" int nbx_count_within(const nbx_list_t* l, const double* pos, const do
   TRY(cudaMemsetAsync(cnt.p, 0, 16, s));
   if (l->n_clusters > 0) {
     count_launch();
-    k_local_coords<<<nb(l->n_clusters * l->m, 256), 256, 0, s>>>(pos, l->n_clusters * l->m, l->m, xl.p);
-    launch_rows<1>(l->m, l->n_clusters, s, l->offsets.p, l->j.p, l->mask.p, nullptr, l->G, pos, xl.p,
+    k_local_coords<<<nb(l->n_clusters * l->m, 256), 256, 0, s>>>(pos, l->bbox, l->n_clusters * l->m, l->m, xl.p);
+    launch_rows<1>(l->m, l->n_clusters, s, l->offsets.p, l->j.p, l->mask.p, l->delta.p, nullptr, l->G, pos, xl.p,
                    make_box(box), r_cut * r_cut, nullptr, nullptr, nullptr, nullptr, nullptr, cnt.p);
   }
   TRY(cudaGetLastError());
