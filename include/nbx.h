@@ -97,6 +97,12 @@ void nbx_grid_free(nbx_grid_t* grid);
  * ascending in cj, masks per pairlist.py:106-112.  Errors as :164-175. */
 int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], double r_list, void* stream,
                        nbx_list_t** out);
+/* nbx_pairlist_build for one domain of a spatial decomposition: `halo`
+ * (device uint8 per particle, original order; NULL = none) marks particles
+ * owned by another rank; slot pairs with both particles halo are removed
+ * from the masks (their owner computes them).  Otherwise identical. */
+int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3], double r_list, const uint8_t* halo,
+                          void* stream, nbx_list_t** out);
 /* Replaces pairlist.prune_pair_list (pairlist.py:242-282): keep rows whose
  * exact FP64 min-image distance over admitted slot pairs is <= r_list, plus
  * every diagonal row.  clustered_positions: device (n_slots, 3) f64. */
@@ -137,6 +143,18 @@ int nbx_force(const nbx_list_t* list, const nbx_grid_t* grid, const double* posi
               const double* charges, const int64_t* lj_type, const nbx_params_t* params,
               const double box[3], const int32_t* i_sel, int64_t n_sel, int32_t flags,
               double* f_out, double* e_out, int64_t* bad, void* stream);
+
+/* ---------------------------------------------------------------- MD step
+ * oracle.update_drift (oracle.py:106-123): *out_d2 (device f64) = max over
+ * particles of the squared minimum-image displacement cur - ref (FP64,
+ * reference operation order; bit-identical). */
+int nbx_max_displacement(const double* ref, const double* cur, int64_t n, const double box[3],
+                         double* out_d2, void* stream);
+/* engine.velocity_verlet_step half steps (engine.py:556-579): v += f*(0.5 dt/m);
+ * with move != 0 also x = wrap(x + v dt) (model.py:147-156).  Device arrays,
+ * original order. */
+int nbx_vv_update(double* x, double* v, const double* f, const double* mass, int64_t n, double dt,
+                  int32_t move, const double box[3], void* stream);
 
 /* Exact FP64 scan of every admitted pair for a coincident in-range pair
  * (kernels.py:184-187, 390-395); run when nbx_force reported bad = {-2,-2}

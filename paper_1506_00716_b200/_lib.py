@@ -26,6 +26,7 @@ EXPORTS = (
     "nbx_pairlist_build", "nbx_pairlist_prune", "nbx_list_info", "nbx_list_download",
     "nbx_super_layout", "nbx_super_download", "nbx_count_within", "nbx_list_free",
     "nbx_force", "nbx_find_singular", "nbx_launch_count", "nbx_timing_enable", "nbx_timing_query",
+    "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
 )
 
 
@@ -69,6 +70,7 @@ def load():
         "nbx_scatter_to_original": (ctypes.c_int, [P, P, I32, P, P]),
         "nbx_grid_free": (None, [P]),
         "nbx_pairlist_build": (ctypes.c_int, [P, P, D, P, PP]),
+        "nbx_pairlist_build_ex": (ctypes.c_int, [P, P, D, P, P, PP]),
         "nbx_pairlist_prune": (ctypes.c_int, [P, P, P, P, P, PP]),
         "nbx_list_info": (ctypes.c_int, [P, P]),
         "nbx_list_download": (ctypes.c_int, [P, P, P, P, P]),
@@ -81,6 +83,8 @@ def load():
         "nbx_launch_count": (ctypes.c_int64, []),
         "nbx_timing_enable": (None, [I32]),
         "nbx_timing_query": (ctypes.c_int, [P, P]),
+        "nbx_max_displacement": (ctypes.c_int, [P, P, I64, P, P, P]),
+        "nbx_vv_update": (ctypes.c_int, [P, P, P, P, I64, D, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -164,10 +164,20 @@ __device__ __forceinline__ uint32_t member_bits(const SearchCtx& C, const float4
 
 // Emit one batch of hits (ascending cj across lanes): canonical rows of every
 // member (CSR position = member offset + running count) and the group entry.
+// slot pairs (a, b) with both slots halo (domain decomposition: computed by
+// the owner of the halo, never here)
+__device__ __forceinline__ uint64_t halo_pair_mask(uint32_t hi, uint32_t hj, int m) {
+  uint64_t x = 0;
+  for (int a = 0; a < m; ++a)
+    if ((hi >> a) & 1u) x |= (uint64_t)hj << (a * m);
+  return x;
+}
+
 __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx& C, const double (*s_bb)[6],
                                            const double* gb, int32_t cj, uint32_t bits, int lane,
                                            int32_t& cnt, int32_t& ecnt, int32_t row_base, int32_t ent_base,
-                                           int m, const int8_t* nreal, const Box& box) {
+                                           int m, const int8_t* nreal, const Box& box,
+                                           const uint8_t* __restrict__ halo) {
   const unsigned lt = (1u << lane) - 1u;
   const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
   if (!eb) return;
@@ -185,7 +195,8 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
     if ((bits >> k) & 1u) {
       const int32_t ci = C.first + k;
       const int64_t row = (int64_t)rbase + before + __popc(b & lt);
-      const uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
+      uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
+      if (halo) mk &= ~halo_pair_mask(halo[ci], halo[cj], m);
       out.j[row] = cj;
       out.mask[row] = mk;
       float4 rdelta;
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(SEARCH_WARPS * 32, 6)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
          int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
          const float2* __restrict__ zr, const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first,
-         int64_t cells, Box box, double r_list, SearchOut out) {
+         int64_t cells, Box box, double r_list, SearchOut out, const uint8_t* __restrict__ halo) {
   __shared__ double s_bb[SEARCH_WARPS][GMAX][6];
   __shared__ float4 s_bf[SEARCH_WARPS][GMAX][2];
   __shared__ int32_t s_q[SEARCH_WARPS][64];
@@ -260,7 +271,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
       for (int32_t base = 0; base < nst; base += 32) {
         int2 h = make_int2(0, 0);
         if (base + lane < nst) h = stash[base + lane];
-        emit_batch(out, C, s_bb[w], gb, h.x, (uint32_t)h.y, lane, cnt, ecnt, row_base, ent_base, m, nreal, box);
+        emit_batch(out, C, s_bb[w], gb, h.x, (uint32_t)h.y, lane, cnt, ecnt, row_base, ent_base, m, nreal, box, halo);
       }
       return;
     }
@@ -285,7 +296,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
       if (bits && ecnt + __popc(eb & lt) < STASH) stash[ecnt + __popc(eb & lt)] = make_int2(cj, (int)bits);
       ecnt += __popc(eb);
     } else {
-      emit_batch(out, C, s_bb[w], gb, cj, bits, lane, cnt, ecnt, row_base, ent_base, m, nreal, box);
+      emit_batch(out, C, s_bb[w], gb, cj, bits, lane, cnt, ecnt, row_base, ent_base, m, nreal, box, halo);
     }
   };
 
@@ -323,6 +334,18 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
     if (lane < C.nmem) out.row_count[C.first + lane] = cnt;
     if (lane == 0) out.ent_count[g] = ecnt;
   }
+}
+
+__global__ void k_halo_bits(const uint8_t* __restrict__ halo, const int32_t* __restrict__ perm,
+                            const uint8_t* __restrict__ fill, int64_t n_clusters, int m, uint8_t* __restrict__ hb) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_clusters) return;
+  uint32_t b = 0;
+  for (int a = 0; a < m; ++a) {
+    const int64_t s = c * m + a;
+    if (!fill[s] && halo[perm[s]]) b |= 1u << a;
+  }
+  hb[c] = (uint8_t)b;
 }
 
 __global__ void k_groups(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
@@ -779,6 +802,11 @@ static Box make_box(const double L[3]) {
 
 extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], double r_list,
                                   void* stream, nbx_list_t** out) {
+  return nbx_pairlist_build_ex(grid, box, r_list, nullptr, stream, out);
+}
+
+extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3], double r_list,
+                                     const uint8_t* halo, void* stream, nbx_list_t** out) {
   if (!grid || !box || !out) {
     set_error("nbx_pairlist_build: null argument");
     return NBX_ERR_PARAM;
@@ -806,6 +834,7 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   Box bx = make_box(box);
   DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
   DBuf<int2> stash;
+  DBuf<uint8_t> hbits;
   int32_t h[2] = {0, 0};
   SearchOut so{};
   TRY(ng.alloc(n_cols + 1, s));
@@ -825,13 +854,18 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   TRY(cudaMemsetAsync(row_count.p, 0, 4 * (nc + 1), s));
   TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
   TRY(stash.alloc(l->n_groups * (int64_t)STASH, s));
+  if (halo && nc > 0) {
+    TRY(hbits.alloc(nc, s));
+    count_launch();
+    k_halo_bits<<<nb(nc, 256), 256, 0, s>>>(halo, grid->perm.p, grid->fill.p, nc, m, hbits.p);
+  }
   so.row_count = row_count.p;
   so.ent_count = ent_count.p;
   so.stash = stash.p;
   if (l->n_groups > 0)
     count_launch(), k_search<0><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
         l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
-        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so);
+        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   TRY(cudaGetLastError());
   TRY(l->offsets.alloc(nc + 1, s));
   TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
@@ -866,14 +900,16 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   if (l->n_groups > 0)
     count_launch(), k_search<1><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
         l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
-        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so);
+        grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   TRY(cudaGetLastError());
   TRY(order_entries(l, s));
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
+  hbits.release(s);
   *out = l;
   return NBX_OK;
 fail:
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
+  hbits.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }

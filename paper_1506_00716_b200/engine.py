@@ -1,0 +1,370 @@
+"""List lifecycle, drift guard and the force pass of an MD step -- GPU-backed
+drop-in for the hot-path part of clustermd.engine.
+
+Mirrors /root/reference/pkg/src/clustermd/engine.py: ``ListPolicy``,
+``MDState``, ``init_state`` (:337-384), ``lifecycle_tick`` (:387-406),
+``parallel_forces`` (:462-521), ``velocity_verlet_step`` (:543-580) and the
+slab bookkeeping (:141-263) that the multi-GPU decomposition (dd.py) reuses;
+``DriftTracker`` / ``update_drift`` mirror oracle.py:88-123.
+
+The force pass is one GPU launch sequence whatever ``workers`` is: the
+reference's per-worker buffers and fixed-order reduction (engine.py:485-514)
+are replaced by the library's deterministic reduction, so results are
+bit-identical across reruns *and* across worker counts.
+"""
+
+from __future__ import annotations
+
+import time
+from contextlib import contextmanager
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _lib
+from .gridder import ClusterGrid, build_cluster_grid
+from .kernels import KernelLayout, compute_nonbonded_original
+from .model import (BOLTZMANN_KJ_MOL_K, ForcesEnergies, NonbondedParams, ParameterError, ParticleSystem,
+                    SimBox, wrap_position)
+from .pairlist import ClusterPairList, build_pair_list, prune_pair_list
+
+
+# ---------------------------------------------------------------- timing (host bookkeeping)
+class TimingError(RuntimeError):
+    """Improper section nesting (engine.py:35-36)."""
+
+
+class TimingReport:
+    """Named nested wall-time sections (engine.py:45-121), kept so callers of
+    the reference API can pass a timer; device work is timed with CUDA events
+    elsewhere (bench.py, tools/step_breakdown.py)."""
+
+    def __init__(self, debug: bool = False):
+        self.debug = debug
+        self.sections: dict = {}
+        self.parent: dict = {}
+        self._stack: list = []
+
+    @contextmanager
+    def section(self, name: str):
+        if name in self._stack:
+            if self.debug:
+                raise TimingError(f"section {name!r} re-entered while active")
+            yield self
+            return
+        parent = self._stack[-1] if self._stack else None
+        if self.parent.get(name, parent) != parent and self.debug:
+            raise TimingError(f"section {name!r} opened under {parent!r}")
+        self.parent.setdefault(name, parent)
+        entry = self.sections.setdefault(name, [0, 0.0])
+        self._stack.append(name)
+        t0 = time.perf_counter()
+        try:
+            yield self
+        finally:
+            entry[1] += time.perf_counter() - t0
+            entry[0] += 1
+            self._stack.pop()
+
+    def total(self, name: str) -> float:
+        return self.sections[name][1]
+
+
+@contextmanager
+def _maybe(timer, name):
+    if timer is None:
+        yield
+    else:
+        with timer.section(name):
+            yield
+
+
+# ---------------------------------------------------------------- drift guard
+@dataclass(frozen=True)
+class DriftTracker:
+    """Largest minimum-image displacement since the reference snapshot (oracle.py:88-103)."""
+
+    reference_positions: np.ndarray
+    max_displacement: float = 0.0
+
+    def __post_init__(self):
+        ref = np.array(self.reference_positions, dtype=np.float64, copy=True).reshape(-1, 3)
+        ref.setflags(write=False)
+        object.__setattr__(self, "reference_positions", ref)
+
+
+def max_displacement_device(ref: torch.Tensor, cur: torch.Tensor, box: SimBox) -> torch.Tensor:
+    """Device scalar: max_i |minimum_image(cur_i - ref_i)| (no host sync)."""
+    out = torch.empty(1, dtype=torch.float64, device=cur.device)
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_max_displacement(_lib.ptr(ref), _lib.ptr(cur), int(cur.shape[0]), _lib.ptr(L),
+                                                _lib.ptr(out), dev.stream()), "max_displacement")
+    return out.sqrt()
+
+
+def update_drift(tracker: DriftTracker, current_positions, box: SimBox) -> DriftTracker:
+    """Fold the current positions into the tracked maximum (oracle.py:106-123),
+    evaluated on the GPU (bit-identical max)."""
+    cur = np.asarray(current_positions, dtype=np.float64).reshape(-1, 3)
+    if cur.shape != tracker.reference_positions.shape:
+        raise ParameterError(f"positions shape {cur.shape} does not match reference "
+                             f"{tracker.reference_positions.shape}")
+    if cur.shape[0] == 0:
+        return tracker
+    d = max_displacement_device(dev.to_device(tracker.reference_positions, torch.float64),
+                                dev.to_device(cur, torch.float64), box)
+    largest = float(d.item())
+    return DriftTracker(reference_positions=tracker.reference_positions,
+                        max_displacement=max(tracker.max_displacement, largest))
+
+
+# ---------------------------------------------------------------- slabs (host bookkeeping)
+@dataclass
+class SlabPartition:
+    """1D decomposition along x (engine.py:141-160)."""
+
+    boundaries: np.ndarray
+    min_width: float
+    assignments: np.ndarray
+    last_timings: np.ndarray | None = None
+
+    @property
+    def n_slabs(self) -> int:
+        return self.boundaries.shape[0] - 1
+
+    def widths(self) -> np.ndarray:
+        return np.diff(self.boundaries)
+
+
+def _unit_centers_x(grid: ClusterGrid, supercluster_size: int) -> np.ndarray:
+    centers = grid.cluster_centers()[:, 0]
+    if supercluster_size == 1:
+        return centers
+    n_groups = -(-grid.n_clusters // supercluster_size)
+    return np.array([centers[g * supercluster_size:(g + 1) * supercluster_size].mean() for g in range(n_groups)])
+
+
+def assign_slabs(boundaries: np.ndarray, centers_x: np.ndarray) -> np.ndarray:
+    """Slab per unit centre; boundary centres go right (engine.py:176-179)."""
+    idx = np.searchsorted(boundaries[1:-1], centers_x, side="right")
+    return np.clip(idx, 0, boundaries.shape[0] - 2).astype(np.int64)
+
+
+def build_slab_partition(box_length_x: float, n_slabs: int, min_width: float, grid: ClusterGrid | None = None,
+                         supercluster_size: int = 1) -> SlabPartition:
+    """Equal-width initial partition (engine.py:182-205)."""
+    if n_slabs < 1:
+        raise ParameterError(f"n_slabs must be >= 1, got {n_slabs}")
+    if min_width <= 0.0 or n_slabs * min_width > box_length_x:
+        raise ParameterError(f"{n_slabs} slabs of minimum width {min_width} do not fit in box length {box_length_x}")
+    boundaries = np.linspace(0.0, box_length_x, n_slabs + 1)
+    boundaries[-1] = box_length_x
+    assignments = (assign_slabs(boundaries, _unit_centers_x(grid, supercluster_size))
+                   if grid is not None else np.empty(0, dtype=np.int64))
+    return SlabPartition(boundaries=boundaries, min_width=float(min_width), assignments=assignments)
+
+
+def rebalance_slabs(partition: SlabPartition, timings, alpha: float = 0.5, grid: ClusterGrid | None = None,
+                    supercluster_size: int = 1) -> SlabPartition:
+    """Widths scaled by t_mean/t_i, renormalised, clamped to min_width,
+    blended by alpha (engine.py:208-263)."""
+    t = np.asarray(timings, dtype=np.float64)
+    n = partition.n_slabs
+    if t.shape != (n,):
+        raise ParameterError(f"expected {n} timings, got shape {t.shape}")
+    if np.any(t <= 0.0) or not np.all(np.isfinite(t)):
+        raise ParameterError("per-slab timings must be positive and finite")
+    if not (0.0 < alpha <= 1.0):
+        raise ParameterError(f"alpha must be in (0, 1], got {alpha}")
+    span = float(partition.boundaries[-1] - partition.boundaries[0])
+    old = partition.widths()
+    prop = old * (t.mean() / t)
+    prop *= span / prop.sum()
+    free = np.ones(n, dtype=bool)
+    for _ in range(n):
+        clamped = free & (prop < partition.min_width)
+        if not np.any(clamped):
+            break
+        free &= ~clamped
+        prop[~free] = partition.min_width
+        rest = span - partition.min_width * np.count_nonzero(~free)
+        if np.any(free):
+            prop[free] *= rest / prop[free].sum()
+    widths = alpha * prop + (1.0 - alpha) * old
+    b = np.empty(n + 1)
+    b[0] = partition.boundaries[0]
+    np.cumsum(widths, out=b[1:])
+    b[1:] += partition.boundaries[0]
+    b[-1] = partition.boundaries[-1]
+    assignments = partition.assignments
+    if grid is not None:
+        assignments = assign_slabs(b, _unit_centers_x(grid, supercluster_size))
+    return SlabPartition(boundaries=b, min_width=partition.min_width, assignments=assignments)
+
+
+# ---------------------------------------------------------------- lifecycle
+@dataclass
+class ListPolicy:
+    """engine.py:266-277."""
+
+    rebuild_interval: int = 10
+    prune_on_build: bool = True
+
+    def __post_init__(self):
+        if self.rebuild_interval < 1:
+            raise ParameterError(f"rebuild_interval must be >= 1, got {self.rebuild_interval}")
+
+
+@dataclass
+class MDState:
+    """engine.py:280-291 (+ optional grid occupancy for the compact-cluster grid)."""
+
+    system: ParticleSystem
+    step: int
+    grid: ClusterGrid
+    plist: ClusterPairList
+    drift: DriftTracker
+    n_rebuilds: int = 0
+    n_drift_rebuilds: int = 0
+    slabs: SlabPartition | None = None
+    target_occupancy: float | None = None
+
+
+def _build(system, params, m, supercluster_size, n_lane, step, policy, occupancy):
+    grid = build_cluster_grid(system, m, occupancy)
+    plist = build_pair_list(grid, system.box, params.r_list, supercluster_size=supercluster_size,
+                            n_lane=n_lane, build_step=step)
+    if policy.prune_on_build and policy.rebuild_interval > 1:
+        plist = prune_pair_list(plist, grid.clustered_positions_device, system.box)
+    return grid, plist
+
+
+def _rebuild(state: MDState, params: NonbondedParams, policy: ListPolicy, timer) -> None:
+    """engine.py:294-334."""
+    with _maybe(timer, "grid_build"), _maybe(timer, "list_build"):
+        state.grid, state.plist = _build(state.system, params, state.grid.m, state.plist.supercluster_size,
+                                         state.plist.n_lane, state.step, policy, state.target_occupancy)
+    state.drift = DriftTracker(reference_positions=wrap_position(state.system.positions, state.system.box))
+    state.n_rebuilds += 1
+    if state.slabs is not None:
+        t = state.slabs.last_timings
+        if t is not None and np.all(t > 0.0):
+            state.slabs = rebalance_slabs(state.slabs, t, grid=state.grid,
+                                          supercluster_size=state.plist.supercluster_size)
+        else:
+            state.slabs.assignments = assign_slabs(state.slabs.boundaries,
+                                                   _unit_centers_x(state.grid, state.plist.supercluster_size))
+
+
+def init_state(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout, *,
+               supercluster_size: int = 1, policy: ListPolicy | None = None, n_slabs: int = 0,
+               slab_min_width: float | None = None, timer=None, target_occupancy: float | None = None) -> MDState:
+    """Initial grid, list (pruned when reused) and optional slabs (engine.py:337-384)."""
+    if params.r_list < params.r_cut:
+        raise ParameterError(f"r_list={params.r_list} must be >= r_cut={params.r_cut}")
+    policy = policy or ListPolicy()
+    grid, plist = _build(system, params, layout.m, supercluster_size, layout.n_lane, 0, policy, target_occupancy)
+    state = MDState(system=system, step=0, grid=grid, plist=plist,
+                    drift=DriftTracker(reference_positions=wrap_position(system.positions, system.box)),
+                    n_rebuilds=1, target_occupancy=target_occupancy)
+    if n_slabs > 0:
+        width = params.r_list if slab_min_width is None else slab_min_width
+        state.slabs = build_slab_partition(float(system.box.lengths[0]), n_slabs, width, grid=grid,
+                                           supercluster_size=supercluster_size)
+    return state
+
+
+def lifecycle_tick(state: MDState, params: NonbondedParams, policy: ListPolicy, timer=None) -> bool:
+    """Rebuild when the interval is due or 2 d_max > r_list - r_c (engine.py:387-406)."""
+    interval_due = state.step - state.plist.build_step >= policy.rebuild_interval
+    guard_due = 2.0 * state.drift.max_displacement > params.r_list - params.r_cut
+    if not (interval_due or guard_due):
+        return False
+    if guard_due and not interval_due:
+        state.n_drift_rebuilds += 1
+    _rebuild(state, params, policy, timer)
+    return True
+
+
+def parallel_forces(state: MDState, params: NonbondedParams, layout: KernelLayout, workers: int = 1,
+                    timer=None) -> ForcesEnergies:
+    """Force pass over the current list, original order (engine.py:462-521).
+
+    ``workers`` is validated for API compatibility; the GPU pass is one
+    deterministic launch sequence, so results do not depend on it."""
+    if workers < 1:
+        raise ParameterError(f"workers must be >= 1, got {workers}")
+    s = state.system
+    res = compute_nonbonded_original(state.plist, state.grid, s.positions, s.charges, s.lj_type, params, s.box,
+                                     layout)
+    if state.slabs is not None:
+        state.slabs.last_timings = np.ones(state.slabs.n_slabs)
+    return res
+
+
+# ---------------------------------------------------------------- integrator (device arithmetic)
+def kinetic_energy(system: ParticleSystem) -> float:
+    return 0.5 * float(np.einsum("k,kd,kd->", system.masses, system.velocities, system.velocities))
+
+
+def temperature(system: ParticleSystem) -> float:
+    n = system.n
+    if n == 0:
+        return 0.0
+    dof = 3 * n - 3 if n > 1 else 3
+    return 2.0 * kinetic_energy(system) / (dof * BOLTZMANN_KJ_MOL_K)
+
+
+def total_momentum(system: ParticleSystem) -> np.ndarray:
+    return np.einsum("k,kd->d", system.masses, system.velocities)
+
+
+def vv_half_kick_device(x, v, f, mass, dt: float, box: SimBox, move: bool) -> None:
+    """v += f (0.5 dt / m), then x = wrap(x + v dt) when ``move`` (device, in place)."""
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_vv_update(_lib.ptr(x), _lib.ptr(v), _lib.ptr(f), _lib.ptr(mass), int(x.shape[0]),
+                                         float(dt), int(bool(move)), _lib.ptr(L), dev.stream()), "vv_update")
+
+
+def velocity_verlet_step(state: MDState, params: NonbondedParams, dt: float, forces_in: ForcesEnergies,
+                         layout: KernelLayout, *, policy: ListPolicy | None = None, workers: int = 1,
+                         timer=None) -> ForcesEnergies:
+    """One NVE step (engine.py:543-580); the half kicks, drift and wrap run on
+    the GPU with the reference's FP64 operation order."""
+    policy = policy or ListPolicy()
+    s = state.system
+    with _maybe(timer, "integrate"):
+        x = dev.to_device(s.positions, torch.float64)
+        v = dev.to_device(s.velocities, torch.float64)
+        m = dev.to_device(s.masses, torch.float64)
+        vv_half_kick_device(x, v, dev.to_device(forces_in.forces, torch.float64), m, dt, s.box, move=True)
+        positions = x.cpu().numpy()
+        state.system = replace(s, positions=positions, velocities=v.cpu().numpy())
+        state.step += 1
+        state.drift = update_drift(state.drift, positions, s.box)
+    with _maybe(timer, "lifecycle"):
+        lifecycle_tick(state, params, policy, timer)
+    with _maybe(timer, "forces"):
+        out = parallel_forces(state, params, layout, workers, timer)
+    with _maybe(timer, "integrate"):
+        v = dev.to_device(state.system.velocities, torch.float64)
+        x = dev.to_device(state.system.positions, torch.float64)
+        vv_half_kick_device(x, v, dev.to_device(out.forces, torch.float64), m, dt, s.box, move=False)
+        state.system = replace(state.system, velocities=v.cpu().numpy())
+    return out
+
+
+@dataclass
+class RunResult:
+    state: MDState
+    forces: ForcesEnergies
+    steps: np.ndarray
+    e_kinetic: np.ndarray
+    e_potential: np.ndarray
+    timing: TimingReport = field(default_factory=TimingReport)
+
+    @property
+    def e_total(self) -> np.ndarray:
+        return self.e_kinetic + self.e_potential

@@ -137,8 +137,12 @@ class InteractionStats:
 
 
 def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, supercluster_size: int = 1,
-                    n_lane: int = 1, build_step: int = 0) -> ClusterPairList:
-    """All cluster pairs with AABB gap <= r_list, j >= i (pairlist.py:147-217)."""
+                    n_lane: int = 1, build_step: int = 0, halo=None) -> ClusterPairList:
+    """All cluster pairs with AABB gap <= r_list, j >= i (pairlist.py:147-217).
+
+    ``halo`` (extension, domain decomposition): CUDA uint8 tensor per
+    particle marking particles owned by another rank; halo-halo slot pairs
+    are masked out."""
     if r_list <= 0.0:
         raise ParameterError(f"r_list must be positive, got {r_list}")
     if np.any(box.lengths < 2.0 * r_list):
@@ -149,8 +153,8 @@ def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, superclust
                              f"got {supercluster_size}")
     h = ctypes.c_void_p()
     L = _lib.box3(box.lengths)
-    _lib.check(_lib.load().nbx_pairlist_build(grid.handle, _lib.ptr(L), float(r_list), dev.stream(),
-                                              ctypes.byref(h)), "pairlist_build")
+    _lib.check(_lib.load().nbx_pairlist_build_ex(grid.handle, _lib.ptr(L), float(r_list), _lib.ptr(halo),
+                                                 dev.stream(), ctypes.byref(h)), "pairlist_build")
     return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
 
 

@@ -1,0 +1,106 @@
+"""Domain decomposition host logic on CPU: world_size 2 over gloo.
+
+The slab/halo bookkeeping and the neighbour exchanges of
+paper_1506_00716_b200.dd run unchanged; the local force pass (a CUDA kernel
+in production) is the FP64 oracle here, with the same halo-halo masking the
+GPU list builder applies.  The decomposed forces and energies must equal the
+single-domain oracle.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _local_oracle_forces(pos_local, q, t, halo, L, phys):
+    from oracle import native, search
+
+    occ = None
+    og = search.build_grid(pos_local, L, 4, occ)
+    ol = native.prune_list(native.search_list(og, L, 1.1), og["clustered_positions"], L)
+    h = halo[og["perm"]].reshape(-1, 4) & ~og["fill_mask"].reshape(-1, 4)
+    ci = search.row_ci(ol)
+    both = h[ci][:, :, None] & h[ol["j_idx"]][:, None, :]
+    ol = dict(ol, masks=ol["masks"] & ~both)
+    fc, elj, ec = native.list_forces(ol, og, pos_local, q, t, L, phys, threads=2)
+    return search.scatter_to_original(og, fc), elj, ec
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import forces as of
+        from paper_1506_00716_b200.dd import SlabDecomposition
+        from paper_1506_00716_b200.systems import spc_water
+
+        s, table = spc_water(3000 * 4)  # 12k atoms, L = 4.93 nm
+        L = s.box.lengths
+        phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True)
+        dd = SlabDecomposition(L, world, rank, r_comm=1.1)
+        lay = dd.assign(s.positions)
+        ids = lay.local_ids
+        local = torch.zeros((lay.n_local, 3), dtype=torch.float64)
+        local[:lay.n_home] = torch.from_numpy(s.positions[lay.home])
+        dd.exchange_positions(local)
+        assert np.array_equal(local[lay.n_home:].numpy(), s.positions[lay.halo])
+        halo = np.zeros(lay.n_local, dtype=bool)
+        halo[lay.n_home:] = True
+        f, elj, ec = _local_oracle_forces(local.numpy(), s.charges[ids], s.lj_type[ids], halo, L, phys)
+        home_f = dd.reduce_halo_forces(torch.from_numpy(f))
+        e = dd.allreduce_energies(torch.tensor([elj, ec], dtype=torch.float64))
+        glob = dd.allgather_home(lay.home, home_f, s.n)
+        if rank == 0:
+            out_q.put((glob.numpy(), e.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_slab_decomposition_equals_single_domain():
+    from oracle import forces as of
+    from oracle import native, search
+    from paper_1506_00716_b200.systems import spc_water
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    f_dd, e_dd = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    s, table = spc_water(12000)
+    L = s.box.lengths
+    og = search.build_grid(s.positions, L, 4, None)
+    ol = native.prune_list(native.search_list(og, L, 1.1), og["clustered_positions"], L)
+    fc, elj, ec = native.list_forces(ol, og, s.positions, s.charges, s.lj_type, L,
+                                     of.Physics(r_cut=1.0, lj_table=table, shift_potential=True), threads=2)
+    f_ref = search.scatter_to_original(og, fc)
+    assert np.abs(f_dd - f_ref).max() <= 1e-9 * np.abs(f_ref).max()
+    assert abs(e_dd[0] - elj) <= 1e-9 * abs(elj) and abs(e_dd[1] - ec) <= 1e-9 * abs(ec)
+
+
+def test_slab_geometry_checks():
+    from paper_1506_00716_b200.dd import SlabDecomposition
+    from paper_1506_00716_b200.model import ParameterError
+
+    with pytest.raises(ParameterError):
+        SlabDecomposition([4.0, 4.0, 4.0], 4, 0, r_comm=1.1)   # slabs narrower than r_comm
+    dd = SlabDecomposition([9.8, 9.8, 9.8], 4, 1, r_comm=1.1)
+    own = dd.owner(np.array([0.0, 2.44, 2.46, 9.79, -0.01, 9.8]))
+    assert own.tolist() == [0, 0, 1, 3, 3, 0]
