@@ -222,11 +222,9 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist = None
     if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_dd(args, world, rank, local)
+    dist = None
     lib = _lib.load()
     system, table, occ = workload(args)
     params = nbx.NonbondedParams(**{k: getattr(make_params(args, table), k) for k in (
@@ -375,6 +373,127 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_dd(args, world, rank, local):
+    """N > 1: strong scaling of the same box over N GPUs with the slab
+    decomposition (paper_1506_00716_b200/dd.py): per step NCCL halo exchange
+    (coordinates in, forces back), local search every nstlist steps after an
+    all-gather of home positions, energies all-reduced on energy steps."""
+    import datetime
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1506_00716_b200 as nbx
+    from paper_1506_00716_b200 import _lib
+    from paper_1506_00716_b200.dd import DomainForces, SlabDecomposition
+    from paper_1506_00716_b200.kernels import flops_per_pair
+
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=120))
+    lib = _lib.load()
+    system, table, occ = workload(args)
+    params = make_params(args, table)
+    box = system.box
+    dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
+    df = DomainForces(dd, system, params, M, occ)
+    pos_glob = torch.from_numpy(np.array(system.positions)).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    lay = df.rebuild(pos_glob)
+
+    def step(k, home_pos=None):
+        nonlocal lay
+        if k % args.nstlist == 0:
+            cur = df.local_pos[:lay.n_home] if home_pos is None else home_pos
+            glob = dd.allgather_home(lay.home, cur, system.n)
+            lay = df.rebuild(glob)
+        elif home_pos is not None:
+            df.local_pos[:lay.n_home].copy_(home_pos)
+        return df.forces(energy=(k % args.nstlist == 0))
+
+    W = max(3, args.warmup)
+    for k in range(W):
+        step(k)
+    torch.cuda.synchronize()
+    st = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, box, R_CUT)
+    cnt = torch.tensor([st.n_within_cutoff, st.n_admitted], dtype=torch.int64, device=dev)
+    dist.all_reduce(cnt)
+    n_within, n_admitted = int(cnt[0].item()), int(cnt[1].item())
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    lib.nbx_timing_query(None, None)
+    lib.nbx_timing_enable(1)
+    launches0 = lib.nbx_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record()
+        step(W + i)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    launches = lib.nbx_launch_count() - launches0
+    lib.nbx_timing_enable(0)
+    fk_ms, fk_n = np.zeros(1), np.zeros(1, dtype=np.int64)
+    _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
+    clk = clocks.stop()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    # e2e: home positions H2D from pinned host memory, home forces + energies D2H, every step
+    home_h = df.local_pos[:lay.n_home].cpu().pin_memory()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    bytes_io = torch.zeros(2, dtype=torch.int64, device=dev)
+    for i in range(W + args.steps):
+        if i >= W:
+            flush.zero_()
+            ev2[i - W][0].record()
+        if home_h.shape[0] != lay.n_home:
+            home_h = df.local_pos[:lay.n_home].cpu().pin_memory()
+        hp = home_h.to(dev, non_blocking=True)
+        f, e = step(W + args.steps + i, home_pos=hp)
+        f_host = torch.empty(f.shape, dtype=f.dtype).pin_memory()
+        f_host.copy_(f, non_blocking=True)
+        e_host = e.to("cpu", non_blocking=True)
+        if i >= W:
+            ev2[i - W][1].record()
+            bytes_io[0] += hp.numel() * 8
+            bytes_io[1] += f.numel() * 8 + 16
+    torch.cuda.synchronize()
+    t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    dist.all_reduce(bytes_io)
+    e2e_ms = float(t2.item())
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tf = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
+    fk_avg_ms = float(fk_ms[0]) / max(1, int(fk_n[0]))
+    achieved = st.n_admitted * flops_per_pair(params) / (fk_avg_ms * 1e-3) / 1e12
+    if rank == 0:
+        line = {
+            "metric": "nonbonded pair-interactions/s (useful, r<=r_c)",
+            "value": n_within * args.steps / (t_ms * 1e-3), "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": W, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32 (pair math; fp64 energy + final force accumulation)",
+            "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
+            "config": config(args, occ, {"parallelism": f"slab DD x{world} (NCCL p2p half-shell halo, r_comm=r_list)"}),
+            "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
+            "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted},
+            "e2e": {"value": n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",
+                    "h2d_bytes_per_step": int(bytes_io[0].item()) // args.steps,
+                    "d2h_bytes_per_step": int(bytes_io[1].item()) // args.steps, "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "fp32", "kernel": "k_force (rank 0)", "achieved": achieved, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None, "kernel_ms": fk_avg_ms,
+                         "flops_per_pair": flops_per_pair(params)},
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -51,12 +51,13 @@ def _wrap_np(x, L):
 
 @dataclass
 class DomainLayout:
-    """Particle sets of one rank after a rebuild (global ids ascending)."""
+    """Particle sets of one rank after a rebuild (global ids ascending), as
+    tensors on the device of the positions they were derived from."""
 
-    home: np.ndarray        # global ids owned here
-    halo: np.ndarray        # global ids received from the +x neighbour
-    send: np.ndarray        # global ids (subset of home) sent to the -x neighbour
-    send_local: np.ndarray  # their indices in the local array [home; halo]
+    home: torch.Tensor        # global ids owned here
+    halo: torch.Tensor        # global ids received from the +x neighbour
+    send: torch.Tensor        # global ids (subset of home) sent to the -x neighbour
+    send_local: torch.Tensor  # their indices in the local array [home; halo]
 
     @property
     def n_home(self) -> int:
@@ -67,8 +68,8 @@ class DomainLayout:
         return int(self.home.shape[0] + self.halo.shape[0])
 
     @property
-    def local_ids(self) -> np.ndarray:
-        return np.concatenate([self.home, self.halo])
+    def local_ids(self) -> torch.Tensor:
+        return torch.cat([self.home, self.halo])
 
 
 class SlabDecomposition:
@@ -102,23 +103,30 @@ class SlabDecomposition:
         return np.clip(np.searchsorted(self.boundaries[1:-1], xw, side="right"), 0, self.N - 1)
 
     def assign(self, positions_global) -> DomainLayout:
-        """Home / halo / send sets from the global positions (same on every rank)."""
-        pos = np.asarray(positions_global, dtype=np.float64).reshape(-1, 3)
-        x = _wrap_np(pos[:, 0], self.L[0])
-        own = self.owner(x)
+        """Home / halo / send sets from the global positions (identical on every
+        rank).  Runs where the positions live (device tensors stay on the GPU)."""
+        pos = positions_global if isinstance(positions_global, torch.Tensor) else \
+            torch.as_tensor(np.asarray(positions_global, dtype=np.float64))
+        pos = pos.reshape(-1, 3)
+        dev = pos.device
+        Lx = float(self.L[0])
+        x = torch.remainder(pos[:, 0], Lx)
+        x = torch.where(x >= Lx, x - Lx, x)
+        inner = torch.as_tensor(self.boundaries[1:-1], dtype=torch.float64, device=dev)
+        own = torch.bucketize(x, inner, right=True).clamp_(0, self.N - 1)
         r = self.rank
-        home = np.nonzero(own == r)[0].astype(np.int64)
+        home = torch.nonzero(own == r).flatten()
         if self.N == 1:
-            empty = np.empty(0, dtype=np.int64)
+            empty = torch.empty(0, dtype=torch.int64, device=dev)
             self.layout = DomainLayout(home=home, halo=empty, send=empty, send_local=empty)
             return self.layout
-        b_lo = self.boundaries[r]
-        send = home[(x[home] - b_lo) < self.r_comm]
+        b_lo = float(self.boundaries[r])
+        sel = (x[home] - b_lo) < self.r_comm
+        send = home[sel]
+        send_local = torch.nonzero(sel).flatten()
         nb = (r + 1) % self.N
-        nb_lo = self.boundaries[nb]
-        cand = np.nonzero(own == nb)[0]
-        halo = cand[(x[cand] - nb_lo) < self.r_comm].astype(np.int64)
-        send_local = np.searchsorted(home, send)
+        nb_lo = float(self.boundaries[nb])
+        halo = torch.nonzero((own == nb) & ((x - nb_lo) < self.r_comm)).flatten()
         self.layout = DomainLayout(home=home, halo=halo, send=send, send_local=send_local)
         return self.layout
 
@@ -142,8 +150,7 @@ class SlabDecomposition:
         lay = self.layout
         if self.N == 1 or lay is None:
             return
-        idx = torch.as_tensor(lay.send_local, device=local_pos.device)
-        send_t = local_pos.index_select(0, idx)
+        send_t = local_pos.index_select(0, lay.send_local)
         recv_t = local_pos[lay.n_home:]
         buf = torch.empty_like(recv_t)
         self._p2p(send_t, (self.rank - 1) % self.N, buf, (self.rank + 1) % self.N)
@@ -158,8 +165,7 @@ class SlabDecomposition:
             return home_f
         recv = torch.empty((lay.send.shape[0], 3), dtype=local_f.dtype, device=local_f.device)
         self._p2p(local_f[lay.n_home:], (self.rank + 1) % self.N, recv, (self.rank - 1) % self.N)
-        idx = torch.as_tensor(lay.send_local, device=local_f.device)
-        home_f.index_add_(0, idx, recv)
+        home_f.index_add_(0, lay.send_local, recv)
         return home_f
 
     def allreduce_energies(self, e: torch.Tensor) -> torch.Tensor:
@@ -170,11 +176,12 @@ class SlabDecomposition:
         dist.all_reduce(e, group=self.group)
         return e
 
-    def allgather_home(self, ids: np.ndarray, pos: torch.Tensor, n_total: int) -> torch.Tensor:
+    def allgather_home(self, ids: torch.Tensor, pos: torch.Tensor, n_total: int) -> torch.Tensor:
         """Global (n_total, 3) positions from every rank's home rows."""
+        ids = torch.as_tensor(ids, device=pos.device)
         if self.N == 1:
             out = torch.empty((n_total, 3), dtype=pos.dtype, device=pos.device)
-            out[torch.as_tensor(ids, device=pos.device)] = pos
+            out[ids] = pos
             return out
         import torch.distributed as dist
 
@@ -184,7 +191,7 @@ class SlabDecomposition:
         dist.all_gather(counts, cnt, group=self.group)
         cmax = int(max(int(c.item()) for c in counts))
         pad_ids = torch.full((cmax,), -1, dtype=torch.int64, device=dev)
-        pad_ids[:ids.shape[0]] = torch.as_tensor(ids, device=dev)
+        pad_ids[:ids.shape[0]] = ids
         pad_pos = torch.zeros((cmax, 3), dtype=pos.dtype, device=dev)
         pad_pos[:ids.shape[0]] = pos
         all_ids = [torch.empty_like(pad_ids) for _ in range(self.N)]
@@ -210,6 +217,14 @@ def local_occupancy(target_occupancy: float, n_local: int, n_total: int, box_len
     return target_occupancy * n_local / n_equiv if n_equiv > 0 else target_occupancy
 
 
+@dataclass
+class _Domain:
+    """What build_cluster_grid needs of a system when positions come separately."""
+
+    n: int
+    box: object
+
+
 class DomainForces:
     """GPU non-bonded pass of one rank: local grid + halo-masked list, rebuilt
     every nstlist steps; per step halo exchange, force pass, halo reduction."""
@@ -225,21 +240,22 @@ class DomainForces:
 
     def rebuild(self, positions_global: torch.Tensor) -> DomainLayout:
         from . import build_cluster_grid, build_pair_list, prune_pair_list
-        from .model import ParticleSystem
 
-        lay = self.dd.assign(positions_global.cpu().numpy())
+        lay = self.dd.assign(positions_global)
         dev = positions_global.device
-        ids = torch.as_tensor(lay.local_ids, device=dev)
+        ids = lay.local_ids
         self.ids = ids
+        if not hasattr(self, "q_all"):
+            self.q_all = torch.as_tensor(np.array(self.system.charges), device=dev)
+            self.t_all = torch.as_tensor(np.array(self.system.lj_type), device=dev)
         self.local_pos = positions_global.index_select(0, ids).contiguous()
-        self.q = torch.as_tensor(np.asarray(self.system.charges)[lay.local_ids], device=dev)
-        self.t = torch.as_tensor(np.asarray(self.system.lj_type)[lay.local_ids], device=dev)
+        self.q = self.q_all.index_select(0, ids)
+        self.t = self.t_all.index_select(0, ids)
         halo = torch.zeros(lay.n_local, dtype=torch.uint8, device=dev)
         halo[lay.n_home:] = 1
         self.halo = halo
         n = lay.n_local
-        sys_local = ParticleSystem(positions=np.zeros((n, 3)), velocities=np.zeros((n, 3)), masses=np.ones(n),
-                                   charges=np.zeros(n), lj_type=np.zeros(n, dtype=np.int64), box=self.system.box)
+        sys_local = _Domain(n, self.system.box)
         occ = self.occ
         if occ is not None and self.dd.N > 1:
             w = float(np.diff(self.dd.boundaries).max())

@@ -52,11 +52,11 @@ def _worker(rank, world, port, out_q):
         phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True)
         dd = SlabDecomposition(L, world, rank, r_comm=1.1)
         lay = dd.assign(s.positions)
-        ids = lay.local_ids
+        ids = lay.local_ids.numpy()
         local = torch.zeros((lay.n_local, 3), dtype=torch.float64)
-        local[:lay.n_home] = torch.from_numpy(s.positions[lay.home])
+        local[:lay.n_home] = torch.from_numpy(s.positions[lay.home.numpy()])
         dd.exchange_positions(local)
-        assert np.array_equal(local[lay.n_home:].numpy(), s.positions[lay.halo])
+        assert np.array_equal(local[lay.n_home:].numpy(), s.positions[lay.halo.numpy()])
         halo = np.zeros(lay.n_local, dtype=bool)
         halo[lay.n_home:] = True
         f, elj, ec = _local_oracle_forces(local.numpy(), s.charges[ids], s.lj_type[ids], halo, L, phys)
@@ -104,3 +104,7 @@ def test_slab_geometry_checks():
     dd = SlabDecomposition([9.8, 9.8, 9.8], 4, 1, r_comm=1.1)
     own = dd.owner(np.array([0.0, 2.44, 2.46, 9.79, -0.01, 9.8]))
     assert own.tolist() == [0, 0, 1, 3, 3, 0]
+    lay = dd.assign(np.array([[0.1, 0, 0], [2.5, 0, 0], [3.0, 0, 0], [4.0, 0, 0], [5.0, 0, 0], [6.0, 0, 0]]))
+    assert lay.home.tolist() == [1, 2, 3]          # slab 1 = [2.45, 4.9)
+    assert lay.send.tolist() == [1, 2]             # within r_comm of its -x face
+    assert lay.halo.tolist() == [4, 5]             # slab 2 within r_comm of 4.9
