@@ -298,8 +298,13 @@ k_force(const ForceArgs A) {
 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane / M, b = lane % M;
-  const int64_t wi = blockIdx.x * (int64_t)FW + w;
-  if (wi >= A.n_work) return;
+  // persistent warps: groups are handed out dynamically (largest first via
+  // A.sel), which removes the wave tail and the group-size imbalance
+  for (;;) {
+  int64_t wi = 0;
+  if (lane == 0) wi = (int64_t)atomicAdd(A.scalars + 4, 1u);
+  wi = __shfl_sync(0xffffffffu, wi, 0);
+  if (wi >= A.n_work) break;
   const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
   const int32_t first = A.grp_first ? A.grp_first[g] : g;
   const int nmem = A.grp_nmem ? A.grp_nmem[g] : 1;
@@ -419,6 +424,8 @@ k_force(const ForceArgs A) {
       A.e_grp[2 * wi] = elj_acc;
       A.e_grp[2 * wi + 1] = ec_acc;
     }
+  }
+  __syncwarp();
   }
 }
 
@@ -541,7 +548,8 @@ __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __
 }
 
 __global__ void k_init_scalars(unsigned int* scalars) {
-  if (threadIdx.x < 4) scalars[threadIdx.x] = threadIdx.x < 2 ? 0u : 0xffffffffu;
+  // [0] max displacement, [1] non-finite flag, [2..3] bad key, [4] work counter
+  if (threadIdx.x < 5) scalars[threadIdx.x] = (threadIdx.x == 2 || threadIdx.x == 3) ? 0xffffffffu : 0u;
 }
 
 __global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, int shift,
@@ -569,7 +577,17 @@ static cudaError_t launch_one(const ForceArgs& A, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
   }
-  const int64_t blocks = (A.n_work + FW - 1) / FW;
+  // persistent grid: as many blocks as fit on the GPU at once
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int dev = 0, n_sm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FW * 32, dyn);
+    max_blocks = n_sm * (per_sm > 0 ? per_sm : 1);
+  }
+  int64_t blocks = (A.n_work + FW - 1) / FW;
+  if (blocks > max_blocks) blocks = max_blocks;
   if (blocks > 0) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool tm = timing_enabled();
@@ -749,7 +767,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
   if (wk.part_i.n < ns) { if ((e = wk.part_i.alloc(ns, s))) goto cuda_fail; }
   if (wk.part_j.n < n_items * m) { if ((e = wk.part_j.alloc(n_items * m, s))) goto cuda_fail; }
   if (wk.e_grp.n < 2 * n_work) { if ((e = wk.e_grp.alloc(2 * n_work + 2, s))) goto cuda_fail; }
-  if (wk.scalars.n < 4) { if ((e = wk.scalars.alloc(4, s))) goto cuda_fail; }
+  if (wk.scalars.n < 8) { if ((e = wk.scalars.alloc(8, s))) goto cuda_fail; }
   if (wk.lj.n < (int64_t)p->n_types * p->n_types) {
     if ((e = wk.lj.alloc((int64_t)p->n_types * p->n_types, s))) goto cuda_fail;
     wk.lj_key.clear();
@@ -790,7 +808,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     }
     ForceArgs A{};
     A.n_work = n_work;
-    A.sel = canonical ? i_sel : nullptr;
+    A.sel = canonical ? i_sel : l->group_order.p;
     A.grp_first = canonical ? nullptr : l->group_first.p;
     A.grp_nmem = canonical ? nullptr : l->group_nmem.p;
     A.ent_off = canonical ? l->offsets.p : l->ent_offsets.p;

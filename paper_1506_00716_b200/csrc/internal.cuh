@@ -96,6 +96,7 @@ struct List {
   // groups / entries
   DBuf<int32_t> group_first;  // (n_groups) first member cluster
   DBuf<int32_t> group_nmem;   // (n_groups)
+  DBuf<int32_t> group_order;  // (n_groups) force-kernel work order (descending entry count)
   DBuf<int32_t> ent_offsets;  // (n_groups + 1)
   DBuf<int32_t> ent_j;        // (n_entries)
   DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset

@@ -733,6 +733,29 @@ __global__ void k_remap_rows(int64_t n_rows, const int32_t* __restrict__ newpos,
 
 static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+__global__ void k_group_keys(const int32_t* __restrict__ ent_off, int64_t n_groups, int32_t* __restrict__ keys,
+                             int32_t* __restrict__ vals) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  keys[g] = 0x3fffffff - (ent_off[g + 1] - ent_off[g]);  // ascending key = descending size
+  vals[g] = (int32_t)g;
+}
+
+// force-kernel work order: groups by descending entry count (LPT)
+static cudaError_t order_groups(List* l, cudaStream_t s) {
+  DBuf<int32_t> keys, keys2, vals;
+  cudaError_t e;
+  if ((e = l->group_order.alloc(l->n_groups, s))) return e;
+  if (l->n_groups == 0) return cudaSuccess;
+  if ((e = keys.alloc(l->n_groups, s)) || (e = keys2.alloc(l->n_groups, s)) || (e = vals.alloc(l->n_groups, s)))
+    return e;
+  count_launch();
+  k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->n_groups, keys.p, vals.p);
+  e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, 30, s);
+  keys.release(s); keys2.release(s); vals.release(s);
+  return e;
+}
+
 // reorder a freshly built / pruned list's entries (see k_entry_order)
 static cudaError_t order_entries(List* l, cudaStream_t s) {
   const int64_t ne = l->n_entries;
@@ -767,7 +790,7 @@ using namespace nbx;
 static void list_release(nbx_list* l, cudaStream_t s) {
   l->offsets.release(s); l->j.release(s); l->mask.release(s); l->delta.release(s);
   l->slack.release(s); l->row_entry.release(s); l->group_first.release(s);
-  l->group_nmem.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
+  l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
   l->ent_delta.release(s); l->ent_slack.release(s); l->ent_mask.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
@@ -903,6 +926,7 @@ extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3]
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   TRY(cudaGetLastError());
   TRY(order_entries(l, s));
+  TRY(order_groups(l, s));
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
   hbits.release(s);
   *out = l;
@@ -996,6 +1020,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
                                                   l->ent_slack.p, l->ent_mask.p);
   TRY(cudaGetLastError());
   TRY(order_entries(l, s));
+  TRY(order_groups(l, s));
   keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
