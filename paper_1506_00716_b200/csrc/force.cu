@@ -772,6 +772,10 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     if ((e = wk.lj.alloc((int64_t)p->n_types * p->n_types, s))) goto cuda_fail;
     wk.lj_key.clear();
   }
+  if (!canonical && !l->ordered) {
+    if ((e = finalize_force_layout(l, s))) goto cuda_fail;
+    wk.t_ready = false;
+  }
   if (!canonical && !wk.t_ready) {
     if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s))) goto cuda_fail;
     wk.t_ready = true;

@@ -106,6 +106,7 @@ struct List {
   int64_t super_size = 0, super_groups = 0, super_entries = 0;
   DBuf<int32_t> super_offsets, super_j, super_pair;
   ForceWork work;
+  bool ordered = false;  // finalize_force_layout done
   int mask_words() const { return m == 8 ? 2 : 1; }
 };
 
@@ -116,6 +117,9 @@ void count_launch(int64_t k = 1);
 // k_force event timing (nbx_timing_*)
 bool timing_enabled();
 void timing_record(cudaEvent_t a, cudaEvent_t b);
+
+struct List;
+cudaError_t finalize_force_layout(List* l, cudaStream_t s);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

@@ -18,6 +18,7 @@
 //     single-shift validity test (force.cu).
 // Two passes (count, write) around a scan keep the output deterministic.
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <utility>
 
 #include "internal.cuh"
@@ -553,6 +554,134 @@ k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, cons
   }
 }
 
+// Entry-wise prune (pairlist.py:242-282 decisions, bit-identical): one warp
+// per group, lane = (entry slot r of 32/m, j-atom b) as in the force kernel;
+// the group's 16 i-atoms sit in shared memory in the group frame, j-atoms are
+// coalesced float4 loads shifted by the entry's frame offset.  Per entry the
+// result is a G-bit "member kept" word; canonical rows and entry masks follow.
+template <int M, int G>
+__global__ void __launch_bounds__(ROWS_WARPS * 32)
+k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem, int64_t n_groups,
+                const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
+                const float4* __restrict__ ent_delta, const uint64_t* __restrict__ ent_mask,
+                const float4* __restrict__ xl, const double* __restrict__ bbox, const double* __restrict__ pos,
+                Box box, double r2, uint32_t* __restrict__ ent_keep) {
+  constexpr int R = 32 / M;
+  constexpr int IA = G * M;
+  constexpr int MM = M * M;
+  constexpr int W = (G * M * M > 64) ? 2 : 1;
+  __shared__ float4 s_xi[ROWS_WARPS][IA];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane / M, b = lane % M;
+  const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
+  const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
+  const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
+  for (int64_t g = blockIdx.x * (int64_t)ROWS_WARPS + w; g < n_groups; g += (int64_t)gridDim.x * ROWS_WARPS) {
+    const int32_t first = grp_first[g];
+    const int nmem = grp_nmem[g];
+    __syncwarp();
+    for (int ia = lane; ia < IA; ia += 32) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ia < nmem * M) {
+        const int64_t c = first + ia / M;
+        v = xl[(int64_t)first * M + ia];
+        v.x = (float)((bbox[6 * c] - bbox[6 * (int64_t)first]) + (double)v.x);
+        v.y = (float)((bbox[6 * c + 1] - bbox[6 * (int64_t)first + 1]) + (double)v.y);
+        v.z = (float)((bbox[6 * c + 2] - bbox[6 * (int64_t)first + 2]) + (double)v.z);
+      }
+      s_xi[w][ia] = v;
+    }
+    __syncwarp();
+    const int32_t e_beg = ent_off[g], e_end = ent_off[g + 1];
+    for (int32_t e0 = e_beg; e0 < e_end; e0 += R) {
+      const int32_t e = e0 + r;
+      const bool valid = e < e_end;
+      uint32_t inbits = 0;   // members with a pair within r_list in this lane's column
+      int32_t cj = -1;
+      if (valid) {
+        cj = __ldg(ent_j + e);
+        const float4 d = __ldg(ent_delta + e);
+        float4 xj = __ldg(xl + (int64_t)cj * M + b);
+        xj.x += d.x;
+        xj.y += d.y;
+        xj.z += d.z;
+        uint32_t wd[2 * W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          const uint64_t mw = __ldg(ent_mask + (int64_t)e * W + q) >> b;
+          wd[2 * q] = (uint32_t)mw;
+          wd[2 * q + 1] = (uint32_t)(mw >> 32);
+        }
+        uint32_t amb = 0;
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+#pragma unroll
+          for (int a = 0; a < M; ++a) {
+            const int p = (W == 2 ? k * 64 : k * MM) + a * M;
+            if (!(wd[p >> 5] & (1u << (p & 31)))) continue;
+            const float4 xi = s_xi[w][k * M + a];
+            float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
+            dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
+            dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
+            dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
+            const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (f < lo) inbits |= 1u << k;
+            else if (f <= hi) amb |= 1u << (k * M + a);
+          }
+        }
+        while (amb) {  // rare: exact FP64 replay of the reference decision
+          const int ia = __ffs(amb) - 1;
+          amb &= amb - 1;
+          const int k = ia / M;
+          if ((inbits >> k) & 1u) continue;
+          if (exact_within(pos, (int64_t)first * M + ia, (int64_t)cj * M + b, box, r2)) inbits |= 1u << k;
+        }
+      }
+      // OR over the entry's M lanes
+#pragma unroll
+      for (int o = 1; o < M; o <<= 1) inbits |= __shfl_xor_sync(0xffffffffu, inbits, o);
+      if (valid && b == 0) {
+        if (cj >= first && cj < first + nmem) inbits |= 1u << (cj - first);  // diagonal rows always survive
+        ent_keep[e] = inbits;
+      }
+    }
+  }
+}
+
+// canonical rows from the entries' member bits; entry masks keep only the
+// surviving members
+__global__ void k_rows_from_entries(const int32_t* __restrict__ offsets, const int32_t* __restrict__ row_entry,
+                                    int64_t n_clusters, int G, const int32_t* __restrict__ cell_of_cluster,
+                                    const int32_t* __restrict__ col_first, const uint32_t* __restrict__ ent_keep,
+                                    int32_t* __restrict__ keep) {
+  // one warp per i-cluster, lanes over its rows (coalesced)
+  const int64_t ci = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (ci >= n_clusters) return;
+  const int k = (int)((ci - col_first[cell_of_cluster[ci]]) % G);
+  const int32_t r1 = offsets[ci + 1];
+  for (int32_t row = offsets[ci] + (threadIdx.x & 31); row < r1; row += 32)
+    keep[row] = (__ldg(ent_keep + __ldg(row_entry + row)) >> k) & 1u;
+}
+
+__global__ void k_entries_keep(const uint32_t* __restrict__ ent_keep, int64_t n_ent, int m, int G,
+                               const uint64_t* __restrict__ emask_in, uint64_t* __restrict__ emask_out,
+                               int32_t* __restrict__ alive) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_ent) return;
+  const uint32_t kb = ent_keep[e];
+  const int mm = m * m;
+  if (m == 8) {
+    for (int k = 0; k < 2; ++k) emask_out[e * 2 + k] = ((kb >> k) & 1u) ? emask_in[e * 2 + k] : 0ull;
+  } else {
+    uint64_t keepmask = 0;
+    const uint64_t one = (mm == 64) ? ~0ull : ((1ull << mm) - 1ull);
+    for (int k = 0; k < G; ++k)
+      if ((kb >> k) & 1u) keepmask |= one << (k * mm);
+    emask_out[e] = emask_in[e] & keepmask;
+  }
+  alive[e] = kb != 0u;
+}
+
 template <int MODE>
 static void launch_rows(int m, int64_t nc, cudaStream_t s, const int32_t* offsets, const int32_t* jv,
                         const uint64_t* mask, const float4* rdelta, const int32_t* row_entry, int G, const double* pos, const float4* xl,
@@ -783,6 +912,18 @@ static cudaError_t order_entries(List* l, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Force layout finishing touches, done once per list at its first force pass
+// (lists that are only pruned never pay for them): entries ordered by member
+// pattern within each group, groups ordered by descending size.
+cudaError_t finalize_force_layout(List* l, cudaStream_t s) {
+  if (l->ordered) return cudaSuccess;
+  cudaError_t e;
+  if ((e = order_entries(l, s))) return e;
+  if ((e = order_groups(l, s))) return e;
+  l->ordered = true;
+  return cudaSuccess;
+}
+
 }  // namespace nbx
 
 using namespace nbx;
@@ -925,8 +1066,6 @@ extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3]
         l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   TRY(cudaGetLastError());
-  TRY(order_entries(l, s));
-  TRY(order_groups(l, s));
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
   hbits.release(s);
   *out = l;
@@ -965,6 +1104,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   DBuf<int32_t> keep, scan, alive, escan;
   DBuf<uint64_t> emask;
   DBuf<float4> xl;
+  DBuf<uint32_t> ekeep;
   int32_t h[2] = {0, 0};
   TRY(keep.alloc(nr + 1, s));
   TRY(scan.alloc(nr + 1, s));
@@ -973,14 +1113,29 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(emask.alloc(ne * W, s));
   TRY(cudaMemsetAsync(keep.p, 0, 4 * (nr + 1), s));
   TRY(cudaMemsetAsync(alive.p, 0, 4 * (ne + 1), s));
-  if (ne) TRY(cudaMemcpyAsync(emask.p, in->ent_mask.p, 8 * ne * W, cudaMemcpyDeviceToDevice, s));
+  TRY(ekeep.alloc(ne + 1, s));
   TRY(xl.alloc(nc * in->m, s));
   if (nc > 0) {
-    count_launch();
+    count_launch(4);
     k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, grid->bbox.p, nc * in->m, in->m, xl.p);
-    launch_rows<0>(in->m, nc, s, in->offsets.p, in->j.p, in->mask.p, in->delta.p, in->row_entry.p, in->G, pos, xl.p,
-                   bx, in->r_list * in->r_list, grid->cell_of_cluster.p, grid->col_first.p, keep.p,
-                   emask.p, alive.p, nullptr);
+    const int pblocks = (int)std::min<int64_t>((in->n_groups + ROWS_WARPS - 1) / ROWS_WARPS, 148 * 16);
+    const double r2 = in->r_list * in->r_list;
+#define NBX_PRUNE(MM, GG)                                                                                    \
+  k_prune_entries<MM, GG><<<pblocks, ROWS_WARPS * 32, 0, s>>>(in->group_first.p, in->group_nmem.p, in->n_groups, \
+                                                              in->ent_offsets.p, in->ent_j.p, in->ent_delta.p,    \
+                                                              in->ent_mask.p, xl.p, grid->bbox.p, pos, bx, r2, ekeep.p)
+    if (pblocks > 0) {
+      switch (in->m) {
+        case 1: NBX_PRUNE(1, 16); break;
+        case 2: NBX_PRUNE(2, 8); break;
+        case 4: NBX_PRUNE(4, 4); break;
+        default: NBX_PRUNE(8, 2); break;
+      }
+    }
+#undef NBX_PRUNE
+    k_rows_from_entries<<<nb(nc, 8), 256, 0, s>>>(in->offsets.p, in->row_entry.p, nc, in->G, grid->cell_of_cluster.p,
+                                                    grid->col_first.p, ekeep.p, keep.p);
+    if (ne) k_entries_keep<<<nb(ne, 256), 256, 0, s>>>(ekeep.p, ne, in->m, in->G, in->ent_mask.p, emask.p, alive.p);
   }
   TRY(cudaGetLastError());
   TRY(exclusive_scan_i32(keep.p, scan.p, nr + 1, s));
@@ -1019,13 +1174,13 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
                                                   in->ent_slack.p, emask.p, l->ent_j.p, l->ent_delta.p,
                                                   l->ent_slack.p, l->ent_mask.p);
   TRY(cudaGetLastError());
-  TRY(order_entries(l, s));
-  TRY(order_groups(l, s));
   keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
+  ekeep.release(s);
   *out = l;
   return NBX_OK;
 fail:
   keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
+  ekeep.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }
