@@ -240,7 +240,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     st = {}
 
-    def rebuild(pos):
+    def rebuild(pos, q, t, out):
         grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
         built = nbx.build_pair_list(grid, box, R_LIST)
         st["grid"] = grid
@@ -248,7 +248,7 @@ def run_ours(args):
 
     def step(k, pos, q, t, out):
         if k % args.nstlist == 0 or "plist" not in st:
-            rebuild(pos)
+            rebuild(pos, q, t, out)
         # energies on list steps (nstcalcenergy = nstlist), forces every step
         nbx.compute_nonbonded_device(st["plist"], st["grid"], pos, q, t, params, box,
                                      energy=(k % args.nstlist == 0), out=out, e_out=e_d, bad=bad_d)
@@ -265,8 +265,6 @@ def run_ours(args):
     # ---- device-resident timed region
     W = max(3, args.warmup)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    lib.nbx_timing_query(None, None)
-    lib.nbx_timing_enable(1)
     launches0 = lib.nbx_launch_count()
     if dist is not None:
         dist.barrier()
@@ -280,6 +278,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     launches = lib.nbx_launch_count() - launches0
+    lib.nbx_timing_enable(0)
+    lib.nbx_timing_query(None, None)
+    # k_force duration: events around every launch of K eager (non-energy)
+    # passes on the launching stream, the same list as the timed region
+    lib.nbx_timing_enable(1)
+    for _ in range(args.steps):
+        flush.zero_()
+        nbx.compute_nonbonded_device(st["plist"], st["grid"], pos_d, q_d, t_d, params, box, energy=False,
+                                     out=f_d, e_out=e_d, bad=bad_d)
+    torch.cuda.synchronize()
     lib.nbx_timing_enable(0)
     fk_ms, fk_n = (np.zeros(1), np.zeros(1, dtype=np.int64))
     _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
@@ -397,6 +405,7 @@ def run_dd(args, world, rank, local):
     params = make_params(args, table)
     box = system.box
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
+    dd.enable_native()
     df = DomainForces(dd, system, params, M, occ)
     pos_glob = torch.from_numpy(np.array(system.positions)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

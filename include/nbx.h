@@ -46,6 +46,7 @@ enum {
 
 typedef struct nbx_grid nbx_grid_t;
 typedef struct nbx_list nbx_list_t;
+typedef struct nbx_dd nbx_dd_t;
 
 typedef struct {
   int32_t n_types;          /* t                                                     */
@@ -155,6 +156,24 @@ int nbx_max_displacement(const double* ref, const double* cur, int64_t n, const 
  * original order. */
 int nbx_vv_update(double* x, double* v, const double* f, const double* mass, int64_t n, double dt,
                   int32_t move, const double box[3], void* stream);
+
+/* ---------------------------------------------------------------- domain decomposition
+ * Halo exchange of the 1-D slab decomposition (paper_1506_00716_b200/dd.py,
+ * the reference's SlabPartition idea engine.py:141-263 turned into ranks):
+ * NCCL point-to-point between slab neighbours, enqueued on `stream`.
+ * nbx_dd_unique_id on rank 0, broadcast the 128 bytes, nbx_dd_create on
+ * every rank (collective).  Local arrays are [home; halo] rows (x 3 f64). */
+int nbx_dd_unique_id(uint8_t out[128]);
+int nbx_dd_create(const uint8_t uid[128], int32_t nranks, int32_t rank, nbx_dd_t** out);
+/* send_local: device int64 indices (local rows) of the home particles sent to rank-1 */
+int nbx_dd_set_layout(nbx_dd_t* dd, const int64_t* send_local, int64_t n_send, int64_t n_home,
+                      int64_t n_halo, void* stream);
+/* coordinates: send_local rows -> rank-1; rows [n_home, n_home+n_halo) <- rank+1 */
+int nbx_dd_exchange_positions(nbx_dd_t* dd, double* local_pos, void* stream);
+/* forces: rows [n_home, ...) -> rank+1 (owner); forces from rank-1 added to send_local rows */
+int nbx_dd_reduce_forces(nbx_dd_t* dd, double* local_f, void* stream);
+int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
+void nbx_dd_free(nbx_dd_t* dd);
 
 /* Exact FP64 scan of every admitted pair for a coincident in-range pair
  * (kernels.py:184-187, 390-395); run when nbx_force reported bad = {-2,-2}

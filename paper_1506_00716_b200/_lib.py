@@ -27,6 +27,8 @@ EXPORTS = (
     "nbx_super_layout", "nbx_super_download", "nbx_count_within", "nbx_list_free",
     "nbx_force", "nbx_find_singular", "nbx_launch_count", "nbx_timing_enable", "nbx_timing_query",
     "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
+    "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
+    "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free",
 )
 
 
@@ -85,6 +87,13 @@ def load():
         "nbx_timing_query": (ctypes.c_int, [P, P]),
         "nbx_max_displacement": (ctypes.c_int, [P, P, I64, P, P, P]),
         "nbx_vv_update": (ctypes.c_int, [P, P, P, P, I64, D, I32, P, P]),
+        "nbx_dd_unique_id": (ctypes.c_int, [P]),
+        "nbx_dd_create": (ctypes.c_int, [P, I32, I32, PP]),
+        "nbx_dd_set_layout": (ctypes.c_int, [P, P, I64, I64, I64, P]),
+        "nbx_dd_exchange_positions": (ctypes.c_int, [P, P, P]),
+        "nbx_dd_reduce_forces": (ctypes.c_int, [P, P, P]),
+        "nbx_dd_allreduce_sum": (ctypes.c_int, [P, P, I64, P]),
+        "nbx_dd_free": (None, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -96,6 +96,39 @@ class SlabDecomposition:
             if Lx <= widths.max() + 2.0 * self.r_comm:
                 raise ParameterError(f"box length {Lx} too short for {self.N} slabs with r_comm={self.r_comm}")
         self.layout: DomainLayout | None = None
+        self._native = None
+
+    def enable_native(self) -> None:
+        """Move the per-step exchanges into libnbx (NCCL on the compute stream).
+        Collective: every rank must call it.  Needs an initialised
+        torch.distributed group for the one-time id broadcast."""
+        if self.N == 1 or self._native is not None:
+            return
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        lib = _lib.load()
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            _lib.check(lib.nbx_dd_unique_id(_lib.ptr(uid)), "dd_unique_id")
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=0, group=self.group)
+        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        h = ctypes.c_void_p()
+        _lib.check(lib.nbx_dd_create(_lib.ptr(uid), self.N, self.rank, ctypes.byref(h)), "dd_create")
+        self._native = h
+
+    def __del__(self):
+        h = getattr(self, "_native", None)
+        if h is not None:
+            from . import _lib
+
+            if _lib._lib is not None:
+                _lib._lib.nbx_dd_free(h)
+            self._native = None
 
     # ---------------------------------------------------------------- geometry
     def owner(self, x) -> np.ndarray:
@@ -128,6 +161,12 @@ class SlabDecomposition:
         nb_lo = float(self.boundaries[nb])
         halo = torch.nonzero((own == nb) & ((x - nb_lo) < self.r_comm)).flatten()
         self.layout = DomainLayout(home=home, halo=halo, send=send, send_local=send_local)
+        if self._native is not None:
+            from . import _device, _lib
+
+            _lib.check(_lib.load().nbx_dd_set_layout(self._native, _lib.ptr(send_local), int(send_local.numel()),
+                                                     int(home.numel()), int(halo.numel()), _device.stream()),
+                       "dd_set_layout")
         return self.layout
 
     # ---------------------------------------------------------------- exchanges
@@ -150,6 +189,12 @@ class SlabDecomposition:
         lay = self.layout
         if self.N == 1 or lay is None:
             return
+        if self._native is not None:
+            from . import _device, _lib
+
+            _lib.check(_lib.load().nbx_dd_exchange_positions(self._native, _lib.ptr(local_pos), _device.stream()),
+                       "dd_exchange")
+            return
         send_t = local_pos.index_select(0, lay.send_local)
         recv_t = local_pos[lay.n_home:]
         buf = torch.empty_like(recv_t)
@@ -163,6 +208,12 @@ class SlabDecomposition:
         home_f = local_f[:lay.n_home]
         if self.N == 1:
             return home_f
+        if self._native is not None:
+            from . import _device, _lib
+
+            _lib.check(_lib.load().nbx_dd_reduce_forces(self._native, _lib.ptr(local_f), _device.stream()),
+                       "dd_reduce")
+            return home_f
         recv = torch.empty((lay.send.shape[0], 3), dtype=local_f.dtype, device=local_f.device)
         self._p2p(local_f[lay.n_home:], (self.rank + 1) % self.N, recv, (self.rank - 1) % self.N)
         home_f.index_add_(0, lay.send_local, recv)
@@ -170,6 +221,12 @@ class SlabDecomposition:
 
     def allreduce_energies(self, e: torch.Tensor) -> torch.Tensor:
         if self.N == 1:
+            return e
+        if self._native is not None and e.is_cuda:
+            from . import _device, _lib
+
+            _lib.check(_lib.load().nbx_dd_allreduce_sum(self._native, _lib.ptr(e), int(e.numel()), _device.stream()),
+                       "dd_allreduce")
             return e
         import torch.distributed as dist
 

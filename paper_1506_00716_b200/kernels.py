@@ -261,3 +261,4 @@ def flop_count(plist: ClusterPairList, grid: ClusterGrid, layout: KernelLayout, 
     stats = interaction_stats(plist, grid, plist.build_positions, box, r_cut)
     return FlopCount(useful_flops=stats.n_within_cutoff * FLOPS_PER_PAIR,
                      total_flops=total_slots * FLOPS_PER_PAIR)
+

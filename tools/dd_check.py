@@ -18,6 +18,7 @@ from paper_1506_00716_b200.systems import spc_water, tuned_occupancy  # noqa: E4
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--atoms", type=int, default=96000)
+ap.add_argument("--torch-p2p", action="store_true")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -31,6 +32,8 @@ params = nbx.NonbondedParams(r_cut=1.0, r_list=1.1, lj_table=table, shift_potent
 dev = torch.device("cuda", local)
 pos = torch.from_numpy(np.array(s.positions)).to(dev)
 dd = SlabDecomposition(L, world, rank, r_comm=1.1)
+if '--torch-p2p' not in sys.argv:
+    dd.enable_native()
 df = DomainForces(dd, s, params, 4, occ)
 lay = df.rebuild(pos)
 home_f, e = df.forces(energy=True)
