@@ -242,9 +242,8 @@ def run_ours(args):
 
     def rebuild(pos, q, t, out):
         grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
-        built = nbx.build_pair_list(grid, box, R_LIST)
         st["grid"] = grid
-        st["plist"] = nbx.prune_pair_list(built, grid.clustered_positions_device, box)
+        st["plist"] = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box)
 
     def step(k, pos, q, t, out):
         if k % args.nstlist == 0 or "plist" not in st:
@@ -254,6 +253,10 @@ def run_ours(args):
                                      energy=(k % args.nstlist == 0), out=out, e_out=e_d, bad=bad_d)
 
     clocks = Clocks(local)
+    # setup (not timed, not counted as warm-up steps): two full list cycles so
+    # the stream-ordered memory pool holds two list generations (steady state)
+    for k in range(2 * args.nstlist if args.nstlist <= 50 else 2):
+        step(k, pos_d, q_d, t_d, f_d)
     for k in range(max(3, args.warmup)):
         step(k, pos_d, q_d, t_d, f_d)
     torch.cuda.synchronize()
@@ -293,6 +296,8 @@ def run_ours(args):
     _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
     clk = clocks.stop()
     t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if os.environ.get("NBX_BENCH_DEBUG"):
+        print("per-step ms:", [round(a.elapsed_time(b), 3) for a, b in ev], file=sys.stderr)
     if dist is not None:
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -422,6 +427,8 @@ def run_dd(args, world, rank, local):
         return df.forces(energy=(k % args.nstlist == 0))
 
     W = max(3, args.warmup)
+    for k in range(2 * args.nstlist if args.nstlist <= 50 else 2):  # setup: memory pool steady state
+        step(k)
     for k in range(W):
         step(k)
     torch.cuda.synchronize()

@@ -104,6 +104,13 @@ int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], double r_lis
  * from the masks (their owner computes them).  Otherwise identical. */
 int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3], double r_list, const uint8_t* halo,
                           void* stream, nbx_list_t** out);
+/* prune_pair_list(build_pair_list(...), positions) in one search (the exact
+ * prune criterion applied to each bounding-box hit before it is stored):
+ * bit-identical to the two-step result, without the unpruned list.
+ * positions: device clustered (n_slots, 3) f64, NULL = the grid's build
+ * positions. */
+int nbx_pairlist_build_pruned(const nbx_grid_t* grid, const double box[3], double r_list,
+                              const double* positions, const uint8_t* halo, void* stream, nbx_list_t** out);
 /* Replaces pairlist.prune_pair_list (pairlist.py:242-282): keep rows whose
  * exact FP64 min-image distance over admitted slot pairs is <= r_list, plus
  * every diagonal row.  clustered_positions: device (n_slots, 3) f64. */

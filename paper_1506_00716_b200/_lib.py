@@ -28,7 +28,7 @@ EXPORTS = (
     "nbx_force", "nbx_find_singular", "nbx_launch_count", "nbx_timing_enable", "nbx_timing_query",
     "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
-    "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free",
+    "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
 )
 
 
@@ -73,6 +73,7 @@ def load():
         "nbx_grid_free": (None, [P]),
         "nbx_pairlist_build": (ctypes.c_int, [P, P, D, P, PP]),
         "nbx_pairlist_build_ex": (ctypes.c_int, [P, P, D, P, P, PP]),
+        "nbx_pairlist_build_pruned": (ctypes.c_int, [P, P, D, P, P, P, PP]),
         "nbx_pairlist_prune": (ctypes.c_int, [P, P, P, P, P, PP]),
         "nbx_list_info": (ctypes.c_int, [P, P]),
         "nbx_list_download": (ctypes.c_int, [P, P, P, P, P]),

@@ -25,7 +25,16 @@ struct DBuf {
     n = count;
     if (count <= 0) return cudaSuccess;
     ensure_pool();
-    return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, s);
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), size_class(sizeof(T) * (size_t)count), s);
+  }
+  // round up to {1, 1.25, 1.5, 1.75} x 2^k so that the per-rebuild buffers of
+  // slightly different sizes reuse the same pool blocks
+  static size_t size_class(size_t b) {
+    if (b <= 4096) return b;
+    size_t p = 1;
+    while ((p << 1) <= b) p <<= 1;
+    const size_t q = p >> 2;
+    return ((b + q - 1) / q) * q;
   }
   void release(cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);

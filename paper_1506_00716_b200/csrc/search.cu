@@ -93,9 +93,12 @@ __device__ __forceinline__ void image_delta(const double* bi, const double* oi, 
 
 constexpr int SEARCH_WARPS = 4;
 constexpr int GMAX = 16;
-constexpr int STASH = 1024;  // hits kept per group between the two passes
+constexpr int STASH = 512;   // hits kept per group between the two passes (overflow: recompute)
 
 struct SearchOut {
+  // fused prune (nbx_pairlist_build_pruned): positions the exact criterion uses
+  const float4* xl = nullptr;     // cluster-local FP32 coordinates (bbox-corner frames)
+  const double* ppos = nullptr;   // clustered FP64 positions (exact fallback)
   // pass 1
   int32_t* row_count;   // (n_clusters)
   int32_t* ent_count;   // (n_groups)
@@ -224,6 +227,61 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
   ecnt += __popc(eb);
 }
 
+// Fused prune (pairlist.py:242-282): keep member k of a hit only if one of
+// its admitted slot pairs with cj is within r_list (FP32 decision outside
+// +-1e-4 r^2, exact FP64 replay inside), diagonal rows always.
+__device__ __noinline__ bool exact_within(const double* __restrict__ pos, int64_t si, int64_t sj, Box box,
+                                          double r2);
+__device__ __forceinline__ uint32_t prune_bits(uint32_t bits, int32_t cj, const SearchCtx& C, const float4* s_xi,
+                                               const double* gb, const double (*s_bb)[6], const SearchOut& out,
+                                               const int8_t* __restrict__ nreal, const uint8_t* __restrict__ halo,
+                                               int m, const Box& box) {
+  if (!bits) return 0u;
+  const float lo = (float)(C.r2 * (1.0 - 1e-4)), hi = (float)(C.r2 * (1.0 + 1e-4));
+  double bj[6];
+  for (int d = 0; d < 6; ++d) bj[d] = C.bbox[6 * (int64_t)cj + d];
+  float4 dlt;
+  float slack;
+  image_delta(gb, s_bb[0], bj, box, &dlt, &slack);
+  float4 xj[8];
+  for (int b = 0; b < m; ++b) {
+    xj[b] = __ldg(out.xl + (int64_t)cj * m + b);
+    xj[b].x += dlt.x;
+    xj[b].y += dlt.y;
+    xj[b].z += dlt.z;
+  }
+  const int nr_j = nreal[cj];
+  uint32_t keep = 0;
+  for (int k = 0; k < C.nmem; ++k) {
+    if (!((bits >> k) & 1u)) continue;
+    const int32_t ci = C.first + k;
+    if (ci == cj) {
+      keep |= 1u << k;
+      continue;
+    }
+    uint64_t mk = row_mask(m, nreal[ci], nr_j, false);
+    if (halo) mk &= ~halo_pair_mask(halo[ci], halo[cj], m);
+    bool found = false;
+    for (int a = 0; a < m && !found; ++a) {
+      const float4 xi = s_xi[k * m + a];
+      for (int b = 0; b < m; ++b) {
+        if (!((mk >> (a * m + b)) & 1ull)) continue;
+        float dx = xi.x - xj[b].x, dy = xi.y - xj[b].y, dz = xi.z - xj[b].z;
+        dx = fmaf(-C.Lf[0], rintf(dx / C.Lf[0]), dx);
+        dy = fmaf(-C.Lf[1], rintf(dy / C.Lf[1]), dy);
+        dz = fmaf(-C.Lf[2], rintf(dz / C.Lf[2]), dz);
+        const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (f < lo || (f <= hi && exact_within(out.ppos, (int64_t)ci * m + a, (int64_t)cj * m + b, box, C.r2))) {
+          found = true;
+          break;
+        }
+      }
+    }
+    if (found) keep |= 1u << k;
+  }
+  return keep;
+}
+
 // MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
 // by re-running the search for groups whose hits overflowed it).
 template <int MODE>
@@ -235,6 +293,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
   __shared__ double s_bb[SEARCH_WARPS][GMAX][6];
   __shared__ float4 s_bf[SEARCH_WARPS][GMAX][2];
   __shared__ int32_t s_q[SEARCH_WARPS][64];
+  __shared__ float4 s_xi[SEARCH_WARPS][16];  // fused prune: the group's i-atoms in the group frame
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = blockIdx.x * (int64_t)SEARCH_WARPS + w;
   if (g >= n_groups) return;
@@ -253,6 +312,20 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
     s_bf[w][lane][1] = bbf[2 * (int64_t)(C.first + lane) + 1];
   }
   __syncwarp();
+  if (out.xl) {
+    for (int ia = lane; ia < 16; ia += 32) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ia < C.nmem * m) {
+        const int k = ia / m;
+        v = __ldg(out.xl + (int64_t)C.first * m + ia);
+        v.x = (float)((s_bb[w][k][0] - s_bb[w][0][0]) + (double)v.x);
+        v.y = (float)((s_bb[w][k][1] - s_bb[w][0][1]) + (double)v.y);
+        v.z = (float)((s_bb[w][k][2] - s_bb[w][0][2]) + (double)v.z);
+      }
+      s_xi[w][ia] = v;
+    }
+    __syncwarp();
+  }
   double gb[6];  // group AABB
   for (int d = 0; d < 3; ++d) {
     gb[d] = s_bb[w][0][d];
@@ -287,7 +360,8 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
 
   auto process = [&](int n_items) {  // the first n_items of the queue
     const int32_t cj = lane < n_items ? s_q[w][lane] : 0;
-    const uint32_t bits = lane < n_items ? member_bits(C, s_bf[w], s_bb[w], cj, box) : 0u;
+    uint32_t bits = lane < n_items ? member_bits(C, s_bf[w], s_bb[w], cj, box) : 0u;
+    if (out.xl) bits = prune_bits(bits, cj, C, s_xi[w], gb, s_bb[w], out, nreal, halo, m, box);
     if (MODE == 0) {
       const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
       for (int k = 0; k < C.nmem; ++k) {
@@ -969,8 +1043,26 @@ extern "C" int nbx_pairlist_build(const nbx_grid_t* grid, const double box[3], d
   return nbx_pairlist_build_ex(grid, box, r_list, nullptr, stream, out);
 }
 
+static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], double r_list, const uint8_t* halo,
+                               const double* prune_pos, void* stream, nbx_list_t** out);
+
 extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3], double r_list,
                                      const uint8_t* halo, void* stream, nbx_list_t** out) {
+  return pairlist_build_impl(grid, box, r_list, halo, nullptr, stream, out);
+}
+
+extern "C" int nbx_pairlist_build_pruned(const nbx_grid_t* grid, const double box[3], double r_list,
+                                         const double* positions, const uint8_t* halo, void* stream,
+                                         nbx_list_t** out) {
+  if (!grid) {
+    set_error("nbx_pairlist_build_pruned: null grid");
+    return NBX_ERR_PARAM;
+  }
+  return pairlist_build_impl(grid, box, r_list, halo, positions ? positions : grid->cpos.p, stream, out);
+}
+
+static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], double r_list, const uint8_t* halo,
+                               const double* prune_pos, void* stream, nbx_list_t** out) {
   if (!grid || !box || !out) {
     set_error("nbx_pairlist_build: null argument");
     return NBX_ERR_PARAM;
@@ -999,6 +1091,7 @@ extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3]
   DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
   DBuf<int2> stash;
   DBuf<uint8_t> hbits;
+  DBuf<float4> xl;
   int32_t h[2] = {0, 0};
   SearchOut so{};
   TRY(ng.alloc(n_cols + 1, s));
@@ -1018,6 +1111,13 @@ extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3]
   TRY(cudaMemsetAsync(row_count.p, 0, 4 * (nc + 1), s));
   TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
   TRY(stash.alloc(l->n_groups * (int64_t)STASH, s));
+  if (prune_pos && nc > 0) {
+    TRY(xl.alloc(nc * m, s));
+    count_launch();
+    k_local_coords<<<nb(nc * m, 256), 256, 0, s>>>(prune_pos, grid->bbox.p, nc * m, m, xl.p);
+    so.xl = xl.p;
+    so.ppos = prune_pos;
+  }
   if (halo && nc > 0) {
     TRY(hbits.alloc(nc, s));
     count_launch();
@@ -1067,12 +1167,12 @@ extern "C" int nbx_pairlist_build_ex(const nbx_grid_t* grid, const double box[3]
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   TRY(cudaGetLastError());
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
-  hbits.release(s);
+  hbits.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
 fail:
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
-  hbits.release(s);
+  hbits.release(s); xl.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }

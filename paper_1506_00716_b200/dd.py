@@ -243,20 +243,30 @@ class SlabDecomposition:
         import torch.distributed as dist
 
         dev = pos.device
+        nccl = dist.get_backend(self.group) == "nccl"
         cnt = torch.tensor([ids.shape[0]], dtype=torch.int64, device=dev)
-        counts = [torch.zeros_like(cnt) for _ in range(self.N)]
-        dist.all_gather(counts, cnt, group=self.group)
-        cmax = int(max(int(c.item()) for c in counts))
+        if nccl:
+            counts = torch.empty(self.N, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(counts, cnt, group=self.group)
+        else:
+            parts = [torch.zeros_like(cnt) for _ in range(self.N)]
+            dist.all_gather(parts, cnt, group=self.group)
+            counts = torch.cat(parts)
+        cmax = int(counts.max().item())  # one host sync
         pad_ids = torch.full((cmax,), -1, dtype=torch.int64, device=dev)
         pad_ids[:ids.shape[0]] = ids
         pad_pos = torch.zeros((cmax, 3), dtype=pos.dtype, device=dev)
         pad_pos[:ids.shape[0]] = pos
-        all_ids = [torch.empty_like(pad_ids) for _ in range(self.N)]
-        all_pos = [torch.empty_like(pad_pos) for _ in range(self.N)]
-        dist.all_gather(all_ids, pad_ids, group=self.group)
-        dist.all_gather(all_pos, pad_pos, group=self.group)
-        ids_cat = torch.cat(all_ids)
-        pos_cat = torch.cat(all_pos)
+        all_ids = torch.empty((self.N, cmax), dtype=torch.int64, device=dev)
+        all_pos = torch.empty((self.N, cmax, 3), dtype=pos.dtype, device=dev)
+        if nccl:
+            dist.all_gather_into_tensor(all_ids, pad_ids, group=self.group)
+            dist.all_gather_into_tensor(all_pos, pad_pos, group=self.group)
+        else:
+            dist.all_gather(list(all_ids.unbind(0)), pad_ids, group=self.group)
+            dist.all_gather(list(all_pos.unbind(0)), pad_pos, group=self.group)
+        ids_cat = all_ids.reshape(-1)
+        pos_cat = all_pos.reshape(-1, 3)
         keep = ids_cat >= 0
         out = torch.empty((n_total, 3), dtype=pos.dtype, device=dev)
         out[ids_cat[keep]] = pos_cat[keep]

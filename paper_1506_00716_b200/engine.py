@@ -233,6 +233,7 @@ class MDState:
 
 
 def _build(system, params, m, supercluster_size, n_lane, step, policy, occupancy):
+    """engine.py:301-314: grid, list, and the prune of a reused list."""
     grid = build_cluster_grid(system, m, occupancy)
     plist = build_pair_list(grid, system.box, params.r_list, supercluster_size=supercluster_size,
                             n_lane=n_lane, build_step=step)

@@ -158,6 +158,40 @@ def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, superclust
     return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
 
 
+def build_pruned_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, positions=None, *,
+                           supercluster_size: int = 1, n_lane: int = 1, build_step: int = 0,
+                           halo=None) -> ClusterPairList:
+    """``prune_pair_list(build_pair_list(grid, box, r_list, ...), positions, box)``
+    in one GPU search (extension): each bounding-box hit is checked against
+    the exact prune criterion before it is stored, so the unpruned list is
+    never materialised.  Bit-identical to the two-step result.  ``positions``
+    (clustered, n_slots x 3) defaults to the grid's build positions."""
+    if r_list <= 0.0:
+        raise ParameterError(f"r_list must be positive, got {r_list}")
+    if np.any(box.lengths < 2.0 * r_list):
+        raise ParameterError(f"every box edge must be >= 2*r_list={2.0 * r_list} "
+                             f"for the single-image convention, got {box.lengths}")
+    if supercluster_size not in VALID_SUPERCLUSTER_SIZES:
+        raise ParameterError(f"supercluster_size must be one of {VALID_SUPERCLUSTER_SIZES}, "
+                             f"got {supercluster_size}")
+    keep_alive = None
+    if positions is None:
+        p = ctypes.c_void_p(0)
+    else:
+        shape = tuple(positions.shape)
+        if shape != (grid.n_slots, 3):
+            raise ParameterError(f"positions shape {shape} does not match the slot layout {(grid.n_slots, 3)}")
+        tmp = ClusterPairList.__new__(ClusterPairList)
+        tmp.grid = grid
+        p, keep_alive = _positions_ptr(tmp, positions)
+    h = ctypes.c_void_p()
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_pairlist_build_pruned(grid.handle, _lib.ptr(L), float(r_list), p, _lib.ptr(halo),
+                                                     dev.stream(), ctypes.byref(h)), "pairlist_build_pruned")
+    del keep_alive
+    return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+
+
 def _positions_ptr(plist: ClusterPairList, positions):
     """Device pointer for clustered positions: the grid's own build snapshot
     when that is what the caller passed, else an uploaded copy."""

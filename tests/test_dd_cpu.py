@@ -40,8 +40,10 @@ def _local_oracle_forces(pos_local, q, t, halo, L, phys):
 
 
 def _worker(rank, world, port, out_q):
+    import datetime
+
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
     try:
         from oracle import forces as of
         from paper_1506_00716_b200.dd import SlabDecomposition
@@ -80,7 +82,7 @@ def test_two_slab_decomposition_equals_single_domain():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    f_dd, e_dd = q.get(timeout=600)
+    f_dd, e_dd = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

@@ -76,6 +76,11 @@ def test_lists_set_identical(name):
     # prune is idempotent (test_pairlist.py:72-82)
     again = nbx.prune_pair_list(pruned, grid.clustered_positions, s.box)
     assert np.array_equal(again.j_idx, pruned.j_idx) and np.array_equal(again.offsets, pruned.offsets)
+    # fused build + prune (one search) is bit-identical to the two steps
+    fused = nbx.build_pruned_pair_list(grid, s.box, float(g["r_list"]), supercluster_size=sc)
+    assert np.array_equal(fused.offsets, g["pruned_offsets"])
+    assert np.array_equal(fused.j_idx, g["pruned_j"])
+    assert np.array_equal(fused.mask_bits, g["pruned_masks"])
     stats = nbx.interaction_stats(pruned, grid, grid.clustered_positions, s.box, float(g["r_cut"]))
     assert stats.n_admitted == int(g["n_admitted"])
     assert stats.n_within_cutoff == int(g["n_within"])
@@ -218,6 +223,9 @@ def test_spc24k_lists_and_forces_vs_oracle(occ_rule):
     op = native.prune_list(ob, og["clustered_positions"], L)
     assert np.array_equal(pruned.offsets, op["offsets"]) and np.array_equal(pruned.j_idx, op["j_idx"])
     assert np.array_equal(pruned.mask_bits, search.pack_masks(op["masks"]))
+    fused = nbx.build_pruned_pair_list(grid, s.box, 1.1)
+    assert np.array_equal(fused.offsets, op["offsets"]) and np.array_equal(fused.j_idx, op["j_idx"])
+    assert np.array_equal(fused.mask_bits, search.pack_masks(op["masks"]))
     layout = nbx.KernelLayout(4, 4)
     for phys, params in (
         (of.Physics(r_cut=1.0, lj_table=table, shift_potential=True),

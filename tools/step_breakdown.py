@@ -50,11 +50,12 @@ def main():
         grid, g_ms, g_w = timed(lambda: nbx.build_cluster_grid(s, 4, occ, positions=pos))
         built, b_ms, b_w = timed(lambda: nbx.build_pair_list(grid, s.box, 1.1))
         pl, p_ms, p_w = timed(lambda: nbx.prune_pair_list(built, grid.clustered_positions_device, s.box))
+        pf, bp_ms, bp_w = timed(lambda: nbx.build_pruned_pair_list(grid, s.box, 1.1))
         _, f1_ms, f1_w = timed(lambda: nbx.compute_nonbonded_device(pl, grid, pos, q, t, params, s.box, out=out))
         _, f2_ms, f2_w = timed(lambda: nbx.compute_nonbonded_device(pl, grid, pos, q, t, params, s.box, out=out,
                                                                      energy=False))
         print(f"rep {rep}: grid {g_ms:.3f} ms (wall {g_w:.3f}) | build {b_ms:.3f} ({b_w:.3f}) | prune {p_ms:.3f} "
-              f"({p_w:.3f}) | force#1 {f1_ms:.3f} ({f1_w:.3f}) | force {f2_ms:.3f} ({f2_w:.3f})")
+              f"({p_w:.3f}) | build_pruned {bp_ms:.3f} | force#1 {f1_ms:.3f} ({f1_w:.3f}) | force {f2_ms:.3f} ({f2_w:.3f})")
     print(f"rows built {built.n_pairs} pruned {pl.n_pairs} groups {pl.n_groups} entries {pl.n_entries}")
 
 
