@@ -780,6 +780,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s))) goto cuda_fail;
     wk.t_ready = true;
   }
+  if (canonical && (e = ensure_row_delta(l, s))) goto cuda_fail;
   if (canonical && !wk.tc_ready) {
     if ((e = build_transpose(l->j.p, l->n_rows, l->n_clusters, wk.tc_first, wk.tc_items, s))) goto cuda_fail;
     wk.tc_ready = true;

@@ -99,8 +99,8 @@ struct List {
   DBuf<int32_t> offsets;    // (n_clusters + 1)
   DBuf<int32_t> j;          // (n_rows)
   DBuf<uint64_t> mask;      // (n_rows)
-  DBuf<float4> delta;       // (n_rows) j-local -> i-local offset (image included)
-  DBuf<float> slack;        // (n_rows) min_d (L - ext_i - ext_j)
+  DBuf<float4> delta;       // (n_rows) j-local -> i-local offset (image included), lazy
+  bool delta_ready = false;
   DBuf<int32_t> row_entry;  // (n_rows) entry holding this row
   // groups / entries
   DBuf<int32_t> group_first;  // (n_groups) first member cluster
@@ -108,8 +108,7 @@ struct List {
   DBuf<int32_t> group_order;  // (n_groups) force-kernel work order (descending entry count)
   DBuf<int32_t> ent_offsets;  // (n_groups + 1)
   DBuf<int32_t> ent_j;        // (n_entries)
-  DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset
-  DBuf<float> ent_slack;      // (n_entries)
+  DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset, w = slack
   DBuf<uint64_t> ent_mask;    // (n_entries * W), W = 2 for m == 8 else 1
   // reference super layout (on demand)
   int64_t super_size = 0, super_groups = 0, super_entries = 0;
@@ -129,6 +128,7 @@ void timing_record(cudaEvent_t a, cudaEvent_t b);
 
 struct List;
 cudaError_t finalize_force_layout(List* l, cudaStream_t s);
+cudaError_t ensure_row_delta(List* l, cudaStream_t s);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

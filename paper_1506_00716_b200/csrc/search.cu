@@ -108,12 +108,9 @@ struct SearchOut {
   const int32_t* ent_offsets;
   int32_t* j;
   uint64_t* mask;
-  float4* delta;
-  float* slack;
   int32_t* row_entry;
   int32_t* ent_j;
   float4* ent_delta;
-  float* ent_slack;
   uint64_t* ent_mask;
 };
 
@@ -203,11 +200,6 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
       if (halo) mk &= ~halo_pair_mask(halo[ci], halo[cj], m);
       out.j[row] = cj;
       out.mask[row] = mk;
-      float4 rdelta;
-      float rslack;
-      image_delta(s_bb[k], s_bb[k], bj, box, &rdelta, &rslack);
-      out.delta[row] = rdelta;
-      out.slack[row] = rslack;
       out.row_entry[row] = ent_pos;
       if (W == 2) emask[k] = mk;
       else emask[0] |= mk << (k * m * m);
@@ -220,7 +212,6 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
     image_delta(gb, s_bb[0], bj, box, &e_delta, &e_slack);
     out.ent_j[ent_pos] = cj;
     out.ent_delta[ent_pos] = e_delta;
-    out.ent_slack[ent_pos] = e_slack;
     out.ent_mask[(int64_t)ent_pos * W] = emask[0];
     if (W == 2) out.ent_mask[(int64_t)ent_pos * W + 1] = emask[1];
   }
@@ -784,29 +775,25 @@ __global__ void k_new_offsets(const int32_t* __restrict__ old_off, int64_t n,
 
 __global__ void k_compact_rows(int64_t n_rows, const int32_t* __restrict__ keep,
                                const int32_t* __restrict__ scan, const int32_t* __restrict__ ent_scan,
-                               const int32_t* j, const uint64_t* mask, const float4* delta,
-                               const float* slack, const int32_t* row_entry, int32_t* j2,
-                               uint64_t* mask2, float4* delta2, float* slack2, int32_t* row_entry2) {
+                               const int32_t* j, const uint64_t* mask, const int32_t* row_entry, int32_t* j2,
+                               uint64_t* mask2, int32_t* row_entry2) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_rows || !keep[r]) return;
   const int32_t p = scan[r];
   j2[p] = j[r];
   mask2[p] = mask[r];
-  delta2[p] = delta[r];
-  slack2[p] = slack[r];
   row_entry2[p] = ent_scan[row_entry[r]];
 }
 
 __global__ void k_compact_entries(int64_t n_ent, int W, const int32_t* __restrict__ alive,
                                   const int32_t* __restrict__ scan, const int32_t* ej,
-                                  const float4* edelta, const float* eslack, const uint64_t* emask,
-                                  int32_t* ej2, float4* edelta2, float* eslack2, uint64_t* emask2) {
+                                  const float4* edelta, const uint64_t* emask,
+                                  int32_t* ej2, float4* edelta2, uint64_t* emask2) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_ent || !alive[e]) return;
   const int32_t p = scan[e];
   ej2[p] = ej[e];
   edelta2[p] = edelta[e];
-  eslack2[p] = eslack[e];
   for (int w = 0; w < W; ++w) emask2[(int64_t)p * W + w] = emask[e * W + w];
 }
 
@@ -918,14 +905,13 @@ k_entry_order(const int32_t* __restrict__ ent_off, int64_t n_groups, const uint6
 }
 
 __global__ void k_permute_entries(int64_t n_ent, int W, const int32_t* __restrict__ newpos, const int32_t* ej,
-                                  const float4* edelta, const float* eslack, const uint64_t* emask, int32_t* ej2,
-                                  float4* edelta2, float* eslack2, uint64_t* emask2) {
+                                  const float4* edelta, const uint64_t* emask, int32_t* ej2, float4* edelta2,
+                                  uint64_t* emask2) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_ent) return;
   const int32_t p = newpos[e];
   ej2[p] = ej[e];
   edelta2[p] = edelta[e];
-  eslack2[p] = eslack[e];
   for (int w = 0; w < W; ++w) emask2[(int64_t)p * W + w] = emask[e * W + w];
 }
 
@@ -966,24 +952,57 @@ static cudaError_t order_entries(List* l, cudaStream_t s) {
   const int W = l->mask_words();
   DBuf<int32_t> newpos, ej;
   DBuf<float4> ed;
-  DBuf<float> es;
   DBuf<uint64_t> em;
   cudaError_t e;
-  if ((e = newpos.alloc(ne, s)) || (e = ej.alloc(ne, s)) || (e = ed.alloc(ne, s)) || (e = es.alloc(ne, s)) ||
-      (e = em.alloc(ne * W, s)))
+  if ((e = newpos.alloc(ne, s)) || (e = ej.alloc(ne, s)) || (e = ed.alloc(ne, s)) || (e = em.alloc(ne * W, s)))
     return e;
   count_launch(3);
   k_entry_order<<<nb(l->n_groups, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(l->ent_offsets.p, l->n_groups,
                                                                          l->ent_mask.p, l->m, l->G, newpos.p);
-  k_permute_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, newpos.p, l->ent_j.p, l->ent_delta.p, l->ent_slack.p,
-                                                 l->ent_mask.p, ej.p, ed.p, es.p, em.p);
+  k_permute_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, newpos.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p, ej.p,
+                                                 ed.p, em.p);
   if (l->n_rows) k_remap_rows<<<nb(l->n_rows, 256), 256, 0, s>>>(l->n_rows, newpos.p, l->row_entry.p);
   std::swap(l->ent_j, ej);
   std::swap(l->ent_delta, ed);
-  std::swap(l->ent_slack, es);
   std::swap(l->ent_mask, em);
-  newpos.release(s); ej.release(s); ed.release(s); es.release(s); em.release(s);
+  newpos.release(s); ej.release(s); ed.release(s); em.release(s);
   return cudaGetLastError();
+}
+
+// Per-row frame offsets (j-local -> i-local, image included, w = slack) for
+// the canonical-row consumers (row statistics, canonical force path); built
+// on demand, the grouped fast path never needs them.
+__global__ void k_row_delta(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, int64_t n_clusters,
+                            const double* __restrict__ bbox, Box box, float4* __restrict__ delta) {
+  const int64_t ci = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (ci >= n_clusters) return;
+  double bi[6];
+  for (int d = 0; d < 6; ++d) bi[d] = bbox[6 * ci + d];
+  for (int32_t row = offsets[ci] + (threadIdx.x & 31); row < offsets[ci + 1]; row += 32) {
+    double bj[6];
+    const int64_t cj = jv[row];
+    for (int d = 0; d < 6; ++d) bj[d] = bbox[6 * cj + d];
+    float4 dl;
+    float sl;
+    image_delta(bi, bi, bj, box, &dl, &sl);
+    delta[row] = dl;
+  }
+}
+
+cudaError_t ensure_row_delta(List* l, cudaStream_t s) {
+  if (l->delta_ready || l->n_rows == 0) return cudaSuccess;
+  cudaError_t e;
+  if ((e = l->delta.alloc(l->n_rows, s))) return e;
+  Box bx;
+  for (int d = 0; d < 3; ++d) {
+    bx.L[d] = l->L[d];
+    bx.invL[d] = 1.0 / l->L[d];
+  }
+  count_launch();
+  k_row_delta<<<nb(l->n_clusters, 8), 256, 0, s>>>(l->offsets.p, l->j.p, l->n_clusters, l->bbox, bx, l->delta.p);
+  if ((e = cudaGetLastError())) return e;
+  l->delta_ready = true;
+  return cudaSuccess;
 }
 
 // Force layout finishing touches, done once per list at its first force pass
@@ -1004,9 +1023,9 @@ using namespace nbx;
 
 static void list_release(nbx_list* l, cudaStream_t s) {
   l->offsets.release(s); l->j.release(s); l->mask.release(s); l->delta.release(s);
-  l->slack.release(s); l->row_entry.release(s); l->group_first.release(s);
+  l->row_entry.release(s); l->group_first.release(s);
   l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
-  l->ent_delta.release(s); l->ent_slack.release(s); l->ent_mask.release(s);
+  l->ent_delta.release(s); l->ent_mask.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
   w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
@@ -1143,23 +1162,17 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   l->n_entries = h[1];
   TRY(l->j.alloc(l->n_rows, s));
   TRY(l->mask.alloc(l->n_rows, s));
-  TRY(l->delta.alloc(l->n_rows, s));
-  TRY(l->slack.alloc(l->n_rows, s));
   TRY(l->row_entry.alloc(l->n_rows, s));
   TRY(l->ent_j.alloc(l->n_entries, s));
   TRY(l->ent_delta.alloc(l->n_entries, s));
-  TRY(l->ent_slack.alloc(l->n_entries, s));
   TRY(l->ent_mask.alloc(l->n_entries * l->mask_words(), s));
   so.offsets = l->offsets.p;
   so.ent_offsets = l->ent_offsets.p;
   so.j = l->j.p;
   so.mask = l->mask.p;
-  so.delta = l->delta.p;
-  so.slack = l->slack.p;
   so.row_entry = l->row_entry.p;
   so.ent_j = l->ent_j.p;
   so.ent_delta = l->ent_delta.p;
-  so.ent_slack = l->ent_slack.p;
   so.ent_mask = l->ent_mask.p;
   if (l->n_groups > 0)
     count_launch(), k_search<1><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
@@ -1248,15 +1261,12 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(l->offsets.alloc(nc + 1, s));
   TRY(l->j.alloc(l->n_rows, s));
   TRY(l->mask.alloc(l->n_rows, s));
-  TRY(l->delta.alloc(l->n_rows, s));
-  TRY(l->slack.alloc(l->n_rows, s));
   TRY(l->row_entry.alloc(l->n_rows, s));
   TRY(l->group_first.alloc(l->n_groups, s));
   TRY(l->group_nmem.alloc(l->n_groups, s));
   TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
   TRY(l->ent_j.alloc(l->n_entries, s));
   TRY(l->ent_delta.alloc(l->n_entries, s));
-  TRY(l->ent_slack.alloc(l->n_entries, s));
   TRY(l->ent_mask.alloc(l->n_entries * W, s));
   count_launch(), k_new_offsets<<<nb(nc + 1, 256), 256, 0, s>>>(in->offsets.p, nc, scan.p, l->offsets.p);
   count_launch(), k_new_offsets<<<nb(l->n_groups + 1, 256), 256, 0, s>>>(in->ent_offsets.p, l->n_groups, escan.p,
@@ -1267,12 +1277,10 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   }
   if (nr)
     count_launch(), k_compact_rows<<<nb(nr, 256), 256, 0, s>>>(nr, keep.p, scan.p, escan.p, in->j.p, in->mask.p,
-                                               in->delta.p, in->slack.p, in->row_entry.p, l->j.p,
-                                               l->mask.p, l->delta.p, l->slack.p, l->row_entry.p);
+                                               in->row_entry.p, l->j.p, l->mask.p, l->row_entry.p);
   if (ne)
     count_launch(), k_compact_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, alive.p, escan.p, in->ent_j.p, in->ent_delta.p,
-                                                  in->ent_slack.p, emask.p, l->ent_j.p, l->ent_delta.p,
-                                                  l->ent_slack.p, l->ent_mask.p);
+                                                  emask.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p);
   TRY(cudaGetLastError());
   keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
   ekeep.release(s);
@@ -1339,6 +1347,7 @@ extern "C" int nbx_count_within(const nbx_list_t* l, const double* pos, const do
   TRY(cnt.alloc(2, s));
   TRY(xl.alloc(l->n_clusters * l->m, s));
   TRY(cudaMemsetAsync(cnt.p, 0, 16, s));
+  TRY(ensure_row_delta(const_cast<nbx_list*>(static_cast<const nbx_list*>(l)), s));
   if (l->n_clusters > 0) {
     count_launch();
     k_local_coords<<<nb(l->n_clusters * l->m, 256), 256, 0, s>>>(pos, l->bbox, l->n_clusters * l->m, l->m, xl.p);
