@@ -180,6 +180,18 @@ int nbx_dd_exchange_positions(nbx_dd_t* dd, double* local_pos, void* stream);
 /* forces: rows [n_home, ...) -> rank+1 (owner); forces from rank-1 added to send_local rows */
 int nbx_dd_reduce_forces(nbx_dd_t* dd, double* local_f, void* stream);
 int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
+/* rebuild-time bookkeeping (dd.SlabDecomposition.assign): from global
+ * positions (device n x 3) and host boundaries (N+1), the rank's home / halo
+ * ids and send_local (device int64, capacity n, ascending), and on the host
+ * counts_out = {n_home, n_halo, n_send, home count of every rank}; also sets
+ * the exchange layout.  Syncs. */
+int nbx_dd_assign(nbx_dd_t* dd, const double* positions, int64_t n, double box_x, const double* boundaries,
+                  double r_comm, int64_t* home, int64_t* halo, int64_t* send_local, int64_t* counts_out,
+                  void* stream);
+/* global positions from every rank's home rows: one ncclAllGather of
+ * (id, x, y, z) records padded to cap >= max home count. */
+int nbx_dd_allgather_home(nbx_dd_t* dd, const int64_t* home_ids, const double* home_pos, int64_t n_home,
+                          int64_t cap, double* positions_global, void* stream);
 void nbx_dd_free(nbx_dd_t* dd);
 
 /* Exact FP64 scan of every admitted pair for a coincident in-range pair

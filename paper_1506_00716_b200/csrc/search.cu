@@ -275,7 +275,7 @@ __device__ __forceinline__ uint32_t prune_bits(uint32_t bits, int32_t cj, const 
 
 // MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
 // by re-running the search for groups whose hits overflowed it).
-template <int MODE>
+template <int MODE, bool PRUNE>
 __global__ void __launch_bounds__(SEARCH_WARPS * 32, 6)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
          int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
@@ -303,7 +303,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
     s_bf[w][lane][1] = bbf[2 * (int64_t)(C.first + lane) + 1];
   }
   __syncwarp();
-  if (out.xl) {
+  if (PRUNE) {
     for (int ia = lane; ia < 16; ia += 32) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (ia < C.nmem * m) {
@@ -352,7 +352,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
   auto process = [&](int n_items) {  // the first n_items of the queue
     const int32_t cj = lane < n_items ? s_q[w][lane] : 0;
     uint32_t bits = lane < n_items ? member_bits(C, s_bf[w], s_bb[w], cj, box) : 0u;
-    if (out.xl) bits = prune_bits(bits, cj, C, s_xi[w], gb, s_bb[w], out, nreal, halo, m, box);
+    if (PRUNE) bits = prune_bits(bits, cj, C, s_xi[w], gb, s_bb[w], out, nreal, halo, m, box);
     if (MODE == 0) {
       const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
       for (int k = 0; k < C.nmem; ++k) {
@@ -1146,9 +1146,13 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   so.ent_count = ent_count.p;
   so.stash = stash.p;
   if (l->n_groups > 0)
-    count_launch(), k_search<0><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+  {
+    count_launch();
+    auto k0 = so.xl ? k_search<0, true> : k_search<0, false>;
+    k0<<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
         l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
+  }
   TRY(cudaGetLastError());
   TRY(l->offsets.alloc(nc + 1, s));
   TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
@@ -1175,9 +1179,13 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   so.ent_delta = l->ent_delta.p;
   so.ent_mask = l->ent_mask.p;
   if (l->n_groups > 0)
-    count_launch(), k_search<1><<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
+  {
+    count_launch();
+    auto k1 = so.xl ? k_search<1, true> : k_search<1, false>;
+    k1<<<nb(l->n_groups, SEARCH_WARPS), SEARCH_WARPS * 32, 0, s>>>(
         l->group_first.p, l->group_nmem.p, l->n_groups, m, G, grid->bbox.p, grid->bbf.p, grid->zr.p,
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
+  }
   TRY(cudaGetLastError());
   ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
   hbits.release(s); xl.release(s);

@@ -142,6 +142,8 @@ class SlabDecomposition:
             torch.as_tensor(np.asarray(positions_global, dtype=np.float64))
         pos = pos.reshape(-1, 3)
         dev = pos.device
+        if self._native is not None and pos.is_cuda:
+            return self._assign_native(pos.contiguous())
         Lx = float(self.L[0])
         x = torch.remainder(pos[:, 0], Lx)
         x = torch.where(x >= Lx, x - Lx, x)
@@ -167,6 +169,29 @@ class SlabDecomposition:
             _lib.check(_lib.load().nbx_dd_set_layout(self._native, _lib.ptr(send_local), int(send_local.numel()),
                                                      int(home.numel()), int(halo.numel()), _device.stream()),
                        "dd_set_layout")
+        return self.layout
+
+    def _assign_native(self, pos: torch.Tensor) -> DomainLayout:
+        """assign() inside libnbx (flags + stable compaction, one host sync)."""
+        from . import _device, _lib
+
+        n = pos.shape[0]
+        if getattr(self, "_abuf_n", -1) != n:
+            self._abuf = torch.empty((3, max(n, 1)), dtype=torch.int64, device=pos.device)
+            self._abuf_n = n
+        counts = np.zeros(3 + self.N, dtype=np.int64)
+        bnd = np.ascontiguousarray(self.boundaries, dtype=np.float64)
+        _lib.check(_lib.load().nbx_dd_assign(self._native, _lib.ptr(pos), n, float(self.L[0]), _lib.ptr(bnd),
+                                             self.r_comm, _lib.ptr(self._abuf[0]), _lib.ptr(self._abuf[1]),
+                                             _lib.ptr(self._abuf[2]), _lib.ptr(counts), _device.stream()), "dd_assign")
+        nh, nl, ns = (int(c) for c in counts[:3])
+        self.home_counts = counts[3:].copy()
+        home = self._abuf[0, :nh].clone()
+        halo = self._abuf[1, :nl].clone()
+        send_local = self._abuf[2, :ns].clone()
+        self.layout = DomainLayout(home=home, halo=halo, send=home.index_select(0, send_local), send_local=send_local)
+        _lib.check(_lib.load().nbx_dd_set_layout(self._native, _lib.ptr(send_local), ns, nh, nl, _device.stream()),
+                   "dd_set_layout")
         return self.layout
 
     # ---------------------------------------------------------------- exchanges
@@ -236,6 +261,15 @@ class SlabDecomposition:
     def allgather_home(self, ids: torch.Tensor, pos: torch.Tensor, n_total: int) -> torch.Tensor:
         """Global (n_total, 3) positions from every rank's home rows."""
         ids = torch.as_tensor(ids, device=pos.device)
+        if self._native is not None and pos.is_cuda and getattr(self, "home_counts", None) is not None:
+            from . import _device, _lib
+
+            cap = int(self.home_counts.max())
+            out = torch.empty((n_total, 3), dtype=torch.float64, device=pos.device)
+            _lib.check(_lib.load().nbx_dd_allgather_home(self._native, _lib.ptr(ids.contiguous()),
+                                                         _lib.ptr(pos.contiguous()), int(ids.shape[0]), cap,
+                                                         _lib.ptr(out), _device.stream()), "dd_allgather")
+            return out
         if self.N == 1:
             out = torch.empty((n_total, 3), dtype=pos.dtype, device=pos.device)
             out[ids] = pos
