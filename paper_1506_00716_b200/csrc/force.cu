@@ -175,33 +175,58 @@ struct Entry {
   uint32_t w[2 * W];
 };
 
-template <int M, int W>
-__device__ __forceinline__ void load_entry(const ForceArgs& A, int32_t e, bool valid, int b, Entry<W>& E) {
-  if (valid) {
-    E.cj = __ldg(A.ent_j + e);
-    E.d = __ldg(A.ent_delta + e);
+// Entry / j-atom staging through shared memory with cp.async: each lane
+// copies its own entry fields (2 iterations ahead) and its j-atom (1 ahead)
+// into per-lane ring slots, so no register ever waits on an in-flight global
+// load (a register-rotation prefetch stalls on the rotation moves).
+// Out-of-range slots copy the group's last entry (a valid address) and are
+// disabled when used.
+template <int W>
+struct Stage {
+  float4 ed[3][32];
+  uint64_t em[3][W][32];
+  int32_t cj[3][32];
+  float4 xj[2][32];
+  int32_t tj[2][32];
+};
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+  else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int W>
+__device__ __forceinline__ void stage_entry(const ForceArgs& A, Stage<W>& S, int slot, int lane, int32_t e,
+                                            int32_t e_last) {
+  const int32_t i = e < e_last ? e : e_last;
+  cp_async(&S.ed[slot][lane], A.ent_delta + i, 16);
 #pragma unroll
-    for (int q = 0; q < W; ++q) {
-      const uint64_t mw = __ldg(A.ent_mask + (int64_t)e * W + q) >> b;
-      E.w[2 * q] = (uint32_t)mw;
-      E.w[2 * q + 1] = (uint32_t)(mw >> 32);
-    }
-  } else {
-    E.cj = 0;
-    E.d = make_float4(0.f, 0.f, 0.f, 3.0e38f);
-#pragma unroll
-    for (int q = 0; q < 2 * W; ++q) E.w[q] = 0u;
-  }
+  for (int q = 0; q < W; ++q) cp_async(&S.em[slot][q][lane], A.ent_mask + (int64_t)i * W + q, 8);
+  cp_async(&S.cj[slot][lane], A.ent_j + i, 4);
 }
 
-template <int M>
-__device__ __forceinline__ void load_jatom(const ForceArgs& A, int32_t cj, int b, const float4& d, float4& xj,
-                                           int& tj) {
-  xj = __ldg(A.xyzq + (int64_t)cj * M + b);
-  tj = __ldg(A.type + (int64_t)cj * M + b);
-  xj.x += d.x;
-  xj.y += d.y;
-  xj.z += d.z;
+template <int M, int W>
+__device__ __forceinline__ void stage_jatom(const ForceArgs& A, Stage<W>& S, int xslot, int lane, int32_t cj,
+                                            int b) {
+  cp_async(&S.xj[xslot][lane], A.xyzq + (int64_t)cj * M + b, 16);
+  cp_async(&S.tj[xslot][lane], A.type + (int64_t)cj * M + b, 4);
+}
+
+template <int W>
+__device__ __forceinline__ void read_entry(const Stage<W>& S, int slot, int lane, bool valid, int b, Entry<W>& E) {
+  E.cj = S.cj[slot][lane];
+  E.d = S.ed[slot][lane];
+  if (!valid) E.d.w = 3.0e38f;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const uint64_t mw = valid ? (S.em[slot][q][lane] >> b) : 0ull;
+    E.w[2 * q] = (uint32_t)mw;
+    E.w[2 * q + 1] = (uint32_t)(mw >> 32);
+  }
 }
 
 template <int M, int W>
@@ -243,6 +268,98 @@ __device__ __forceinline__ void sweep(const ForceArgs& A, const float4* __restri
       fjy = fmaf(-fscal, dy, fjy);
       fjz = fmaf(-fscal, dz, fjz);
     }
+  }
+}
+
+// The same iteration on PAIRS of i-atoms (2h, 2h+1) with Blackwell's packed
+// FP32 instructions (FFMA2 / FMUL2 / FADD2: two lanes' worth of FP32 work per
+// issue slot, j-atom operands broadcast from one register).  The FP32 pipe
+// work is unchanged but the issue slots it needs halve, which is what bounds
+// the scalar sweep (ncu: issue ~73 % busy, FMA pipe ~50 %).  i-atom data are
+// pair-interleaved in shared memory: s_xy[h] = {x0, x1, y0, y1},
+// s_zq[h] = {z0, z1, q0, q1}, s_l2[h] = {-6c6_0, -6c6_1, 12c12_0, 12c12_1}
+// (for this lane's j-type), s_sh[h] = {shift_0, shift_1}.
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
+template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND, bool MI, int W>
+__device__ __forceinline__ void sweep2(const ForceArgs& A, const float4* __restrict__ s_xy,
+                                       const float4* __restrict__ s_zq, const float4* __restrict__ s_l2,
+                                       const float2* __restrict__ s_sh, const Entry<W>& E, unsigned wpres,
+                                       const float4& xj, float2 (&fi)[G * M / 2][3], float2& fjx, float2& fjy,
+                                       float2& fjz, float2& elj, float2& ec, uint32_t& near) {
+  constexpr int IA = G * M, H = IA / 2, MM = M * M;
+  const float2 nx = bc2(-xj.x), ny = bc2(-xj.y), nz = bc2(-xj.z), qj = bc2(xj.w);
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const int ia0 = 2 * h, ia1 = 2 * h + 1;
+    const int k0 = ia0 / M, k1 = ia1 / M;
+    if (!(((wpres >> k0) | (wpres >> k1)) & 1u)) continue;
+    const float4 xy = s_xy[h], zq = s_zq[h], l2 = s_l2[h];
+    float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nx);
+    float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), ny);
+    float2 dz = __fadd2_rn(make_float2(zq.x, zq.y), nz);
+    if (MI) {
+      dx.x = fmaf(-A.L[0], rintf(dx.x * A.invL[0]), dx.x);
+      dx.y = fmaf(-A.L[0], rintf(dx.y * A.invL[0]), dx.y);
+      dy.x = fmaf(-A.L[1], rintf(dy.x * A.invL[1]), dy.x);
+      dy.y = fmaf(-A.L[1], rintf(dy.y * A.invL[1]), dy.y);
+      dz.x = fmaf(-A.L[2], rintf(dz.x * A.invL[2]), dz.x);
+      dz.y = fmaf(-A.L[2], rintf(dz.y * A.invL[2]), dz.y);
+    }
+    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+    const int p0 = (W == 2 ? k0 * 64 : k0 * MM) + (ia0 % M) * M;
+    const int p1 = (W == 2 ? k1 * 64 : k1 * MM) + (ia1 % M) * M;
+    const bool adm0 = entry_bit<M, W>(E, p0), adm1 = entry_bit<M, W>(E, p1);
+    const bool inc0 = adm0 && (r2.x <= A.rc2), inc1 = adm1 && (r2.y <= A.rc2);
+    if (BAND) {
+      near |= (adm0 && fabsf(r2.x - A.rc2) < A.band) ? (1u << ia0) : 0u;
+      near |= (adm1 && fabsf(r2.y - A.rc2) < A.band) ? (1u << ia1) : 0u;
+    }
+    float2 rinv = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+    rinv.x = inc0 ? rinv.x : 0.f;
+    rinv.y = inc1 ? rinv.y : 0.f;
+    const float2 rinv2 = __fmul2_rn(rinv, rinv);
+    const float2 rinv6 = __fmul2_rn(__fmul2_rn(rinv2, rinv2), rinv2);
+    const float2 c6n = make_float2(l2.x, l2.y), c12 = make_float2(l2.z, l2.w);
+    const float2 flj = __fmul2_rn(rinv6, __ffma2_rn(c12, rinv6, c6n));  // 12 c12/r^12 - 6 c6/r^6
+    const float2 qq = __fmul2_rn(make_float2(zq.z, zq.w), qj);
+    float2 fscal;
+    if (ELEC == FE_RF) {
+      fscal = __fmul2_rn(__ffma2_rn(qq, rinv, flj), rinv2);
+      if (KRF || ENERGY) {
+        const float2 qm = make_float2(inc0 ? qq.x : 0.f, inc1 ? qq.y : 0.f);
+        if (KRF) fscal = __ffma2_rn(qm, bc2(-A.k2rf), fscal);
+        if (ENERGY)
+          ec = __fadd2_rn(ec, __ffma2_rn(qm, __ffma2_rn(bc2(A.krf), r2, bc2(-A.crf)), __fmul2_rn(qq, rinv)));
+      }
+    } else {
+      const float2 qm = make_float2(inc0 ? qq.x : 0.f, inc1 ? qq.y : 0.f);
+      const float2 u = __ffma2_rn(r2, bc2(A.ew_a), bc2(-1.f));
+      float2 gf = bc2(A.ew_f[0]);
+#pragma unroll
+      for (int k = 1; k <= EW_DEG_F; ++k) gf = __ffma2_rn(gf, u, bc2(A.ew_f[k]));
+      const float2 t = __ffma2_rn(bc2(-A.beta3), gf, __fmul2_rn(rinv, rinv2));
+      fscal = __ffma2_rn(qm, t, __fmul2_rn(flj, rinv2));
+      if (ENERGY) {
+        float2 gv = bc2(A.ew_v[0]);
+#pragma unroll
+        for (int k = 1; k <= EW_DEG_V; ++k) gv = __ffma2_rn(gv, u, bc2(A.ew_v[k]));
+        ec = __ffma2_rn(qm, __fadd2_rn(rinv, __ffma2_rn(bc2(-A.beta), gv, bc2(-A.ew_shift))), ec);
+      }
+    }
+    if (ENERGY) {
+      const float2 sh = s_sh[h];
+      const float2 shm = make_float2(inc0 ? -sh.x : 0.f, inc1 ? -sh.y : 0.f);
+      const float2 e6 = __fmul2_rn(rinv6, __ffma2_rn(__fmul2_rn(c12, bc2(1.f / 12.f)), rinv6,
+                                                     __fmul2_rn(c6n, bc2(1.f / 6.f))));
+      elj = __fadd2_rn(elj, __fadd2_rn(e6, shm));
+    }
+    fi[h][0] = __ffma2_rn(fscal, dx, fi[h][0]);
+    fi[h][1] = __ffma2_rn(fscal, dy, fi[h][1]);
+    fi[h][2] = __ffma2_rn(fscal, dz, fi[h][2]);
+    fjx = __ffma2_rn(fscal, dx, fjx);  // j-side sign applied once per iteration
+    fjy = __ffma2_rn(fscal, dy, fjy);
+    fjz = __ffma2_rn(fscal, dz, fjz);
   }
 }
 
@@ -291,8 +408,16 @@ k_force(const ForceArgs A) {
   constexpr int IA = G * M;   // i-atoms per group
   constexpr int W = (G * M * M > 64) ? 2 : 1;
   constexpr int MM = M * M;
-  extern __shared__ float4 s_dyn[];  // [FW][nt][IA] LJ params per (j-type, i-atom)
+  constexpr bool PK = (IA % 2) == 0;  // packed FP32x2 sweep over i-atom pairs
+  constexpr int H = PK ? IA / 2 : 1;
+  // dynamic: [FW][nt][IA] float4 LJ per (j-type, i-atom) (scalar sweep and
+  // band fixes), then [FW][nt][H] float4 pair-interleaved LJ, [FW][nt][H]
+  // float2 pair-interleaved shifts
+  extern __shared__ float4 s_dyn[];
   __shared__ float4 s_xi[FW][IA];
+  __shared__ float4 s_xy[FW][H];
+  __shared__ float4 s_zq[FW][H];
+  __shared__ Stage<W> s_stage[FW];
   __shared__ float s_red[FW][32][IA * 3 + 1];
   __shared__ float s_corr[FW][IA * 3];
 
@@ -310,14 +435,21 @@ k_force(const ForceArgs A) {
   const int nmem = A.grp_nmem ? A.grp_nmem[g] : 1;
   const int32_t e_beg = A.ent_off[g], e_end = A.ent_off[g + 1];
   float4* s_lj = s_dyn + (size_t)w * IA * A.nt;
+  float4* s_l2 = s_dyn + (size_t)FW * IA * A.nt + (size_t)w * H * A.nt;
+  float2* s_sh = reinterpret_cast<float2*>(s_dyn + (size_t)FW * (IA + H) * A.nt) + (size_t)w * H * A.nt;
 
-  // software pipeline: entry data two iterations ahead, j-atom one ahead
-  Entry<W> cur, nxt;
-  float4 xj;
-  int tj;
-  load_entry<M, W>(A, e_beg + r, e_beg + r < e_end, b, cur);
-  load_entry<M, W>(A, e_beg + R + r, e_beg + R + r < e_end, b, nxt);
-  load_jatom<M>(A, cur.cj, b, cur.d, xj, tj);
+  // software pipeline (cp.async into per-lane smem slots): entry data two
+  // iterations ahead, j-atom one ahead
+  const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
+  Stage<W>& S = s_stage[w];
+  if (e_end > e_beg) {
+    stage_entry<W>(A, S, 0, lane, e_beg + r, e_last);
+    stage_entry<W>(A, S, 1, lane, e_beg + R + r, e_last);
+    cp_async_commit();
+    cp_async_wait_all();
+    stage_jatom<M, W>(A, S, 0, lane, S.cj[0][lane], b);
+    cp_async_commit();
+  }
 
   // stage the group's i-atoms (group frame) and their LJ parameters per j-type
   for (int ia = lane; ia < IA; ia += 32) {
@@ -331,32 +463,68 @@ k_force(const ForceArgs A) {
       v.w *= A.coul;
     }
     s_xi[w][ia] = v;
+    if (PK) {
+      float* xyf = reinterpret_cast<float*>(&s_xy[w][0]);
+      float* zqf = reinterpret_cast<float*>(&s_zq[w][0]);
+      const int h = ia >> 1, o = ia & 1;
+      xyf[4 * h + o] = v.x;
+      xyf[4 * h + 2 + o] = v.y;
+      zqf[4 * h + o] = v.z;
+      zqf[4 * h + 2 + o] = v.w;
+    }
   }
-  for (int idx = lane; idx < IA * A.nt; idx += 32) {
-    const int t = idx / IA, ia = idx - t * IA;
-    const int ti = ia < nmem * M ? A.type[(int64_t)first * M + ia] : 0;
-    s_lj[idx] = __ldg(&A.lj[ti * A.nt + t]);
-  }
+  if (!PK || BAND)
+    for (int idx = lane; idx < IA * A.nt; idx += 32) {
+      const int t = idx / IA, ia = idx - t * IA;
+      const int ti = ia < nmem * M ? A.type[(int64_t)first * M + ia] : 0;
+      s_lj[idx] = __ldg(&A.lj[ti * A.nt + t]);
+    }
+  if (PK)
+    for (int idx = lane; idx < H * A.nt; idx += 32) {
+      const int t = idx / H, h = idx - t * H;
+      const int ti0 = 2 * h < nmem * M ? A.type[(int64_t)first * M + 2 * h] : 0;
+      const int ti1 = 2 * h + 1 < nmem * M ? A.type[(int64_t)first * M + 2 * h + 1] : 0;
+      const float4 a0 = __ldg(&A.lj[ti0 * A.nt + t]), a1 = __ldg(&A.lj[ti1 * A.nt + t]);
+      s_l2[idx] = make_float4(-a0.x, -a1.x, a0.y, a1.y);
+      s_sh[idx] = make_float2(a0.z, a1.z);
+    }
   if (BAND)
     for (int c = lane; c < IA * 3; c += 32) s_corr[w][c] = 0.f;
   __syncwarp();
 
   const float slack_thr = A.slack_base + 4.f * __uint_as_float(A.scalars[0]);
-  float fi[IA][3];
+  float fi[PK ? 1 : IA][3];
+  float2 fi2[H][3];
+  if constexpr (PK) {
 #pragma unroll
-  for (int ia = 0; ia < IA; ++ia) fi[ia][0] = fi[ia][1] = fi[ia][2] = 0.f;
+    for (int h = 0; h < H; ++h) fi2[h][0] = fi2[h][1] = fi2[h][2] = make_float2(0.f, 0.f);
+  } else {
+#pragma unroll
+    for (int ia = 0; ia < IA; ++ia) fi[ia][0] = fi[ia][1] = fi[ia][2] = 0.f;
+  }
   double elj_acc = 0.0, ec_acc = 0.0;
   constexpr uint64_t colmask = column_bits<M>();
 
+  int es = 0, xs = 0;
   for (int32_t e0 = e_beg; e0 < e_end; e0 += R) {
     const int32_t e = e0 + r;
     const bool valid = e < e_end;
-    // prefetch: entry data for e0 + 2R, j-atom for e0 + R
-    Entry<W> nx2;
-    load_entry<M, W>(A, e + 2 * R, e + 2 * R < e_end, b, nx2);
-    float4 xj_n;
-    int tj_n;
-    load_jatom<M>(A, nxt.cj, b, nxt.d, xj_n, tj_n);
+    // this iteration's entry (slot es) and j-atom (slot xs) have landed;
+    // stage the j-atom of the next iteration and the entry two ahead
+    cp_async_wait_all();
+    Entry<W> cur;
+    read_entry<W>(S, es, lane, valid, b, cur);
+    const float4 xr = S.xj[xs][lane];
+    const int tj = S.tj[xs][lane];
+    {
+      const int es1 = es == 2 ? 0 : es + 1, es2 = es1 == 2 ? 0 : es1 + 1;
+      stage_jatom<M, W>(A, S, xs ^ 1, lane, S.cj[es1][lane], b);
+      stage_entry<W>(A, S, es2, lane, e + 2 * R, e_last);
+      cp_async_commit();
+      es = es1;
+      xs ^= 1;
+    }
+    const float4 xj = make_float4(xr.x + cur.d.x, xr.y + cur.d.y, xr.z + cur.d.z, xr.w);
 
     unsigned pres = 0;
 #pragma unroll
@@ -372,10 +540,29 @@ k_force(const ForceArgs A) {
     float fjx = 0.f, fjy = 0.f, fjz = 0.f;
     float elj = 0.f, ec = 0.f;
     uint32_t near = 0;
-    if (!wunsafe)
-      sweep<M, G, ELEC, KRF, ENERGY, BAND, false, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
-    else
-      sweep<M, G, ELEC, KRF, ENERGY, BAND, true, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+    if constexpr (PK) {
+      const float4* s_l2t = s_l2 + tj * H;
+      const float2* s_sht = s_sh + tj * H;
+      float2 gx = make_float2(0.f, 0.f), gy = gx, gz = gx, el2 = gx, ec2 = gx;
+      if (!wunsafe)
+        sweep2<M, G, ELEC, KRF, ENERGY, BAND, false, W>(A, s_xy[w], s_zq[w], s_l2t, s_sht, cur, wpres, xj, fi2, gx,
+                                                        gy, gz, el2, ec2, near);
+      else
+        sweep2<M, G, ELEC, KRF, ENERGY, BAND, true, W>(A, s_xy[w], s_zq[w], s_l2t, s_sht, cur, wpres, xj, fi2, gx,
+                                                       gy, gz, el2, ec2, near);
+      fjx = -(gx.x + gx.y);
+      fjy = -(gy.x + gy.y);
+      fjz = -(gz.x + gz.y);
+      if (ENERGY) {
+        elj = el2.x + el2.y;
+        ec = ec2.x + ec2.y;
+      }
+    } else {
+      if (!wunsafe)
+        sweep<M, G, ELEC, KRF, ENERGY, BAND, false, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+      else
+        sweep<M, G, ELEC, KRF, ENERGY, BAND, true, W>(A, s_xi[w], s_ljt, cur, wpres, xj, fi, fjx, fjy, fjz, elj, ec, near);
+    }
     if (BAND && __any_sync(0xffffffffu, near != 0)) {
       if (near) {
         if (!wunsafe)
@@ -390,18 +577,26 @@ k_force(const ForceArgs A) {
       elj_acc += (double)elj;
       ec_acc += (double)ec;
     }
-    cur = nxt;
-    nxt = nx2;
-    xj = xj_n;
-    tj = tj_n;
   }
 
+  cp_async_wait_all();  // nothing in flight into the slots the next group reuses
+
   // i-force transpose-reduce through shared memory
+  if constexpr (PK) {
 #pragma unroll
-  for (int ia = 0; ia < IA; ++ia) {
-    s_red[w][lane][3 * ia + 0] = fi[ia][0];
-    s_red[w][lane][3 * ia + 1] = fi[ia][1];
-    s_red[w][lane][3 * ia + 2] = fi[ia][2];
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s_red[w][lane][3 * (2 * h) + c] = fi2[h][c].x;
+        s_red[w][lane][3 * (2 * h + 1) + c] = fi2[h][c].y;
+      }
+  } else {
+#pragma unroll
+    for (int ia = 0; ia < IA; ++ia) {
+      s_red[w][lane][3 * ia + 0] = fi[ia][0];
+      s_red[w][lane][3 * ia + 1] = fi[ia][1];
+      s_red[w][lane][3 * ia + 2] = fi[ia][2];
+    }
   }
   __syncwarp();
   for (int c = lane; c < IA * 3; c += 32) {
@@ -571,11 +766,14 @@ __global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, i
 template <int M, int G, int ELEC, bool KRF, bool ENERGY, bool BAND>
 static cudaError_t launch_one(const ForceArgs& A, cudaStream_t s) {
   constexpr int IA = G * M;
-  const size_t dyn = sizeof(float4) * (size_t)FW * IA * A.nt;
+  constexpr int H = (IA % 2) == 0 ? IA / 2 : 1;
+  const size_t dyn = (sizeof(float4) * (size_t)(IA + H) + sizeof(float2) * (size_t)H) * FW * A.nt;
   auto kern = k_force<M, G, ELEC, KRF, ENERGY, BAND>;
-  if (dyn > 32 * 1024) {
+  static size_t dyn_set = 0;  // static + dynamic may exceed the default 48 KB
+  if (dyn > dyn_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
+    dyn_set = dyn;
   }
   // persistent grid: as many blocks as fit on the GPU at once
   static int max_blocks = 0;
