@@ -109,7 +109,10 @@ __host__ __device__ constexpr uint64_t column_bits() {
 // with rinv, so they are masked through qm = inc ? qq : 0.
 // degree 10 for the force term (force rel-RMS ~5e-6 vs FP64 on SPC water,
 // tolerance 1e-4), 12 for the energy term (~2e-8, tolerance 1e-5)
-constexpr int EW_DEG_F = 10;
+#ifndef NBX_EW_DEG_F
+#define NBX_EW_DEG_F 10
+#endif
+constexpr int EW_DEG_F = NBX_EW_DEG_F;
 constexpr int EW_DEG_V = 12;
 
 // One pair: F/r, plus energies when requested.  `inc` zeroes rinv, which
@@ -289,11 +292,18 @@ __device__ __forceinline__ void sweep2(const ForceArgs& A, const float4* __restr
                                        float2& fjz, float2& elj, float2& ec, uint32_t& near) {
   constexpr int IA = G * M, H = IA / 2, MM = M * M;
   const float2 nx = bc2(-xj.x), ny = bc2(-xj.y), nz = bc2(-xj.z), qj = bc2(xj.w);
+  // one warp-uniform branch per member (per pair of members when m = 1), so
+  // the member's pair-pairs share a basic block and their dependency chains
+  // interleave
+  constexpr int HB = M >= 2 ? M / 2 : 1;  // pair-pairs per branch
 #pragma unroll
-  for (int h = 0; h < H; ++h) {
+  for (int hb = 0; hb < H; hb += HB) {
+    const int kb0 = (2 * hb) / M, kb1 = (2 * hb + 2 * HB - 1) / M;
+    if (!(((wpres >> kb0) | (wpres >> kb1)) & 1u)) continue;
+#pragma unroll
+  for (int h = hb; h < hb + HB; ++h) {
     const int ia0 = 2 * h, ia1 = 2 * h + 1;
     const int k0 = ia0 / M, k1 = ia1 / M;
-    if (!(((wpres >> k0) | (wpres >> k1)) & 1u)) continue;
     const float4 xy = s_xy[h], zq = s_zq[h], l2 = s_l2[h];
     float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nx);
     float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), ny);
@@ -361,6 +371,7 @@ __device__ __forceinline__ void sweep2(const ForceArgs& A, const float4* __restr
     fjy = __ffma2_rn(fscal, dy, fjy);
     fjz = __ffma2_rn(fscal, dz, fjz);
   }
+  }
 }
 
 // Rare path: pairs whose FP32 r^2 fell within `band` of r_c^2 get the exact
@@ -417,8 +428,13 @@ k_force(const ForceArgs A) {
   __shared__ float4 s_xi[FW][IA];
   __shared__ float4 s_xy[FW][H];
   __shared__ float4 s_zq[FW][H];
-  __shared__ Stage<W> s_stage[FW];
-  __shared__ float s_red[FW][32][IA * 3 + 1];
+  // per-warp scratch: the staging ring during the entry loop, the i-force
+  // transpose buffer after it
+  union Scratch {
+    Stage<W> st;
+    float red[32][IA * 3 + 1];
+  };
+  __shared__ Scratch s_ws[FW];
   __shared__ float s_corr[FW][IA * 3];
 
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -441,7 +457,7 @@ k_force(const ForceArgs A) {
   // software pipeline (cp.async into per-lane smem slots): entry data two
   // iterations ahead, j-atom one ahead
   const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
-  Stage<W>& S = s_stage[w];
+  Stage<W>& S = s_ws[w].st;
   if (e_end > e_beg) {
     stage_entry<W>(A, S, 0, lane, e_beg + r, e_last);
     stage_entry<W>(A, S, 1, lane, e_beg + R + r, e_last);
@@ -580,6 +596,7 @@ k_force(const ForceArgs A) {
   }
 
   cp_async_wait_all();  // nothing in flight into the slots the next group reuses
+  __syncwarp();         // ... and every lane's copies landed before the scratch is reused
 
   // i-force transpose-reduce through shared memory
   if constexpr (PK) {
@@ -587,28 +604,28 @@ k_force(const ForceArgs A) {
     for (int h = 0; h < H; ++h)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        s_red[w][lane][3 * (2 * h) + c] = fi2[h][c].x;
-        s_red[w][lane][3 * (2 * h + 1) + c] = fi2[h][c].y;
+        s_ws[w].red[lane][3 * (2 * h) + c] = fi2[h][c].x;
+        s_ws[w].red[lane][3 * (2 * h + 1) + c] = fi2[h][c].y;
       }
   } else {
 #pragma unroll
     for (int ia = 0; ia < IA; ++ia) {
-      s_red[w][lane][3 * ia + 0] = fi[ia][0];
-      s_red[w][lane][3 * ia + 1] = fi[ia][1];
-      s_red[w][lane][3 * ia + 2] = fi[ia][2];
+      s_ws[w].red[lane][3 * ia + 0] = fi[ia][0];
+      s_ws[w].red[lane][3 * ia + 1] = fi[ia][1];
+      s_ws[w].red[lane][3 * ia + 2] = fi[ia][2];
     }
   }
   __syncwarp();
   for (int c = lane; c < IA * 3; c += 32) {
     float sacc = BAND ? s_corr[w][c] : 0.f;
 #pragma unroll 8
-    for (int l = 0; l < 32; ++l) sacc += s_red[w][l][c];
-    s_red[w][0][c] = sacc;  // column c is read and written by this lane only
+    for (int l = 0; l < 32; ++l) sacc += s_ws[w].red[l][c];
+    s_ws[w].red[0][c] = sacc;  // column c is read and written by this lane only
   }
   __syncwarp();
   if (lane < nmem * M) {
     A.part_i[(int64_t)first * M + lane] =
-        make_float4(s_red[w][0][3 * lane], s_red[w][0][3 * lane + 1], s_red[w][0][3 * lane + 2], 0.f);
+        make_float4(s_ws[w].red[0][3 * lane], s_ws[w].red[0][3 * lane + 1], s_ws[w].red[0][3 * lane + 2], 0.f);
   }
   if (ENERGY) {
     for (int o = 16; o; o >>= 1) {

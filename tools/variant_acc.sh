@@ -1,1 +1,5 @@
-for f in tools/variants/*.so; do cp $f paper_1506_00716_b200/libnbx.so; echo $f; python tools/ewald_accuracy.py 24000; python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/var.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/var.json')); print('k_force', round(d['roofline']['kernel_ms']*1e3,1), 'us frac', round(d['roofline']['frac'],4))"; done
+# Ewald accuracy of each library variant in tools/variants/
+for f in tools/variants/*.so; do
+  cp $f paper_1506_00716_b200/libnbx.so
+  echo "$f: $(python tools/ewald_accuracy.py 2>&1 | grep ewald)"
+done
