@@ -117,8 +117,13 @@ int nbx_pairlist_build_pruned(const nbx_grid_t* grid, const double box[3], doubl
 int nbx_pairlist_prune(const nbx_list_t* list, const nbx_grid_t* grid,
                        const double* clustered_positions, const double box[3], void* stream,
                        nbx_list_t** out);
-/* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; syncs */
+/* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; n_rows is -1 until
+ * the canonical rows are materialised (lists hold the grouped entries; the
+ * canonical CSR is derived from them on first use) */
 int nbx_list_info(const nbx_list_t* list, int64_t out[5]);
+/* materialise the canonical CSR rows (pairlist.ClusterPairList offsets /
+ * j_idx / masks) if needed and return their count; syncs */
+int nbx_list_rows(nbx_list_t* list, void* stream, int64_t* n_rows);
 /* host outputs (any may be NULL): offsets (n_i_clusters+1), j_idx (n_rows),
  * masks (n_rows, bit a*m+b of uint64); syncs */
 int nbx_list_download(const nbx_list_t* list, int64_t* offsets, int64_t* j_idx, uint64_t* masks,

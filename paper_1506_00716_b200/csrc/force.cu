@@ -967,6 +967,12 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
   const int m = l->m;
   const int64_t ns = l->n_clusters * m;
   const bool canonical = (i_sel != nullptr) || (flags & NBX_FORCE_CANONICAL);
+  if (canonical) {
+    if (cudaError_t e0 = ensure_rows(l, to_stream(stream))) {
+      set_error("nbx_force: %s", cudaGetErrorString(e0));
+      return NBX_ERR_CUDA;
+    }
+  }
   const int64_t n_items = canonical ? l->n_rows : l->n_entries;
   const int64_t n_work = canonical ? (i_sel ? n_sel : l->n_clusters) : l->n_groups;
   Box bx;
@@ -1146,6 +1152,7 @@ extern "C" int nbx_find_singular(const nbx_list_t* l, const nbx_grid_t* grid, co
     A.box.L[d] = box[d];
     A.box.invL[d] = 1.0 / box[d];
   }
+  if ((e = ensure_rows(const_cast<nbx_list*>(static_cast<const nbx_list*>(l)), s))) goto fail;
   if ((e = sc.alloc(4, s))) goto fail;
   if ((e = cudaMemcpyAsync(sc.p, h, 16, cudaMemcpyHostToDevice, s))) goto fail;
   A.scalars = sc.p;

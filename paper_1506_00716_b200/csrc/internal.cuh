@@ -95,13 +95,14 @@ struct List {
   double r_list = 0.0;
   double L[3] = {0, 0, 0};
   const double* bbox = nullptr;  // the grid's boxes (frame of `delta`); the grid outlives its lists
-  // canonical CSR
+  // canonical CSR: materialised from the entries on demand (ensure_rows);
+  // the force path never needs it
+  bool rows_ready = false;
   DBuf<int32_t> offsets;    // (n_clusters + 1)
   DBuf<int32_t> j;          // (n_rows)
   DBuf<uint64_t> mask;      // (n_rows)
   DBuf<float4> delta;       // (n_rows) j-local -> i-local offset (image included), lazy
   bool delta_ready = false;
-  DBuf<int32_t> row_entry;  // (n_rows) entry holding this row
   // groups / entries
   DBuf<int32_t> group_first;  // (n_groups) first member cluster
   DBuf<int32_t> group_nmem;   // (n_groups)
@@ -110,6 +111,11 @@ struct List {
   DBuf<int32_t> ent_j;        // (n_entries)
   DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset, w = slack
   DBuf<uint64_t> ent_mask;    // (n_entries * W), W = 2 for m == 8 else 1
+  DBuf<uint16_t> ent_pres;    // (n_entries) members holding a (canonical) row with this j-cluster
+  // entries are stored in force order (member pattern) once ordered; the
+  // t-th entry of a group in ascending-j order is ent_jorder[t] (empty: identity)
+  DBuf<int32_t> ent_jorder;
+  bool entries_ordered = false;
   // reference super layout (on demand)
   int64_t super_size = 0, super_groups = 0, super_entries = 0;
   DBuf<int32_t> super_offsets, super_j, super_pair;
@@ -129,6 +135,7 @@ void timing_record(cudaEvent_t a, cudaEvent_t b);
 struct List;
 cudaError_t finalize_force_layout(List* l, cudaStream_t s);
 cudaError_t ensure_row_delta(List* l, cudaStream_t s);
+cudaError_t ensure_rows(List* l, cudaStream_t s);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

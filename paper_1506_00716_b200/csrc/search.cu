@@ -100,18 +100,14 @@ struct SearchOut {
   const float4* xl = nullptr;     // cluster-local FP32 coordinates (bbox-corner frames)
   const double* ppos = nullptr;   // clustered FP64 positions (exact fallback)
   // pass 1
-  int32_t* row_count;   // (n_clusters)
   int32_t* ent_count;   // (n_groups)
   int2* stash;          // (n_groups * STASH) {cj, member bits}
   // pass 2
-  const int32_t* offsets;
   const int32_t* ent_offsets;
-  int32_t* j;
-  uint64_t* mask;
-  int32_t* row_entry;
   int32_t* ent_j;
   float4* ent_delta;
   uint64_t* ent_mask;
+  uint16_t* ent_pres;
 };
 
 // FP32 periodic gap of one dimension (same formula as gap_1d)
@@ -175,38 +171,26 @@ __device__ __forceinline__ uint64_t halo_pair_mask(uint32_t hi, uint32_t hj, int
 }
 
 __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx& C, const double (*s_bb)[6],
-                                           const double* gb, int32_t cj, uint32_t bits, int lane,
-                                           int32_t& cnt, int32_t& ecnt, int32_t row_base, int32_t ent_base,
-                                           int m, const int8_t* nreal, const Box& box,
+                                           const double* gb, int32_t cj, uint32_t bits, int lane, int32_t& ecnt,
+                                           int32_t ent_base, int m, const int8_t* nreal, const Box& box,
                                            const uint8_t* __restrict__ halo) {
   const unsigned lt = (1u << lane) - 1u;
   const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
   if (!eb) return;
-  const int ent_pos = ent_base + ecnt + __popc(eb & lt);
-  const int W = (m == 8) ? 2 : 1;
-  uint64_t emask[2] = {0ull, 0ull};
-  double bj[6];
-  if (bits)
+  if (bits) {
+    const int ent_pos = ent_base + ecnt + __popc(eb & lt);
+    const int W = (m == 8) ? 2 : 1;
+    uint64_t emask[2] = {0ull, 0ull};
+    double bj[6];
     for (int d = 0; d < 6; ++d) bj[d] = C.bbox[6 * (int64_t)cj + d];
-  for (int k = 0; k < C.nmem; ++k) {
-    const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
-    if (!b) continue;
-    const int32_t before = __shfl_sync(0xffffffffu, cnt, k);
-    const int32_t rbase = __shfl_sync(0xffffffffu, row_base, k);
-    if ((bits >> k) & 1u) {
+    for (int k = 0; k < C.nmem; ++k) {
+      if (!((bits >> k) & 1u)) continue;
       const int32_t ci = C.first + k;
-      const int64_t row = (int64_t)rbase + before + __popc(b & lt);
       uint64_t mk = row_mask(m, nreal[ci], nreal[cj], ci == cj);
       if (halo) mk &= ~halo_pair_mask(halo[ci], halo[cj], m);
-      out.j[row] = cj;
-      out.mask[row] = mk;
-      out.row_entry[row] = ent_pos;
       if (W == 2) emask[k] = mk;
       else emask[0] |= mk << (k * m * m);
     }
-    if (lane == k) cnt += __popc(b);
-  }
-  if (bits) {
     float4 e_delta;
     float e_slack;
     image_delta(gb, s_bb[0], bj, box, &e_delta, &e_slack);
@@ -214,6 +198,7 @@ __device__ __forceinline__ void emit_batch(const SearchOut& out, const SearchCtx
     out.ent_delta[ent_pos] = e_delta;
     out.ent_mask[(int64_t)ent_pos * W] = emask[0];
     if (W == 2) out.ent_mask[(int64_t)ent_pos * W + 1] = emask[1];
+    out.ent_pres[ent_pos] = (uint16_t)bits;
   }
   ecnt += __popc(eb);
 }
@@ -326,17 +311,16 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
       gb[3 + d] = fmax(gb[3 + d], s_bb[w][k][3 + d]);
     }
   }
-  int32_t cnt = 0, ecnt = 0, row_base = 0, ent_base = 0;
+  int32_t ecnt = 0, ent_base = 0;
   int2* stash = out.stash + g * (int64_t)STASH;
   if (MODE == 1) {
-    if (lane < C.nmem) row_base = out.offsets[C.first + lane];
     ent_base = out.ent_offsets[g];
     const int32_t nst = out.ent_count[g];  // hits of this group (== its entry count)
     if (nst <= STASH) {
       for (int32_t base = 0; base < nst; base += 32) {
         int2 h = make_int2(0, 0);
         if (base + lane < nst) h = stash[base + lane];
-        emit_batch(out, C, s_bb[w], gb, h.x, (uint32_t)h.y, lane, cnt, ecnt, row_base, ent_base, m, nreal, box, halo);
+        emit_batch(out, C, s_bb[w], gb, h.x, (uint32_t)h.y, lane, ecnt, ent_base, m, nreal, box, halo);
       }
       return;
     }
@@ -355,14 +339,10 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
     if (PRUNE) bits = prune_bits(bits, cj, C, s_xi[w], gb, s_bb[w], out, nreal, halo, m, box);
     if (MODE == 0) {
       const unsigned eb = __ballot_sync(0xffffffffu, bits != 0);
-      for (int k = 0; k < C.nmem; ++k) {
-        const unsigned b = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
-        if (lane == k) cnt += __popc(b);
-      }
       if (bits && ecnt + __popc(eb & lt) < STASH) stash[ecnt + __popc(eb & lt)] = make_int2(cj, (int)bits);
       ecnt += __popc(eb);
     } else {
-      emit_batch(out, C, s_bb[w], gb, cj, bits, lane, cnt, ecnt, row_base, ent_base, m, nreal, box, halo);
+      emit_batch(out, C, s_bb[w], gb, cj, bits, lane, ecnt, ent_base, m, nreal, box, halo);
     }
   };
 
@@ -396,10 +376,7 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
     }
   }
   if (qn > 0) process(qn);
-  if (MODE == 0) {
-    if (lane < C.nmem) out.row_count[C.first + lane] = cnt;
-    if (lane == 0) out.ent_count[g] = ecnt;
-  }
+  if (MODE == 0 && lane == 0) out.ent_count[g] = ecnt;
 }
 
 __global__ void k_halo_bits(const uint8_t* __restrict__ halo, const int32_t* __restrict__ perm,
@@ -619,33 +596,37 @@ k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, cons
   }
 }
 
-// Entry-wise prune (pairlist.py:242-282 decisions, bit-identical): one warp
-// per group, lane = (entry slot r of 32/m, j-atom b) as in the force kernel;
-// the group's 16 i-atoms sit in shared memory in the group frame, j-atoms are
-// coalesced float4 loads shifted by the entry's frame offset.  Per entry the
-// result is a G-bit "member kept" word; canonical rows and entry masks follow.
+// Entry-wise prune (pairlist.py:242-282 decisions, bit-identical): one
+// BLOCK per group, its warps striding over the group's entries; lane = (entry
+// slot r of 32/m, j-atom b) as in the force kernel.  The group's 16 i-atoms
+// sit in shared memory in the group frame, j-atoms are coalesced float4 loads
+// shifted by the entry's frame offset.  Per entry the result is a G-bit
+// "member kept" word (diagonal rows always kept); per group the number of
+// surviving entries.
+constexpr int PRUNE_WARPS = 4;
 template <int M, int G>
-__global__ void __launch_bounds__(ROWS_WARPS * 32)
+__global__ void __launch_bounds__(PRUNE_WARPS * 32)
 k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem, int64_t n_groups,
                 const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
                 const float4* __restrict__ ent_delta, const uint64_t* __restrict__ ent_mask,
                 const float4* __restrict__ xl, const double* __restrict__ bbox, const double* __restrict__ pos,
-                Box box, double r2, uint32_t* __restrict__ ent_keep) {
+                Box box, double r2, uint32_t* __restrict__ ent_keep, int32_t* __restrict__ grp_alive) {
   constexpr int R = 32 / M;
   constexpr int IA = G * M;
   constexpr int MM = M * M;
   constexpr int W = (G * M * M > 64) ? 2 : 1;
-  __shared__ float4 s_xi[ROWS_WARPS][IA];
+  __shared__ float4 s_xi[IA];
+  __shared__ int32_t s_cnt[PRUNE_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane / M, b = lane % M;
   const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
   const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
   const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
-  for (int64_t g = blockIdx.x * (int64_t)ROWS_WARPS + w; g < n_groups; g += (int64_t)gridDim.x * ROWS_WARPS) {
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const int32_t first = grp_first[g];
     const int nmem = grp_nmem[g];
-    __syncwarp();
-    for (int ia = lane; ia < IA; ia += 32) {
+    __syncthreads();
+    for (int ia = threadIdx.x; ia < IA; ia += blockDim.x) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (ia < nmem * M) {
         const int64_t c = first + ia / M;
@@ -654,11 +635,12 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
         v.y = (float)((bbox[6 * c + 1] - bbox[6 * (int64_t)first + 1]) + (double)v.y);
         v.z = (float)((bbox[6 * c + 2] - bbox[6 * (int64_t)first + 2]) + (double)v.z);
       }
-      s_xi[w][ia] = v;
+      s_xi[ia] = v;
     }
-    __syncwarp();
+    __syncthreads();
     const int32_t e_beg = ent_off[g], e_end = ent_off[g + 1];
-    for (int32_t e0 = e_beg; e0 < e_end; e0 += R) {
+    int32_t alive = 0;
+    for (int32_t e0 = e_beg + w * R; e0 < e_end; e0 += PRUNE_WARPS * R) {
       const int32_t e = e0 + r;
       const bool valid = e < e_end;
       uint32_t inbits = 0;   // members with a pair within r_list in this lane's column
@@ -684,7 +666,7 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
           for (int a = 0; a < M; ++a) {
             const int p = (W == 2 ? k * 64 : k * MM) + a * M;
             if (!(wd[p >> 5] & (1u << (p & 31)))) continue;
-            const float4 xi = s_xi[w][k * M + a];
+            const float4 xi = s_xi[k * M + a];
             float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
             dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
             dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
@@ -709,42 +691,134 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
         if (cj >= first && cj < first + nmem) inbits |= 1u << (cj - first);  // diagonal rows always survive
         ent_keep[e] = inbits;
       }
+      alive += __popc(__ballot_sync(0xffffffffu, valid && b == 0 && inbits != 0u));
+    }
+    if (lane == 0) s_cnt[w] = alive;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int32_t t = 0;
+      for (int q = 0; q < PRUNE_WARPS; ++q) t += s_cnt[q];
+      grp_alive[g] = t;
     }
   }
 }
 
-// canonical rows from the entries' member bits; entry masks keep only the
-// surviving members
-__global__ void k_rows_from_entries(const int32_t* __restrict__ offsets, const int32_t* __restrict__ row_entry,
-                                    int64_t n_clusters, int G, const int32_t* __restrict__ cell_of_cluster,
-                                    const int32_t* __restrict__ col_first, const uint32_t* __restrict__ ent_keep,
-                                    int32_t* __restrict__ keep) {
-  // one warp per i-cluster, lanes over its rows (coalesced)
-  const int64_t ci = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (ci >= n_clusters) return;
-  const int k = (int)((ci - col_first[cell_of_cluster[ci]]) % G);
-  const int32_t r1 = offsets[ci + 1];
-  for (int32_t row = offsets[ci] + (threadIdx.x & 31); row < r1; row += 32)
-    keep[row] = (__ldg(ent_keep + __ldg(row_entry + row)) >> k) & 1u;
+// ---------------------------------------------------------------- entry order
+// Within each group, entries are stored by member-presence pattern (stable,
+// then by j-cluster) so that the 32/m entries a force-kernel warp handles per
+// iteration share their members: the kernel skips a member only when no entry
+// of the iteration has it, so homogeneous iterations waste no lanes.
+constexpr int SORT_SMEM = 1024;
+constexpr int ORDER_WARPS = 4;
+
+__device__ __forceinline__ uint32_t mask_pattern(const uint64_t* em, int m, int G) {
+  uint32_t pat = 0;
+  const int mm = m * m;
+  for (int k = 0; k < G; ++k) {
+    uint64_t bits;
+    if (m == 8) bits = em[k];
+    else bits = (em[0] >> (k * mm)) & (mm == 64 ? ~0ull : ((1ull << mm) - 1ull));
+    pat |= (bits != 0ull ? 1u : 0u) << k;
+  }
+  return pat;
 }
 
-__global__ void k_entries_keep(const uint32_t* __restrict__ ent_keep, int64_t n_ent, int m, int G,
-                               const uint64_t* __restrict__ emask_in, uint64_t* __restrict__ emask_out,
-                               int32_t* __restrict__ alive) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= n_ent) return;
-  const uint32_t kb = ent_keep[e];
+__device__ __forceinline__ uint64_t keep_mask(uint32_t kb, int m, int G) {
   const int mm = m * m;
-  if (m == 8) {
-    for (int k = 0; k < 2; ++k) emask_out[e * 2 + k] = ((kb >> k) & 1u) ? emask_in[e * 2 + k] : 0ull;
-  } else {
-    uint64_t keepmask = 0;
-    const uint64_t one = (mm == 64) ? ~0ull : ((1ull << mm) - 1ull);
-    for (int k = 0; k < G; ++k)
-      if ((kb >> k) & 1u) keepmask |= one << (k * mm);
-    emask_out[e] = emask_in[e] & keepmask;
+  const uint64_t one = (mm == 64) ? ~0ull : ((1ull << mm) - 1ull);
+  uint64_t km = 0;
+  for (int k = 0; k < G; ++k)
+    if ((kb >> k) & 1u) km |= one << (k * mm);
+  return km;
+}
+
+// Stable order of one group's live entries by key (warp-cooperative, keys in
+// shared memory, key 0xffffffff = dead): returns through `opos` each live
+// entry's position among the live entries.  Iterations = distinct keys.
+__device__ __forceinline__ void warp_order(const uint32_t* s_key, int32_t* s_pos, int n, int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t placed = 0;
+  int64_t prev = -1;
+  for (;;) {
+    uint32_t mn = 0xffffffffu;
+    for (int t = lane; t < n; t += 32) {
+      const uint32_t k = s_key[t];
+      if ((int64_t)k > prev && k < mn) mn = k;
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (mn == 0xffffffffu) break;
+    for (int base = 0; base < n; base += 32) {
+      const int t = base + lane;
+      const bool hit = t < n && s_key[t] == mn;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) s_pos[t] = placed + __popc(bal & lt);
+      placed += __popc(bal);
+    }
+    prev = mn;
   }
-  alive[e] = kb != 0u;
+}
+
+// Pruned list from the keep words: surviving entries of each group written
+// in force order (member pattern of the pruned masks), their masks reduced to
+// the kept members, and the ascending-j index ent_jorder.  One warp per group.
+__global__ void __launch_bounds__(ORDER_WARPS * 32)
+k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int32_t* __restrict__ jorder_in,
+                const uint32_t* __restrict__ ent_keep, const int32_t* __restrict__ ej, const float4* __restrict__ ed, const uint64_t* __restrict__ em,
+                int m, int G, const int32_t* __restrict__ off_out, int32_t* __restrict__ ej2,
+                float4* __restrict__ ed2, uint64_t* __restrict__ em2, uint16_t* __restrict__ ep2,
+                int32_t* __restrict__ jorder2) {
+  __shared__ uint32_t s_key[ORDER_WARPS][SORT_SMEM];
+  __shared__ int32_t s_pos[ORDER_WARPS][SORT_SMEM];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.x * (int64_t)ORDER_WARPS + w;
+  if (g >= n_groups) return;
+  const int W = (m == 8) ? 2 : 1;
+  const unsigned lt = (1u << lane) - 1u;
+  const int32_t e0 = off_in[g], n = off_in[g + 1] - e0, o0 = off_out[g];
+  const bool sorted = n <= SORT_SMEM;  // very long lists (needle clusters): keep j order
+  if (sorted) {
+    for (int t = lane; t < n; t += 32) {
+      const int64_t e = jorder_in ? jorder_in[e0 + t] : e0 + t;  // t-th entry in ascending j
+      const uint32_t kb = ent_keep[e];
+      uint32_t key = 0xffffffffu;
+      if (kb) {
+        uint64_t mk[2];
+        for (int q = 0; q < W; ++q) mk[q] = em[e * W + q];
+        if (W == 2) {
+          for (int q = 0; q < 2; ++q)
+            if (!((kb >> q) & 1u)) mk[q] = 0ull;
+        } else {
+          mk[0] &= keep_mask(kb, m, G);
+        }
+        key = mask_pattern(mk, m, G);
+      }
+      s_key[w][t] = key;
+    }
+    __syncwarp();
+    warp_order(s_key[w], s_pos[w], n, lane);
+    __syncwarp();
+  }
+  int32_t jr = 0;  // live entries before this chunk (ascending j)
+  for (int base = 0; base < n; base += 32) {
+    const int t = base + lane;
+    const int64_t e = t < n ? (jorder_in ? jorder_in[e0 + t] : e0 + t) : 0;
+    const uint32_t kb = t < n ? ent_keep[e] : 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, kb != 0u);
+    if (kb) {
+      const int32_t rank = jr + __popc(bal & lt);
+      const int32_t p = o0 + (sorted ? s_pos[w][t] : rank);
+      ej2[p] = ej[e];
+      ed2[p] = ed[e];
+      if (W == 2) {
+        for (int q = 0; q < 2; ++q) em2[(int64_t)p * 2 + q] = ((kb >> q) & 1u) ? em[e * 2 + q] : 0ull;
+      } else {
+        em2[p] = em[e] & keep_mask(kb, m, G);
+      }
+      ep2[p] = (uint16_t)kb;
+      jorder2[o0 + rank] = p;
+    }
+    jr += __popc(bal);
+  }
 }
 
 template <int MODE>
@@ -847,77 +921,39 @@ __global__ void k_super_fill(const uint64_t* __restrict__ keys, const int32_t* _
 }
 
 
-// ---------------------------------------------------------------- entry order
-// Within each group, order entries by member-presence pattern (stable, then
-// by j-cluster) so that the 32/m entries a force-kernel warp handles per
-// iteration share their members: the kernel skips a member only when no
-// entry of the iteration has it, so homogeneous iterations waste no lanes.
-constexpr int SORT_SMEM = 1024;
-
-__device__ __forceinline__ uint32_t entry_pattern(const uint64_t* emask, int64_t e, int m, int G) {
-  const int W = (m == 8) ? 2 : 1;
-  uint32_t pat = 0;
-  const int mm = m * m;
-  for (int k = 0; k < G; ++k) {
-    uint64_t bits;
-    if (W == 2) bits = emask[e * 2 + k];
-    else bits = (emask[e] >> (k * mm)) & (mm == 64 ? ~0ull : ((1ull << mm) - 1ull));
-    pat |= (bits != 0ull ? 1u : 0u) << k;
-  }
-  return pat;
-}
-
-__global__ void __launch_bounds__(ROWS_WARPS * 32)
+// force order of a built (unpruned) list's entries: newpos[e] = storage
+// position of the e-th entry (ascending j) of its group
+__global__ void __launch_bounds__(ORDER_WARPS * 32)
 k_entry_order(const int32_t* __restrict__ ent_off, int64_t n_groups, const uint64_t* __restrict__ emask,
               int m, int G, int32_t* __restrict__ newpos) {
-  __shared__ uint32_t s_key[ROWS_WARPS][SORT_SMEM];
+  __shared__ uint32_t s_key[ORDER_WARPS][SORT_SMEM];
+  __shared__ int32_t s_pos[ORDER_WARPS][SORT_SMEM];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t g = blockIdx.x * (int64_t)ROWS_WARPS + w;
+  const int64_t g = blockIdx.x * (int64_t)ORDER_WARPS + w;
   if (g >= n_groups) return;
+  const int W = (m == 8) ? 2 : 1;
   const int32_t e0 = ent_off[g], n = ent_off[g + 1] - e0;
   if (n > SORT_SMEM) {  // very long lists (needle clusters): keep j order
     for (int t = lane; t < n; t += 32) newpos[e0 + t] = e0 + t;
     return;
   }
-  for (int t = lane; t < n; t += 32) s_key[w][t] = entry_pattern(emask, e0 + t, m, G);
+  for (int t = lane; t < n; t += 32) s_key[w][t] = mask_pattern(emask + (int64_t)(e0 + t) * W, m, G);
   __syncwarp();
-  // stable counting order: repeatedly extract the smallest remaining key and
-  // place its entries in index order (iterations = distinct patterns)
-  const unsigned lt = (1u << lane) - 1u;
-  int32_t placed = 0;
-  int64_t prev = -1;
-  while (placed < n) {
-    uint32_t mn = 0xffffffffu;
-    for (int t = lane; t < n; t += 32) {
-      const uint32_t k = s_key[w][t];
-      if ((int64_t)k > prev && k < mn) mn = k;
-    }
-    mn = __reduce_min_sync(0xffffffffu, mn);
-    for (int base = 0; base < n; base += 32) {
-      const int t = base + lane;
-      const bool hit = t < n && s_key[w][t] == mn;
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (hit) newpos[e0 + t] = e0 + placed + __popc(bal & lt);
-      placed += __popc(bal);
-    }
-    prev = mn;
-  }
+  warp_order(s_key[w], s_pos[w], n, lane);
+  __syncwarp();
+  for (int t = lane; t < n; t += 32) newpos[e0 + t] = e0 + s_pos[w][t];
 }
 
 __global__ void k_permute_entries(int64_t n_ent, int W, const int32_t* __restrict__ newpos, const int32_t* ej,
-                                  const float4* edelta, const uint64_t* emask, int32_t* ej2, float4* edelta2,
-                                  uint64_t* emask2) {
+                                  const float4* edelta, const uint64_t* emask, const uint16_t* epres, int32_t* ej2,
+                                  float4* edelta2, uint64_t* emask2, uint16_t* epres2) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_ent) return;
   const int32_t p = newpos[e];
   ej2[p] = ej[e];
   edelta2[p] = edelta[e];
+  epres2[p] = epres[e];
   for (int w = 0; w < W; ++w) emask2[(int64_t)p * W + w] = emask[e * W + w];
-}
-
-__global__ void k_remap_rows(int64_t n_rows, const int32_t* __restrict__ newpos, int32_t* __restrict__ row_entry) {
-  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r < n_rows) row_entry[r] = newpos[row_entry[r]];
 }
 
 static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
@@ -945,28 +981,125 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
   return e;
 }
 
-// reorder a freshly built / pruned list's entries (see k_entry_order)
+// reorder a built list's entries into force order (pruned lists are written
+// in force order by the prune itself)
 static cudaError_t order_entries(List* l, cudaStream_t s) {
   const int64_t ne = l->n_entries;
-  if (ne == 0 || l->n_groups == 0) return cudaSuccess;
+  if (ne == 0 || l->n_groups == 0) {
+    l->entries_ordered = true;
+    return cudaSuccess;
+  }
   const int W = l->mask_words();
   DBuf<int32_t> newpos, ej;
   DBuf<float4> ed;
   DBuf<uint64_t> em;
+  DBuf<uint16_t> ep;
   cudaError_t e;
-  if ((e = newpos.alloc(ne, s)) || (e = ej.alloc(ne, s)) || (e = ed.alloc(ne, s)) || (e = em.alloc(ne * W, s)))
+  if ((e = newpos.alloc(ne, s)) || (e = ej.alloc(ne, s)) || (e = ed.alloc(ne, s)) || (e = em.alloc(ne * W, s)) ||
+      (e = ep.alloc(ne, s)))
     return e;
-  count_launch(3);
-  k_entry_order<<<nb(l->n_groups, ROWS_WARPS), ROWS_WARPS * 32, 0, s>>>(l->ent_offsets.p, l->n_groups,
-                                                                         l->ent_mask.p, l->m, l->G, newpos.p);
-  k_permute_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, newpos.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p, ej.p,
-                                                 ed.p, em.p);
-  if (l->n_rows) k_remap_rows<<<nb(l->n_rows, 256), 256, 0, s>>>(l->n_rows, newpos.p, l->row_entry.p);
+  count_launch(2);
+  k_entry_order<<<nb(l->n_groups, ORDER_WARPS), ORDER_WARPS * 32, 0, s>>>(l->ent_offsets.p, l->n_groups,
+                                                                           l->ent_mask.p, l->m, l->G, newpos.p);
+  k_permute_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, newpos.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p,
+                                                 l->ent_pres.p, ej.p, ed.p, em.p, ep.p);
   std::swap(l->ent_j, ej);
   std::swap(l->ent_delta, ed);
   std::swap(l->ent_mask, em);
-  newpos.release(s); ej.release(s); ed.release(s); em.release(s);
+  std::swap(l->ent_pres, ep);
+  std::swap(l->ent_jorder, newpos);  // j-order position -> storage position
+  ej.release(s); ed.release(s); em.release(s); ep.release(s); newpos.release(s);
+  l->entries_ordered = true;
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- canonical rows
+// The canonical CSR (pairlist.py:185-201 order: rows of ci ascending in cj)
+// from the entries: member k of a group has a row with cj iff bit k of the
+// entry's ent_pres is set; walking the group's entries in ascending j gives
+// every member's rows in order.  One warp per group.
+__global__ void k_rows_count(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
+                             int64_t n_groups, const int32_t* __restrict__ ent_off,
+                             const uint16_t* __restrict__ ent_pres, int32_t* __restrict__ row_count) {
+  const int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const int lane = threadIdx.x & 31;
+  const int nmem = grp_nmem[g];
+  int32_t cnt = 0;  // lane k: rows of member k
+  for (int32_t e = ent_off[g] + lane; e - lane < ent_off[g + 1]; e += 32) {
+    const uint32_t p = e < ent_off[g + 1] ? ent_pres[e] : 0u;
+    for (int k = 0; k < nmem; ++k) {
+      const int c = __popc(__ballot_sync(0xffffffffu, (p >> k) & 1u));
+      if (lane == k) cnt += c;
+    }
+  }
+  if (lane < nmem) row_count[grp_first[g] + lane] = cnt;
+}
+
+__global__ void k_rows_fill(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
+                            int64_t n_groups, const int32_t* __restrict__ ent_off, const int32_t* __restrict__ jorder,
+                            const int32_t* __restrict__ ent_j, const uint64_t* __restrict__ ent_mask,
+                            const uint16_t* __restrict__ ent_pres, int m, const int32_t* __restrict__ offsets,
+                            int32_t* __restrict__ jv, uint64_t* __restrict__ mask) {
+  const int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nmem = grp_nmem[g];
+  const int32_t first = grp_first[g];
+  const int W = (m == 8) ? 2 : 1, mm = m * m;
+  const uint64_t one = (mm == 64) ? ~0ull : ((1ull << mm) - 1ull);
+  int32_t run = lane < nmem ? offsets[first + lane] : 0;  // lane k: next row of member k
+  const int32_t e_beg = ent_off[g], e_end = ent_off[g + 1];
+  for (int32_t t = e_beg + lane; t - lane < e_end; t += 32) {
+    const bool valid = t < e_end;
+    const int32_t e = valid ? (jorder ? jorder[t] : t) : 0;
+    const uint32_t p = valid ? ent_pres[e] : 0u;
+    const int32_t cj = valid ? ent_j[e] : 0;
+    for (int k = 0; k < nmem; ++k) {
+      const unsigned b = __ballot_sync(0xffffffffu, (p >> k) & 1u);
+      if (!b) continue;
+      const int32_t base = __shfl_sync(0xffffffffu, run, k);
+      if ((p >> k) & 1u) {
+        const int32_t row = base + __popc(b & lt);
+        jv[row] = cj;
+        mask[row] = (W == 2) ? ent_mask[(int64_t)e * 2 + k] : ((ent_mask[e] >> (k * mm)) & one);
+      }
+      if (lane == k) run += __popc(b);
+    }
+  }
+}
+
+cudaError_t ensure_rows(List* l, cudaStream_t s) {
+  if (l->rows_ready) return cudaSuccess;
+  const int64_t nc = l->n_clusters;
+  DBuf<int32_t> cnt;
+  int32_t h = 0;
+  cudaError_t e;
+  if ((e = cnt.alloc(nc + 1, s)) || (e = l->offsets.alloc(nc + 1, s))) goto out;
+  if ((e = cudaMemsetAsync(cnt.p, 0, 4 * (nc + 1), s))) goto out;
+  if (l->n_groups > 0) {
+    count_launch();
+    k_rows_count<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups,
+                                                     l->ent_offsets.p, l->ent_pres.p, cnt.p);
+  }
+  if ((e = exclusive_scan_i32(cnt.p, l->offsets.p, nc + 1, s))) goto out;
+  if ((e = cudaMemcpyAsync(&h, l->offsets.p + nc, 4, cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaStreamSynchronize(s))) goto out;
+  l->n_rows = h;
+  if ((e = l->j.alloc(l->n_rows, s)) || (e = l->mask.alloc(l->n_rows, s))) goto out;
+  if (l->n_groups > 0 && l->n_rows > 0) {
+    count_launch();
+    k_rows_fill<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups,
+                                                    l->ent_offsets.p, l->ent_jorder.p, l->ent_j.p, l->ent_mask.p,
+                                                    l->ent_pres.p, l->m, l->offsets.p, l->j.p, l->mask.p);
+  }
+  if ((e = cudaGetLastError())) goto out;
+  l->rows_ready = true;
+  l->delta_ready = false;
+out:
+  cnt.release(s);
+  return e;
 }
 
 // Per-row frame offsets (j-local -> i-local, image included, w = slack) for
@@ -990,8 +1123,9 @@ __global__ void k_row_delta(const int32_t* __restrict__ offsets, const int32_t* 
 }
 
 cudaError_t ensure_row_delta(List* l, cudaStream_t s) {
-  if (l->delta_ready || l->n_rows == 0) return cudaSuccess;
   cudaError_t e;
+  if ((e = ensure_rows(l, s))) return e;
+  if (l->delta_ready || l->n_rows == 0) return cudaSuccess;
   if ((e = l->delta.alloc(l->n_rows, s))) return e;
   Box bx;
   for (int d = 0; d < 3; ++d) {
@@ -1011,7 +1145,7 @@ cudaError_t ensure_row_delta(List* l, cudaStream_t s) {
 cudaError_t finalize_force_layout(List* l, cudaStream_t s) {
   if (l->ordered) return cudaSuccess;
   cudaError_t e;
-  if ((e = order_entries(l, s))) return e;
+  if (!l->entries_ordered && (e = order_entries(l, s))) return e;
   if ((e = order_groups(l, s))) return e;
   l->ordered = true;
   return cudaSuccess;
@@ -1023,9 +1157,9 @@ using namespace nbx;
 
 static void list_release(nbx_list* l, cudaStream_t s) {
   l->offsets.release(s); l->j.release(s); l->mask.release(s); l->delta.release(s);
-  l->row_entry.release(s); l->group_first.release(s);
+  l->group_first.release(s);
   l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
-  l->ent_delta.release(s); l->ent_mask.release(s);
+  l->ent_delta.release(s); l->ent_mask.release(s); l->ent_pres.release(s); l->ent_jorder.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
   w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
@@ -1107,7 +1241,7 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   l->bbox = grid->bbox.p;
   for (int d = 0; d < 3; ++d) l->L[d] = box[d];
   Box bx = make_box(box);
-  DBuf<int32_t> ng, grp_col_first, row_count, ent_count;
+  DBuf<int32_t> ng, grp_col_first, ent_count;
   DBuf<int2> stash;
   DBuf<uint8_t> hbits;
   DBuf<float4> xl;
@@ -1125,9 +1259,7 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   if (n_cols > 0)
     count_launch(), k_groups<<<nb(n_cols, 256), 256, 0, s>>>(grid->col_first.p, n_cols, G, grp_col_first.p,
                                              l->group_first.p, l->group_nmem.p);
-  TRY(row_count.alloc(nc + 1, s));
   TRY(ent_count.alloc(l->n_groups + 1, s));
-  TRY(cudaMemsetAsync(row_count.p, 0, 4 * (nc + 1), s));
   TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
   TRY(stash.alloc(l->n_groups * (int64_t)STASH, s));
   if (prune_pos && nc > 0) {
@@ -1142,7 +1274,6 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
     count_launch();
     k_halo_bits<<<nb(nc, 256), 256, 0, s>>>(halo, grid->perm.p, grid->fill.p, nc, m, hbits.p);
   }
-  so.row_count = row_count.p;
   so.ent_count = ent_count.p;
   so.stash = stash.p;
   if (l->n_groups > 0)
@@ -1154,30 +1285,20 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   }
   TRY(cudaGetLastError());
-  TRY(l->offsets.alloc(nc + 1, s));
   TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
-  TRY(exclusive_scan_i32(row_count.p, l->offsets.p, nc + 1, s));
   TRY(exclusive_scan_i32(ent_count.p, l->ent_offsets.p, l->n_groups + 1, s));
-  so.ent_count = ent_count.p;  // per-group hit counts (read by the emit pass)
-  TRY(cudaMemcpyAsync(&h[0], l->offsets.p + nc, 4, cudaMemcpyDeviceToHost, s));
   TRY(cudaMemcpyAsync(&h[1], l->ent_offsets.p + l->n_groups, 4, cudaMemcpyDeviceToHost, s));
   TRY(cudaStreamSynchronize(s));
-  l->n_rows = h[0];
   l->n_entries = h[1];
-  TRY(l->j.alloc(l->n_rows, s));
-  TRY(l->mask.alloc(l->n_rows, s));
-  TRY(l->row_entry.alloc(l->n_rows, s));
   TRY(l->ent_j.alloc(l->n_entries, s));
   TRY(l->ent_delta.alloc(l->n_entries, s));
   TRY(l->ent_mask.alloc(l->n_entries * l->mask_words(), s));
-  so.offsets = l->offsets.p;
+  TRY(l->ent_pres.alloc(l->n_entries, s));
   so.ent_offsets = l->ent_offsets.p;
-  so.j = l->j.p;
-  so.mask = l->mask.p;
-  so.row_entry = l->row_entry.p;
   so.ent_j = l->ent_j.p;
   so.ent_delta = l->ent_delta.p;
   so.ent_mask = l->ent_mask.p;
+  so.ent_pres = l->ent_pres.p;
   if (l->n_groups > 0)
   {
     count_launch();
@@ -1187,12 +1308,12 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   }
   TRY(cudaGetLastError());
-  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
+  ng.release(s); grp_col_first.release(s); ent_count.release(s); stash.release(s);
   hbits.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  ng.release(s); grp_col_first.release(s); row_count.release(s); ent_count.release(s); stash.release(s);
+  ng.release(s); grp_col_first.release(s); ent_count.release(s); stash.release(s);
   hbits.release(s); xl.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
@@ -1220,83 +1341,62 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   l->bbox = in->bbox;
   for (int d = 0; d < 3; ++d) l->L[d] = in->L[d];
   const int W = in->mask_words();
-  const int64_t nr = in->n_rows, ne = in->n_entries, nc = in->n_clusters;
+  const int64_t ne = in->n_entries, nc = in->n_clusters, ng = in->n_groups;
   Box bx = make_box(box);
-  DBuf<int32_t> keep, scan, alive, escan;
-  DBuf<uint64_t> emask;
+  DBuf<int32_t> alive;
   DBuf<float4> xl;
   DBuf<uint32_t> ekeep;
-  int32_t h[2] = {0, 0};
-  TRY(keep.alloc(nr + 1, s));
-  TRY(scan.alloc(nr + 1, s));
-  TRY(alive.alloc(ne + 1, s));
-  TRY(escan.alloc(ne + 1, s));
-  TRY(emask.alloc(ne * W, s));
-  TRY(cudaMemsetAsync(keep.p, 0, 4 * (nr + 1), s));
-  TRY(cudaMemsetAsync(alive.p, 0, 4 * (ne + 1), s));
+  int32_t h = 0;
+  TRY(alive.alloc(ng + 1, s));
+  TRY(cudaMemsetAsync(alive.p, 0, 4 * (ng + 1), s));
   TRY(ekeep.alloc(ne + 1, s));
   TRY(xl.alloc(nc * in->m, s));
-  if (nc > 0) {
-    count_launch(4);
+  if (nc > 0 && ng > 0) {
+    count_launch(2);
     k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, grid->bbox.p, nc * in->m, in->m, xl.p);
-    const int pblocks = (int)std::min<int64_t>((in->n_groups + ROWS_WARPS - 1) / ROWS_WARPS, 148 * 16);
+    const int pblocks = (int)std::min<int64_t>(ng, 148 * 64);
     const double r2 = in->r_list * in->r_list;
-#define NBX_PRUNE(MM, GG)                                                                                    \
-  k_prune_entries<MM, GG><<<pblocks, ROWS_WARPS * 32, 0, s>>>(in->group_first.p, in->group_nmem.p, in->n_groups, \
-                                                              in->ent_offsets.p, in->ent_j.p, in->ent_delta.p,    \
-                                                              in->ent_mask.p, xl.p, grid->bbox.p, pos, bx, r2, ekeep.p)
-    if (pblocks > 0) {
-      switch (in->m) {
-        case 1: NBX_PRUNE(1, 16); break;
-        case 2: NBX_PRUNE(2, 8); break;
-        case 4: NBX_PRUNE(4, 4); break;
-        default: NBX_PRUNE(8, 2); break;
-      }
+#define NBX_PRUNE(MM, GG)                                                                                     \
+  k_prune_entries<MM, GG><<<pblocks, PRUNE_WARPS * 32, 0, s>>>(in->group_first.p, in->group_nmem.p, ng,        \
+                                                               in->ent_offsets.p, in->ent_j.p, in->ent_delta.p, \
+                                                               in->ent_mask.p, xl.p, grid->bbox.p, pos, bx, r2,  \
+                                                               ekeep.p, alive.p)
+    switch (in->m) {
+      case 1: NBX_PRUNE(1, 16); break;
+      case 2: NBX_PRUNE(2, 8); break;
+      case 4: NBX_PRUNE(4, 4); break;
+      default: NBX_PRUNE(8, 2); break;
     }
 #undef NBX_PRUNE
-    k_rows_from_entries<<<nb(nc, 8), 256, 0, s>>>(in->offsets.p, in->row_entry.p, nc, in->G, grid->cell_of_cluster.p,
-                                                    grid->col_first.p, ekeep.p, keep.p);
-    if (ne) k_entries_keep<<<nb(ne, 256), 256, 0, s>>>(ekeep.p, ne, in->m, in->G, in->ent_mask.p, emask.p, alive.p);
   }
   TRY(cudaGetLastError());
-  TRY(exclusive_scan_i32(keep.p, scan.p, nr + 1, s));
-  TRY(exclusive_scan_i32(alive.p, escan.p, ne + 1, s));
-  TRY(cudaMemcpyAsync(&h[0], scan.p + nr, 4, cudaMemcpyDeviceToHost, s));
-  TRY(cudaMemcpyAsync(&h[1], escan.p + ne, 4, cudaMemcpyDeviceToHost, s));
+  TRY(l->ent_offsets.alloc(ng + 1, s));
+  TRY(exclusive_scan_i32(alive.p, l->ent_offsets.p, ng + 1, s));
+  TRY(cudaMemcpyAsync(&h, l->ent_offsets.p + ng, 4, cudaMemcpyDeviceToHost, s));
   TRY(cudaStreamSynchronize(s));
-  l->n_rows = h[0];
-  l->n_entries = h[1];
-  TRY(l->offsets.alloc(nc + 1, s));
-  TRY(l->j.alloc(l->n_rows, s));
-  TRY(l->mask.alloc(l->n_rows, s));
-  TRY(l->row_entry.alloc(l->n_rows, s));
-  TRY(l->group_first.alloc(l->n_groups, s));
-  TRY(l->group_nmem.alloc(l->n_groups, s));
-  TRY(l->ent_offsets.alloc(l->n_groups + 1, s));
+  l->n_entries = h;
+  TRY(l->group_first.alloc(ng, s));
+  TRY(l->group_nmem.alloc(ng, s));
   TRY(l->ent_j.alloc(l->n_entries, s));
   TRY(l->ent_delta.alloc(l->n_entries, s));
   TRY(l->ent_mask.alloc(l->n_entries * W, s));
-  count_launch(), k_new_offsets<<<nb(nc + 1, 256), 256, 0, s>>>(in->offsets.p, nc, scan.p, l->offsets.p);
-  count_launch(), k_new_offsets<<<nb(l->n_groups + 1, 256), 256, 0, s>>>(in->ent_offsets.p, l->n_groups, escan.p,
-                                                         l->ent_offsets.p);
-  if (l->n_groups) {
-    TRY(cudaMemcpyAsync(l->group_first.p, in->group_first.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
-    TRY(cudaMemcpyAsync(l->group_nmem.p, in->group_nmem.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
+  TRY(l->ent_pres.alloc(l->n_entries, s));
+  TRY(l->ent_jorder.alloc(l->n_entries, s));
+  if (ng) {
+    TRY(cudaMemcpyAsync(l->group_first.p, in->group_first.p, 4 * ng, cudaMemcpyDeviceToDevice, s));
+    TRY(cudaMemcpyAsync(l->group_nmem.p, in->group_nmem.p, 4 * ng, cudaMemcpyDeviceToDevice, s));
+    count_launch();
+    k_compact_order<<<nb(ng, ORDER_WARPS), ORDER_WARPS * 32, 0, s>>>(
+        in->ent_offsets.p, ng, in->ent_jorder.p, ekeep.p, in->ent_j.p, in->ent_delta.p, in->ent_mask.p, in->m, in->G,
+        l->ent_offsets.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p, l->ent_pres.p, l->ent_jorder.p);
   }
-  if (nr)
-    count_launch(), k_compact_rows<<<nb(nr, 256), 256, 0, s>>>(nr, keep.p, scan.p, escan.p, in->j.p, in->mask.p,
-                                               in->row_entry.p, l->j.p, l->mask.p, l->row_entry.p);
-  if (ne)
-    count_launch(), k_compact_entries<<<nb(ne, 256), 256, 0, s>>>(ne, W, alive.p, escan.p, in->ent_j.p, in->ent_delta.p,
-                                                  emask.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p);
   TRY(cudaGetLastError());
-  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
-  ekeep.release(s);
+  l->entries_ordered = true;
+  alive.release(s); xl.release(s); ekeep.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  keep.release(s); scan.release(s); alive.release(s); escan.release(s); emask.release(s); xl.release(s);
-  ekeep.release(s);
+  alive.release(s); xl.release(s); ekeep.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }
@@ -1307,7 +1407,7 @@ extern "C" int nbx_list_info(const nbx_list_t* l, int64_t out[5]) {
     return NBX_ERR_PARAM;
   }
   out[0] = l->n_clusters;
-  out[1] = l->n_rows;
+  out[1] = l->rows_ready ? l->n_rows : -1;  // canonical rows: nbx_list_rows
   out[2] = l->m;
   out[3] = l->n_groups;
   out[4] = l->n_entries;
@@ -1326,6 +1426,20 @@ static cudaError_t dl(const TD* d, int64_t count, TH* h, cudaStream_t s) {
   return e;
 }
 
+extern "C" int nbx_list_rows(nbx_list_t* l, void* stream, int64_t* n_rows) {
+  if (!l || !n_rows) {
+    set_error("nbx_list_rows: null argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaError_t e = ensure_rows(l, to_stream(stream));
+  if (e) {
+    set_error("nbx_list_rows: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  *n_rows = l->n_rows;
+  return NBX_OK;
+}
+
 extern "C" int nbx_list_download(const nbx_list_t* l, int64_t* offsets, int64_t* j_idx,
                                  uint64_t* masks, void* stream) {
   if (!l) {
@@ -1334,7 +1448,7 @@ extern "C" int nbx_list_download(const nbx_list_t* l, int64_t* offsets, int64_t*
   }
   cudaStream_t s = to_stream(stream);
   cudaError_t e;
-  if ((e = dl(l->offsets.p, l->n_clusters + 1, offsets, s)) || (e = dl(l->j.p, l->n_rows, j_idx, s)) ||
+  if ((e = ensure_rows(const_cast<nbx_list*>(static_cast<const nbx_list*>(l)), s)) || (e = dl(l->offsets.p, l->n_clusters + 1, offsets, s)) || (e = dl(l->j.p, l->n_rows, j_idx, s)) ||
       (e = dl(l->mask.p, l->n_rows, masks, s))) {
     set_error("nbx_list_download: %s", cudaGetErrorString(e));
     return NBX_ERR_CUDA;
@@ -1383,6 +1497,10 @@ extern "C" int nbx_super_layout(const nbx_list_t* lc, int32_t size, void* stream
   }
   nbx_list* l = const_cast<nbx_list*>(static_cast<const nbx_list*>(lc));
   cudaStream_t s = to_stream(stream);
+  if (cudaError_t e0 = ensure_rows(l, s)) {
+    set_error("nbx_super_layout: %s", cudaGetErrorString(e0));
+    return NBX_ERR_CUDA;
+  }
   const int64_t nr = l->n_rows, nc = l->n_clusters;
   const int64_t ngr = (nc + size - 1) / size;
   DBuf<int32_t> ci_of_row, vals, vals2, head, hscan, gcount;

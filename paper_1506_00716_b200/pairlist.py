@@ -65,6 +65,10 @@ class ClusterPairList:
 
     @property
     def n_pairs(self) -> int:
+        if self._n_rows < 0:  # canonical rows are derived from the entries on first use
+            n = ctypes.c_int64()
+            _lib.check(_lib.load().nbx_list_rows(self._h, dev.stream(), ctypes.byref(n)), "list_rows")
+            self._n_rows = int(n.value)
         return self._n_rows
 
     @property
@@ -76,8 +80,8 @@ class ClusterPairList:
     def _materialise(self):
         if self._host is None:
             off = np.empty(self._n_i + 1, dtype=np.int64)
-            jj = np.empty(self._n_rows, dtype=np.int64)
-            mk = np.empty(self._n_rows, dtype=np.uint64)
+            jj = np.empty(self.n_pairs, dtype=np.int64)
+            mk = np.empty(self.n_pairs, dtype=np.uint64)
             torch.cuda.synchronize()
             _lib.check(_lib.load().nbx_list_download(self._h, _lib.ptr(off), _lib.ptr(jj), _lib.ptr(mk),
                                                      dev.stream()), "list_download")
@@ -215,7 +219,7 @@ def prune_pair_list(plist: ClusterPairList, positions, box: SimBox) -> ClusterPa
     if shape != (plist.grid.n_slots, 3):
         raise ParameterError(f"positions shape {shape} does not match the list's slot layout "
                              f"{(plist.grid.n_slots, 3)}")
-    if plist.n_pairs == 0:
+    if plist.n_entries == 0:
         return plist
     p, keep_alive = _positions_ptr(plist, positions)
     h = ctypes.c_void_p()
