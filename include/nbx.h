@@ -117,10 +117,14 @@ int nbx_pairlist_build_pruned(const nbx_grid_t* grid, const double box[3], doubl
 int nbx_pairlist_prune(const nbx_list_t* list, const nbx_grid_t* grid,
                        const double* clustered_positions, const double box[3], void* stream,
                        nbx_list_t** out);
-/* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; n_rows is -1 until
- * the canonical rows are materialised (lists hold the grouped entries; the
- * canonical CSR is derived from them on first use) */
+/* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; never syncs.
+ * n_rows is -1 until the canonical rows are materialised (lists hold the
+ * grouped entries; the canonical CSR is derived from them on first use,
+ * nbx_list_rows); n_entries is -1 while a pruned list's live entry count is
+ * still only on the device (nbx_list_entries). */
 int nbx_list_info(const nbx_list_t* list, int64_t out[5]);
+/* live (group, j-cluster) entry count; syncs if not yet known */
+int nbx_list_entries(nbx_list_t* list, void* stream, int64_t* n_entries);
 /* materialise the canonical CSR rows (pairlist.ClusterPairList offsets /
  * j_idx / masks) if needed and return their count; syncs */
 int nbx_list_rows(nbx_list_t* list, void* stream, int64_t* n_rows);

@@ -23,7 +23,7 @@ FORCE_ENERGY, FORCE_ACCUMULATE, FORCE_CLUSTERED, FORCE_CANONICAL = 1, 2, 4, 8
 EXPORTS = (
     "nbx_version", "nbx_last_error", "nbx_grid_build", "nbx_grid_info", "nbx_grid_download",
     "nbx_grid_clustered_positions", "nbx_scatter_to_original", "nbx_grid_free",
-    "nbx_pairlist_build", "nbx_pairlist_prune", "nbx_list_info", "nbx_list_rows", "nbx_list_download",
+    "nbx_pairlist_build", "nbx_pairlist_prune", "nbx_list_info", "nbx_list_rows", "nbx_list_entries", "nbx_list_download",
     "nbx_super_layout", "nbx_super_download", "nbx_count_within", "nbx_list_free",
     "nbx_force", "nbx_find_singular", "nbx_launch_count", "nbx_timing_enable", "nbx_timing_query",
     "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
@@ -78,6 +78,7 @@ def load():
         "nbx_pairlist_prune": (ctypes.c_int, [P, P, P, P, P, PP]),
         "nbx_list_info": (ctypes.c_int, [P, P]),
         "nbx_list_rows": (ctypes.c_int, [P, P, P]),
+        "nbx_list_entries": (ctypes.c_int, [P, P, P]),
         "nbx_list_download": (ctypes.c_int, [P, P, P, P, P]),
         "nbx_super_layout": (ctypes.c_int, [P, I32, P, P]),
         "nbx_super_download": (ctypes.c_int, [P, P, P, P, P]),

@@ -913,8 +913,9 @@ __global__ void k_first_sorted(const int32_t* __restrict__ keys, int64_t n, int6
                                int32_t* __restrict__ first) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
-  const int32_t prev = i == 0 ? -1 : keys[i - 1];
-  const int32_t cur = i == n ? (int32_t)n_keys : keys[i];
+  // keys >= n_keys are unused storage slots (sorted last)
+  const int32_t prev = i == 0 ? -1 : min(keys[i - 1], (int32_t)n_keys);
+  const int32_t cur = i == n ? (int32_t)n_keys : min(keys[i], (int32_t)n_keys);
   for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
 }
 

@@ -42,11 +42,29 @@ __global__ void k_bin(const double* __restrict__ pos, int64_t n, Box box, int64_
   atomicAdd(&col_count[cid], 1);
 }
 
-__global__ void k_col_clusters(const int32_t* __restrict__ col_count, int64_t n_cols, int m,
-                               int32_t* __restrict__ ncl) {
+__global__ void k_col_clusters(const int32_t* __restrict__ col_count, int64_t n_cols, int m, int G,
+                               int32_t* __restrict__ ncl, int32_t* __restrict__ ngr) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c < n_cols) ncl[c] = (col_count[c] + m - 1) / m;
-  if (c == n_cols) ncl[c] = 0;
+  if (c < n_cols) {
+    const int32_t k = (col_count[c] + m - 1) / m;
+    ncl[c] = k;
+    ngr[c] = (k + G - 1) / G;
+  }
+  if (c == n_cols) ncl[c] = ngr[c] = 0;
+}
+
+// groups of G consecutive clusters of one column (the search / force work unit)
+__global__ void k_groups(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
+                         const int32_t* __restrict__ grp_col_first, int32_t* __restrict__ group_first,
+                         int32_t* __restrict__ group_nmem) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const int32_t f = col_first[c], ncl = col_first[c + 1] - f;
+  const int32_t g0 = grp_col_first[c];
+  for (int32_t t = 0; t * G < ncl; ++t) {
+    group_first[g0 + t] = f + t * G;
+    group_nmem[g0 + t] = min(G, ncl - t * G);
+  }
 }
 
 __global__ void k_scatter(const int32_t* __restrict__ cell, int64_t n,
@@ -252,11 +270,11 @@ extern "C" int nbx_grid_build(const double* positions, int64_t n, const double b
   }
   const int64_t n_cols = cells * cells;
   DBuf<double> wpos;
-  DBuf<int32_t> cell, col_count, col_atom_first, ncl, col_fill, sorted;
+  DBuf<int32_t> cell, col_count, col_atom_first, ncl, col_fill, sorted, ngr, grp_col_first;
   auto fail = [&](cudaError_t e) {
     set_error("nbx_grid_build: %s", cudaGetErrorString(e));
     wpos.release(s); cell.release(s); col_count.release(s); col_atom_first.release(s);
-    ncl.release(s); col_fill.release(s); sorted.release(s);
+    ncl.release(s); col_fill.release(s); sorted.release(s); ngr.release(s); grp_col_first.release(s);
     nbx_grid_free(g);
     return NBX_ERR_CUDA;
   };
@@ -264,22 +282,31 @@ extern "C" int nbx_grid_build(const double* positions, int64_t n, const double b
   if ((e = wpos.alloc(3 * n, s)) || (e = cell.alloc(n, s)) || (e = col_count.alloc(n_cols + 1, s)) ||
       (e = col_atom_first.alloc(n_cols + 1, s)) || (e = ncl.alloc(n_cols + 1, s)) ||
       (e = col_fill.alloc(n_cols, s)) || (e = g->col_first.alloc(n_cols + 1, s)) ||
-      (e = sorted.alloc(n, s)) || (e = g->inverse_perm.alloc(n, s)))
+      (e = sorted.alloc(n, s)) || (e = g->inverse_perm.alloc(n, s)) || (e = ngr.alloc(n_cols + 1, s)) ||
+      (e = grp_col_first.alloc(n_cols + 1, s)))
     return fail(e);
   if ((e = cudaMemsetAsync(col_count.p, 0, sizeof(int32_t) * (n_cols + 1), s)) ||
       (e = cudaMemsetAsync(col_fill.p, 0, sizeof(int32_t) * n_cols, s)))
     return fail(e);
   if (n > 0) count_launch(), k_bin<<<blocks(n, 256), 256, 0, s>>>(positions, n, bx, cells, wpos.p, cell.p, col_count.p);
   count_launch();
-  k_col_clusters<<<blocks(n_cols + 1, 256), 256, 0, s>>>(col_count.p, n_cols, m, ncl.p);
+  const int G = 16 / m;
+  k_col_clusters<<<blocks(n_cols + 1, 256), 256, 0, s>>>(col_count.p, n_cols, m, G, ncl.p, ngr.p);
   if ((e = exclusive_scan_i32(col_count.p, col_atom_first.p, n_cols + 1, s)) ||
-      (e = exclusive_scan_i32(ncl.p, g->col_first.p, n_cols + 1, s)))
+      (e = exclusive_scan_i32(ncl.p, g->col_first.p, n_cols + 1, s)) ||
+      (e = exclusive_scan_i32(ngr.p, grp_col_first.p, n_cols + 1, s)))
     return fail(e);
-  int32_t nc = 0;
+  int32_t nc = 0, ngroups = 0;
   if ((e = cudaMemcpyAsync(&nc, g->col_first.p + n_cols, sizeof(int32_t), cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(&ngroups, grp_col_first.p + n_cols, sizeof(int32_t), cudaMemcpyDeviceToHost, s)) ||
       (e = cudaStreamSynchronize(s)))
     return fail(e);
   g->n_clusters = nc;
+  g->n_groups = ngroups;
+  if ((e = g->group_first.alloc(ngroups, s)) || (e = g->group_nmem.alloc(ngroups, s))) return fail(e);
+  if (n_cols > 0)
+    count_launch(), k_groups<<<blocks(n_cols, 256), 256, 0, s>>>(g->col_first.p, n_cols, G, grp_col_first.p,
+                                                  g->group_first.p, g->group_nmem.p);
   const int64_t ns = (int64_t)nc * m;
   if ((e = g->perm.alloc(ns, s)) || (e = g->fill.alloc(ns, s)) || (e = g->cpos.alloc(3 * ns, s)) ||
       (e = g->cell_of_cluster.alloc(nc, s)) || (e = g->bbox.alloc(6 * (int64_t)nc, s)) ||
@@ -296,7 +323,7 @@ extern "C" int nbx_grid_build(const double* positions, int64_t n, const double b
   }
   if ((e = cudaGetLastError())) return fail(e);
   wpos.release(s); cell.release(s); col_count.release(s); col_atom_first.release(s);
-  ncl.release(s); col_fill.release(s); sorted.release(s);
+  ncl.release(s); col_fill.release(s); sorted.release(s); ngr.release(s); grp_col_first.release(s);
   *out = g;
   return NBX_OK;
 }
@@ -375,5 +402,6 @@ extern "C" void nbx_grid_free(nbx_grid_t* g) {
   g->perm.release(s); g->inverse_perm.release(s); g->fill.release(s);
   g->cell_of_cluster.release(s); g->col_first.release(s); g->cpos.release(s);
   g->bbox.release(s); g->zr.release(s); g->bbf.release(s); g->nreal.release(s);
+  g->group_first.release(s); g->group_nmem.release(s);
   delete g;
 }

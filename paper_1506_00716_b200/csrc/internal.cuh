@@ -60,6 +60,10 @@ struct Grid {
   DBuf<float2> zr;              // (n_clusters) z range rounded outward (search prefilter)
   DBuf<float4> bbf;             // (n_clusters, 2) FP32 box rounded outward (search)
   DBuf<int8_t> nreal;           // (n_clusters) real (non-filler) slots
+  // search / force groups: G = 16/m consecutive clusters of one column
+  int64_t n_groups = 0;
+  DBuf<int32_t> group_first;    // (n_groups) first member cluster
+  DBuf<int32_t> group_nmem;     // (n_groups)
   int64_t n_slots() const { return n_clusters * m; }
 };
 
@@ -91,7 +95,9 @@ struct List {
   int64_t n_clusters = 0;
   int64_t n_rows = 0;
   int64_t n_groups = 0;
-  int64_t n_entries = 0;
+  int64_t n_entries = 0;         // entry storage (>= the live count when !entries_exact)
+  bool entries_exact = true;      // n_live known on the host
+  int64_t n_live = -1;            // live entries (-1: == n_entries)
   double r_list = 0.0;
   double L[3] = {0, 0, 0};
   const double* bbox = nullptr;  // the grid's boxes (frame of `delta`); the grid outlives its lists

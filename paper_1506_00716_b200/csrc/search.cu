@@ -391,26 +391,6 @@ __global__ void k_halo_bits(const uint8_t* __restrict__ halo, const int32_t* __r
   hb[c] = (uint8_t)b;
 }
 
-__global__ void k_groups(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
-                         const int32_t* __restrict__ grp_col_first, int32_t* __restrict__ group_first,
-                         int32_t* __restrict__ group_nmem) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n_cols) return;
-  const int32_t f = col_first[c], ncl = col_first[c + 1] - f;
-  const int32_t g0 = grp_col_first[c];
-  for (int32_t t = 0; t * G < ncl; ++t) {
-    group_first[g0 + t] = f + t * G;
-    group_nmem[g0 + t] = min(G, ncl - t * G);
-  }
-}
-
-__global__ void k_groups_per_col(const int32_t* __restrict__ col_first, int64_t n_cols, int G,
-                                 int32_t* __restrict__ ng) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c < n_cols) ng[c] = (col_first[c + 1] - col_first[c] + G - 1) / G;
-  if (c == n_cols) ng[c] = 0;
-}
-
 // ---------------------------------------------------------------- exact pair decisions
 // d2 of slots (si, sj) of `pos` with the reference's min image
 // (model.py:159-172) and einsum order (pairlist.py:236).
@@ -451,12 +431,21 @@ constexpr int ROWS_WARPS = 4;
 // Positions for the row kernels: FP32, relative to the cluster's build-time
 // box corner (the frame of the per-row `delta` offsets), ~1e-7 nm resolution.
 __global__ void k_local_coords(const double* __restrict__ pos, const double* __restrict__ bbox, int64_t n_slots,
-                               int m, float4* __restrict__ xl) {
+                               int m, float4* __restrict__ xl, const double* __restrict__ cpos = nullptr,
+                               unsigned int* __restrict__ dmax = nullptr) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= n_slots) return;
-  const int64_t c = s / m;
-  xl[s] = make_float4((float)(pos[3 * s] - bbox[6 * c]), (float)(pos[3 * s + 1] - bbox[6 * c + 1]),
-                      (float)(pos[3 * s + 2] - bbox[6 * c + 2]), 0.f);
+  float d = 0.f;
+  if (s < n_slots) {
+    const int64_t c = s / m;
+    xl[s] = make_float4((float)(pos[3 * s] - bbox[6 * c]), (float)(pos[3 * s + 1] - bbox[6 * c + 1]),
+                        (float)(pos[3 * s + 2] - bbox[6 * c + 2]), 0.f);
+    if (dmax)  // largest coordinate displacement from the build positions (no wrapping: a wrap counts as L)
+      for (int k = 0; k < 3; ++k) d = fmaxf(d, (float)fabs(pos[3 * s + k] - cpos[3 * s + k]));
+  }
+  if (dmax) {
+    for (int o = 16; o; o >>= 1) d = fmaxf(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(dmax, __float_as_uint(d * 1.0001f + 1e-6f));
+  }
 }
 
 // Exact replay of the reference decision d^2 <= r^2 for slots (si, sj)
@@ -604,17 +593,52 @@ k_rows(const int32_t* __restrict__ offsets, const int32_t* __restrict__ jv, cons
 // "member kept" word (diagonal rows always kept); per group the number of
 // surviving entries.
 constexpr int PRUNE_WARPS = 4;
+
+// One prune batch (R entries of a warp) against the group's i-atoms:
+// branch-free over the member's pairs, members absent from the whole batch
+// skipped warp-uniformly.  MI = per-pair minimum image (entries whose slack
+// cannot guarantee the single shift at the current displacements).
+template <int M, int G, int W, bool MI>
+__device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, const uint32_t (&wd)[2 * W],
+                                            const float4& xj, float lo, float hi, const float (&Lf)[3],
+                                            const float (&iLf)[3], uint32_t& inbits, uint32_t& amb) {
+  constexpr int MM = M * M;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int p0 = W == 2 ? k * 64 : k * MM;
+    uint32_t cb = 0;  // this member's column bits (pairs (a, b) for this lane's b)
+#pragma unroll
+    for (int a = 0; a < M; ++a) cb |= (wd[(p0 + a * M) >> 5] >> ((p0 + a * M) & 31)) & 1u ? (1u << a) : 0u;
+    if (!__any_sync(0xffffffffu, cb != 0u)) continue;
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+      const float4 xi = s_xi[k * M + a];
+      float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
+      if (MI) {
+        dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
+        dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
+        dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
+      }
+      const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const bool adm = (cb >> a) & 1u;
+      inbits |= (adm && f < lo) ? (1u << k) : 0u;
+      amb |= (adm && f >= lo && f <= hi) ? (1u << (k * M + a)) : 0u;
+    }
+  }
+}
+
 template <int M, int G>
 __global__ void __launch_bounds__(PRUNE_WARPS * 32)
 k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem, int64_t n_groups,
                 const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
                 const float4* __restrict__ ent_delta, const uint64_t* __restrict__ ent_mask,
                 const float4* __restrict__ xl, const double* __restrict__ bbox, const double* __restrict__ pos,
-                Box box, double r2, uint32_t* __restrict__ ent_keep, int32_t* __restrict__ grp_alive) {
+                Box box, double r2, const unsigned int* __restrict__ dmax_bits, float slack_base,
+                uint32_t* __restrict__ ent_keep, int32_t* __restrict__ grp_alive) {
   constexpr int R = 32 / M;
   constexpr int IA = G * M;
-  constexpr int MM = M * M;
   constexpr int W = (G * M * M > 64) ? 2 : 1;
+  constexpr int U = 2;  // batches in flight per warp
   __shared__ float4 s_xi[IA];
   __shared__ int32_t s_cnt[PRUNE_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -622,6 +646,7 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
   const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
   const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
   const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
+  const float slack_thr = slack_base + 4.f * __uint_as_float(*dmax_bits);
   for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const int32_t first = grp_first[g];
     const int nmem = grp_nmem[g];
@@ -640,58 +665,58 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
     __syncthreads();
     const int32_t e_beg = ent_off[g], e_end = ent_off[g + 1];
     int32_t alive = 0;
-    for (int32_t e0 = e_beg + w * R; e0 < e_end; e0 += PRUNE_WARPS * R) {
-      const int32_t e = e0 + r;
-      const bool valid = e < e_end;
-      uint32_t inbits = 0;   // members with a pair within r_list in this lane's column
-      int32_t cj = -1;
-      if (valid) {
-        cj = __ldg(ent_j + e);
-        const float4 d = __ldg(ent_delta + e);
-        float4 xj = __ldg(xl + (int64_t)cj * M + b);
-        xj.x += d.x;
-        xj.y += d.y;
-        xj.z += d.z;
-        uint32_t wd[2 * W];
+    for (int32_t e0 = e_beg + w * R; e0 < e_end; e0 += PRUNE_WARPS * R * U) {
+      // loads of U batches first (memory-level parallelism), then the math
+      int32_t cj[U];
+      float4 xj[U];
+      uint32_t wd[U][2 * W];
+      bool valid[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t e = e0 + u * PRUNE_WARPS * R + r;
+        valid[u] = e < e_end;
+        cj[u] = valid[u] ? __ldg(ent_j + e) : -1;
+        float4 d = make_float4(0.f, 0.f, 0.f, 3.0e38f);
+        if (valid[u]) d = __ldg(ent_delta + e);
+        xj[u] = d;
 #pragma unroll
         for (int q = 0; q < W; ++q) {
-          const uint64_t mw = __ldg(ent_mask + (int64_t)e * W + q) >> b;
-          wd[2 * q] = (uint32_t)mw;
-          wd[2 * q + 1] = (uint32_t)(mw >> 32);
+          const uint64_t mw = valid[u] ? (__ldg(ent_mask + (int64_t)e * W + q) >> b) : 0ull;
+          wd[u][2 * q] = (uint32_t)mw;
+          wd[u][2 * q + 1] = (uint32_t)(mw >> 32);
         }
-        uint32_t amb = 0;
+      }
 #pragma unroll
-        for (int k = 0; k < G; ++k) {
-#pragma unroll
-          for (int a = 0; a < M; ++a) {
-            const int p = (W == 2 ? k * 64 : k * MM) + a * M;
-            if (!(wd[p >> 5] & (1u << (p & 31)))) continue;
-            const float4 xi = s_xi[k * M + a];
-            float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
-            dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
-            dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
-            dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
-            const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            if (f < lo) inbits |= 1u << k;
-            else if (f <= hi) amb |= 1u << (k * M + a);
-          }
+      for (int u = 0; u < U; ++u) {
+        if (valid[u]) {
+          const float4 x = __ldg(xl + (int64_t)cj[u] * M + b);
+          xj[u] = make_float4(x.x + xj[u].x, x.y + xj[u].y, x.z + xj[u].z, xj[u].w);
         }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!__any_sync(0xffffffffu, valid[u])) break;
+        uint32_t inbits = 0, amb = 0;
+        if (!__any_sync(0xffffffffu, valid[u] && xj[u].w < slack_thr))
+          prune_batch<M, G, W, false>(s_xi, wd[u], xj[u], lo, hi, Lf, iLf, inbits, amb);
+        else
+          prune_batch<M, G, W, true>(s_xi, wd[u], xj[u], lo, hi, Lf, iLf, inbits, amb);
         while (amb) {  // rare: exact FP64 replay of the reference decision
           const int ia = __ffs(amb) - 1;
           amb &= amb - 1;
           const int k = ia / M;
           if ((inbits >> k) & 1u) continue;
-          if (exact_within(pos, (int64_t)first * M + ia, (int64_t)cj * M + b, box, r2)) inbits |= 1u << k;
+          if (exact_within(pos, (int64_t)first * M + ia, (int64_t)cj[u] * M + b, box, r2)) inbits |= 1u << k;
         }
-      }
-      // OR over the entry's M lanes
+        // OR over the entry's M lanes
 #pragma unroll
-      for (int o = 1; o < M; o <<= 1) inbits |= __shfl_xor_sync(0xffffffffu, inbits, o);
-      if (valid && b == 0) {
-        if (cj >= first && cj < first + nmem) inbits |= 1u << (cj - first);  // diagonal rows always survive
-        ent_keep[e] = inbits;
+        for (int o = 1; o < M; o <<= 1) inbits |= __shfl_xor_sync(0xffffffffu, inbits, o);
+        if (valid[u] && b == 0) {
+          if (cj[u] >= first && cj[u] < first + nmem) inbits |= 1u << (cj[u] - first);  // diagonal rows survive
+          ent_keep[e0 + u * PRUNE_WARPS * R + r] = inbits;
+        }
+        alive += __popc(__ballot_sync(0xffffffffu, valid[u] && b == 0 && inbits != 0u));
       }
-      alive += __popc(__ballot_sync(0xffffffffu, valid && b == 0 && inbits != 0u));
     }
     if (lane == 0) s_cnt[w] = alive;
     __syncthreads();
@@ -957,6 +982,11 @@ __global__ void k_permute_entries(int64_t n_ent, int W, const int32_t* __restric
 }
 
 static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+__global__ void k_fill_i32(int32_t* __restrict__ v, int64_t n, int32_t x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = x;
+}
 
 __global__ void k_group_keys(const int32_t* __restrict__ ent_off, int64_t n_groups, int32_t* __restrict__ keys,
                              int32_t* __restrict__ vals) {
@@ -1241,24 +1271,20 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   l->bbox = grid->bbox.p;
   for (int d = 0; d < 3; ++d) l->L[d] = box[d];
   Box bx = make_box(box);
-  DBuf<int32_t> ng, grp_col_first, ent_count;
+  DBuf<int32_t> ent_count;
   DBuf<int2> stash;
   DBuf<uint8_t> hbits;
   DBuf<float4> xl;
   int32_t h[2] = {0, 0};
   SearchOut so{};
-  TRY(ng.alloc(n_cols + 1, s));
-  TRY(grp_col_first.alloc(n_cols + 1, s));
-  count_launch(), k_groups_per_col<<<nb(n_cols + 1, 256), 256, 0, s>>>(grid->col_first.p, n_cols, G, ng.p);
-  TRY(exclusive_scan_i32(ng.p, grp_col_first.p, n_cols + 1, s));
-  TRY(cudaMemcpyAsync(&h[0], grp_col_first.p + n_cols, 4, cudaMemcpyDeviceToHost, s));
-  TRY(cudaStreamSynchronize(s));
-  l->n_groups = h[0];
+  (void)n_cols;
+  l->n_groups = grid->n_groups;
   TRY(l->group_first.alloc(l->n_groups, s));
   TRY(l->group_nmem.alloc(l->n_groups, s));
-  if (n_cols > 0)
-    count_launch(), k_groups<<<nb(n_cols, 256), 256, 0, s>>>(grid->col_first.p, n_cols, G, grp_col_first.p,
-                                             l->group_first.p, l->group_nmem.p);
+  if (l->n_groups) {
+    TRY(cudaMemcpyAsync(l->group_first.p, grid->group_first.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
+    TRY(cudaMemcpyAsync(l->group_nmem.p, grid->group_nmem.p, 4 * l->n_groups, cudaMemcpyDeviceToDevice, s));
+  }
   TRY(ent_count.alloc(l->n_groups + 1, s));
   TRY(cudaMemsetAsync(ent_count.p, 0, 4 * (l->n_groups + 1), s));
   TRY(stash.alloc(l->n_groups * (int64_t)STASH, s));
@@ -1308,12 +1334,12 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
         grid->nreal.p, grid->col_first.p, grid->cells, bx, r_list, so, hbits.p);
   }
   TRY(cudaGetLastError());
-  ng.release(s); grp_col_first.release(s); ent_count.release(s); stash.release(s);
+  ent_count.release(s); stash.release(s);
   hbits.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  ng.release(s); grp_col_first.release(s); ent_count.release(s); stash.release(s);
+  ent_count.release(s); stash.release(s);
   hbits.release(s); xl.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
@@ -1345,22 +1371,26 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   Box bx = make_box(box);
   DBuf<int32_t> alive;
   DBuf<float4> xl;
-  DBuf<uint32_t> ekeep;
+  DBuf<uint32_t> ekeep, dmax;
   int32_t h = 0;
+  TRY(dmax.alloc(1, s));
+  TRY(cudaMemsetAsync(dmax.p, 0, 4, s));
   TRY(alive.alloc(ng + 1, s));
   TRY(cudaMemsetAsync(alive.p, 0, 4 * (ng + 1), s));
   TRY(ekeep.alloc(ne + 1, s));
   TRY(xl.alloc(nc * in->m, s));
   if (nc > 0 && ng > 0) {
     count_launch(2);
-    k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, grid->bbox.p, nc * in->m, in->m, xl.p);
+    k_local_coords<<<nb(nc * in->m, 256), 256, 0, s>>>(pos, grid->bbox.p, nc * in->m, in->m, xl.p, grid->cpos.p,
+                                                       dmax.p);
     const int pblocks = (int)std::min<int64_t>(ng, 148 * 64);
+    const float slack_base = (float)(2.0 * in->r_list + 1e-3);
     const double r2 = in->r_list * in->r_list;
 #define NBX_PRUNE(MM, GG)                                                                                     \
   k_prune_entries<MM, GG><<<pblocks, PRUNE_WARPS * 32, 0, s>>>(in->group_first.p, in->group_nmem.p, ng,        \
                                                                in->ent_offsets.p, in->ent_j.p, in->ent_delta.p, \
                                                                in->ent_mask.p, xl.p, grid->bbox.p, pos, bx, r2,  \
-                                                               ekeep.p, alive.p)
+                                                               dmax.p, slack_base, ekeep.p, alive.p)
     switch (in->m) {
       case 1: NBX_PRUNE(1, 16); break;
       case 2: NBX_PRUNE(2, 8); break;
@@ -1372,9 +1402,12 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(cudaGetLastError());
   TRY(l->ent_offsets.alloc(ng + 1, s));
   TRY(exclusive_scan_i32(alive.p, l->ent_offsets.p, ng + 1, s));
-  TRY(cudaMemcpyAsync(&h, l->ent_offsets.p + ng, 4, cudaMemcpyDeviceToHost, s));
-  TRY(cudaStreamSynchronize(s));
-  l->n_entries = h;
+  // no host sync: storage sized by the input's entries (an upper bound), the
+  // live count stays on the device (ent_offsets[n_groups]); unused j slots
+  // hold n_clusters so that they sort last in the force-layout transposes
+  (void)h;
+  l->n_entries = ne;
+  l->entries_exact = (ne == 0);
   TRY(l->group_first.alloc(ng, s));
   TRY(l->group_nmem.alloc(ng, s));
   TRY(l->ent_j.alloc(l->n_entries, s));
@@ -1382,6 +1415,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(l->ent_mask.alloc(l->n_entries * W, s));
   TRY(l->ent_pres.alloc(l->n_entries, s));
   TRY(l->ent_jorder.alloc(l->n_entries, s));
+  if (ne) count_launch(), k_fill_i32<<<nb(ne, 256), 256, 0, s>>>(l->ent_j.p, ne, (int32_t)nc);
   if (ng) {
     TRY(cudaMemcpyAsync(l->group_first.p, in->group_first.p, 4 * ng, cudaMemcpyDeviceToDevice, s));
     TRY(cudaMemcpyAsync(l->group_nmem.p, in->group_nmem.p, 4 * ng, cudaMemcpyDeviceToDevice, s));
@@ -1392,11 +1426,11 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   }
   TRY(cudaGetLastError());
   l->entries_ordered = true;
-  alive.release(s); xl.release(s); ekeep.release(s);
+  alive.release(s); xl.release(s); ekeep.release(s); dmax.release(s);
   *out = l;
   return NBX_OK;
 fail:
-  alive.release(s); xl.release(s); ekeep.release(s);
+  alive.release(s); xl.release(s); ekeep.release(s); dmax.release(s);
   nbx_list_free(l);
   return NBX_ERR_CUDA;
 }
@@ -1410,7 +1444,28 @@ extern "C" int nbx_list_info(const nbx_list_t* l, int64_t out[5]) {
   out[1] = l->rows_ready ? l->n_rows : -1;  // canonical rows: nbx_list_rows
   out[2] = l->m;
   out[3] = l->n_groups;
-  out[4] = l->n_entries;
+  out[4] = l->entries_exact ? (l->n_live >= 0 ? l->n_live : l->n_entries) : -1;  // -1: nbx_list_entries
+  return NBX_OK;
+}
+
+extern "C" int nbx_list_entries(nbx_list_t* l, void* stream, int64_t* n_entries) {
+  if (!l || !n_entries) {
+    set_error("nbx_list_entries: null argument");
+    return NBX_ERR_PARAM;
+  }
+  if (!l->entries_exact) {  // live entry count of a pruned list (kept on the device until asked for)
+    int32_t h = 0;
+    cudaStream_t s = to_stream(stream);
+    cudaError_t e = cudaMemcpyAsync(&h, l->ent_offsets.p + l->n_groups, 4, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) {
+      set_error("nbx_list_entries: %s", cudaGetErrorString(e));
+      return NBX_ERR_CUDA;
+    }
+    l->n_live = h;
+    l->entries_exact = true;
+  }
+  *n_entries = l->n_live >= 0 ? l->n_live : l->n_entries;
   return NBX_OK;
 }
 

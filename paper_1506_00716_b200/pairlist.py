@@ -40,7 +40,7 @@ class ClusterPairList:
         self.grid = grid
         info = np.zeros(5, dtype=np.int64)
         _lib.check(_lib.load().nbx_list_info(handle, _lib.ptr(info)), "list_info")
-        self._n_i, self._n_rows, self.m, self.n_groups, self.n_entries = (int(v) for v in info)
+        self._n_i, self._n_rows, self.m, self.n_groups, self._n_entries = (int(v) for v in info)
         self.r_list = float(r_list)
         self.n_lane = n_lane
         self.build_step = build_step
@@ -62,6 +62,15 @@ class ClusterPairList:
     @property
     def n_i_clusters(self) -> int:
         return self._n_i
+
+    @property
+    def n_entries(self) -> int:
+        """Live (group, j-cluster) entries of the grouped force layout."""
+        if self._n_entries < 0:  # a pruned list's count stays on the device until asked for
+            n = ctypes.c_int64()
+            _lib.check(_lib.load().nbx_list_entries(self._h, dev.stream(), ctypes.byref(n)), "list_entries")
+            self._n_entries = int(n.value)
+        return self._n_entries
 
     @property
     def n_pairs(self) -> int:
@@ -219,7 +228,7 @@ def prune_pair_list(plist: ClusterPairList, positions, box: SimBox) -> ClusterPa
     if shape != (plist.grid.n_slots, 3):
         raise ParameterError(f"positions shape {shape} does not match the list's slot layout "
                              f"{(plist.grid.n_slots, 3)}")
-    if plist.n_entries == 0:
+    if plist._n_entries == 0:  # (-1: pruned list, count on the device -- never empty)
         return plist
     p, keep_alive = _positions_ptr(plist, positions)
     h = ctypes.c_void_p()
