@@ -686,11 +686,24 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
   const int sidx = lane / m, b = lane - sidx * m;
   double fx = 0.0, fy = 0.0, fz = 0.0;
   const int32_t t1 = t_first[c + 1];
-  for (int32_t t = t_first[c] + sidx; t < t1; t += S) {
-    const float4 pj = __ldg(part_j + (int64_t)__ldg(t_items + t) * m + b);
-    fx += pj.x;
-    fy += pj.y;
-    fz += pj.z;
+  // U transposed items per lane in flight (index loads, then partial loads);
+  // the summation order is unchanged (ascending t per lane)
+  constexpr int U = 4;
+  for (int32_t t0 = t_first[c] + sidx; t0 < t1; t0 += S * U) {
+    int32_t it[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) it[u] = t0 + u * S < t1 ? __ldg(t_items + t0 + u * S) : -1;
+    float4 pj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      pj[u] = it[u] >= 0 ? __ldg(part_j + (int64_t)it[u] * m + b) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (it[u] < 0) break;
+      fx += pj[u].x;
+      fy += pj[u].y;
+      fz += pj[u].z;
+    }
   }
   for (int o = 16; o >= m; o >>= 1) {
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
