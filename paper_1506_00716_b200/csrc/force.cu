@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -62,6 +64,7 @@ struct ForceArgs {
   float rc2, k2rf, krf, crf, coul;
   float beta, beta3, ew_shift, ew_a;
   float ew_f[16], ew_v[16];         // EW_DEG + 1 (<= 16) coefficients, highest first
+  float ew_s[16];                   // -beta^3 * ew_f (k_force_h)
   float slack_base;           // 2 r_c + margin; unsafe if slack < base + 4 d_max
   float band;
   float L[3], invL[3];
@@ -109,11 +112,22 @@ __host__ __device__ constexpr uint64_t column_bits() {
 // with rinv, so they are masked through qm = inc ? qq : 0.
 // degree 10 for the force term (force rel-RMS ~5e-6 vs FP64 on SPC water,
 // tolerance 1e-4), 12 for the energy term (~2e-8, tolerance 1e-5)
+#ifndef NBX_EW_ESTRIN
+#define NBX_EW_ESTRIN 0
+#endif
 #ifndef NBX_EW_DEG_F
 #define NBX_EW_DEG_F 10
 #endif
 constexpr int EW_DEG_F = NBX_EW_DEG_F;
 constexpr int EW_DEG_V = 12;
+
+// bits a*M + {0, 1}, a < M: one member's i-atoms against a lane's two j-atoms
+template <int M>
+__host__ __device__ constexpr uint64_t pair_column_bits() {
+  uint64_t c = 0;
+  for (int a = 0; a < M; ++a) c |= 3ull << (a * M);
+  return c;
+}
 
 // One pair: F/r, plus energies when requested.  `inc` zeroes rinv, which
 // masks every force term; energy shift terms are masked explicitly.
@@ -641,6 +655,526 @@ k_force(const ForceArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_force_h: the grouped kernel with TWO j-atoms per lane (m = 4, 8).
+//
+// Lane (ih, r, jp) = (half, entry slot r of R = 32/m, j-atom pair jp of m/2)
+// holds two j-atoms of entry r in registers and sweeps i-atom PAIRS from
+// shared memory: half ih owns pairs pp < m/4 starting at atom 2 ih (m/4) of
+// EVERY member, so the warp-uniform member branches skip exactly what
+// k_force skips.  Against k_force (one j-atom per lane over all 16 i-atoms)
+// every i-atom pair loaded from shared memory serves two j-atoms, the i-force
+// accumulators halve, and the entry fields are staged once per entry rather
+// than once per lane.  The lane's "a" j-atom is 2jp + ih and its "b" j-atom
+// 2jp + 1 - ih, so after one shuffle per component (the partner half's
+// partial of a) each lane owns the full force on its a-atom: one store per
+// (entry, j-atom), k_reduce unchanged.
+//
+// Sign convention: d = x_j - x_i (i-atoms are staged negated), so the j-force
+// fscal d accumulates with no negation and the i-accumulators hold -F_i,
+// negated once per group.  Masked or out-of-range pairs get r^2 = +inf
+// before the rsqrt (rinv = 0, hence every force term 0).  Ewald force term:
+//   F/r = rinv2 (flj + qq (rinv + r2 Gs(u))),  Gs = -beta^3 Gf.
+// Per-warp staging, one CHUNK of CH = 128/m entries at a time: entry fields
+// in a 3-slot ring (staged two chunks ahead), j-atoms in a 2-slot ring (one
+// chunk ahead), stored [q][entry][m/2] so that a lane's a/b atoms of one
+// iteration are read conflict-free.
+template <int M, int W>
+struct StageH {
+  static constexpr int CH = 128 / M;
+  float4 ed[3][CH];
+  uint64_t em[3][CH][W];
+  int32_t cj[3][CH];
+  float4 xj[2][128];
+  int32_t tj[2][128];
+};
+
+// admit = mask bit set and r2 <= rc2; returns r2 or +inf (rinv = 0)
+__device__ __forceinline__ float admit_r2(float r2, float rc2, uint64_t mw, int p) {
+  float out;
+  const uint32_t word = p < 32 ? (uint32_t)mw : (uint32_t)(mw >> 32);
+  const uint32_t bit = 1u << (p & 31);
+  asm("{\n\t.reg .pred pm, pc;\n\t"
+      "setp.ne.b32 pm, %3, 0;\n\t"
+      "setp.le.and.ftz.f32 pc, %1, %2, pm;\n\t"
+      "selp.f32 %0, %1, 0f7F800000, pc;\n\t}"
+      : "=f"(out)
+      : "f"(r2), "f"(rc2), "r"(word & bit));
+  return out;
+}
+
+template <bool MI>
+__device__ __forceinline__ float2 geom2(const ForceArgs& A, const float4& xy, const float4& zq, const float4& xj,
+                                        float2& dx, float2& dy, float2& dz) {
+  dx = __fadd2_rn(make_float2(xy.x, xy.y), bc2(xj.x));
+  dy = __fadd2_rn(make_float2(xy.z, xy.w), bc2(xj.y));
+  dz = __fadd2_rn(make_float2(zq.x, zq.y), bc2(xj.z));
+  if (MI) {
+    dx.x = fmaf(-A.L[0], rintf(dx.x * A.invL[0]), dx.x);
+    dx.y = fmaf(-A.L[0], rintf(dx.y * A.invL[0]), dx.y);
+    dy.x = fmaf(-A.L[1], rintf(dy.x * A.invL[1]), dy.x);
+    dy.y = fmaf(-A.L[1], rintf(dy.y * A.invL[1]), dy.y);
+    dz.x = fmaf(-A.L[2], rintf(dz.x * A.invL[2]), dz.x);
+    dz.y = fmaf(-A.L[2], rintf(dz.y * A.invL[2]), dz.y);
+  }
+  return __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+}
+
+// F/r (and energies) of one i-atom pair against one j-atom; inc0/inc1 are
+// the admitted-and-within-r_c decisions.
+template <int ELEC, bool KRF, bool ENERGY>
+__device__ __forceinline__ float2 pair2_eval(const ForceArgs& A, const float4& zq, const float4& l2, float qj,
+                                             float2 r2, float2 r2m, const float2& sh, float2& elj, float2& ec) {
+  // r2m = r2 where admitted and within r_c, +inf elsewhere
+  const float inf = __int_as_float(0x7f800000);
+  const bool inc0 = r2m.x != inf, inc1 = r2m.y != inf;
+  float2 rinv = make_float2(rsqrtf(r2m.x), rsqrtf(r2m.y));
+  const float2 rinv2 = __fmul2_rn(rinv, rinv);
+  const float2 rinv6 = __fmul2_rn(__fmul2_rn(rinv2, rinv2), rinv2);
+  const float2 c6n = make_float2(l2.x, l2.y), c12 = make_float2(l2.z, l2.w);
+  const float2 flj = __fmul2_rn(rinv6, __ffma2_rn(c12, rinv6, c6n));  // 12 c12/r^12 - 6 c6/r^6
+  const float2 qq = __fmul2_rn(make_float2(zq.z, zq.w), bc2(qj));
+  float2 fscal;
+  if (ELEC == FE_RF) {
+    fscal = __fmul2_rn(__ffma2_rn(qq, rinv, flj), rinv2);
+    if (KRF || ENERGY) {
+      const float2 qm = make_float2(inc0 ? qq.x : 0.f, inc1 ? qq.y : 0.f);
+      if (KRF) fscal = __ffma2_rn(qm, bc2(-A.k2rf), fscal);
+      if (ENERGY)
+        ec = __fadd2_rn(ec, __ffma2_rn(qm, __ffma2_rn(bc2(A.krf), r2, bc2(-A.crf)), __fmul2_rn(qq, rinv)));
+    }
+  } else {
+    const float2 u = __ffma2_rn(r2, bc2(A.ew_a), bc2(-1.f));
+    float2 gs;
+#if NBX_EW_ESTRIN
+    static_assert(EW_DEG_F == 10, "Estrin scheme written for degree 10");
+    {  // depth 4 instead of 10 (a_i = ew_s[10 - i])
+      const float* c = A.ew_s;
+      const float2 u2 = __fmul2_rn(u, u), u4 = __fmul2_rn(u2, u2), u8 = __fmul2_rn(u4, u4);
+      const float2 b0 = __ffma2_rn(bc2(c[9]), u, bc2(c[10])), b1 = __ffma2_rn(bc2(c[7]), u, bc2(c[8]));
+      const float2 b2 = __ffma2_rn(bc2(c[5]), u, bc2(c[6])), b3 = __ffma2_rn(bc2(c[3]), u, bc2(c[4]));
+      const float2 b4 = __ffma2_rn(bc2(c[1]), u, bc2(c[2]));
+      const float2 c0 = __ffma2_rn(b1, u2, b0), c1 = __ffma2_rn(b3, u2, b2), c2 = __ffma2_rn(bc2(c[0]), u2, b4);
+      gs = __ffma2_rn(c2, u8, __ffma2_rn(c1, u4, c0));
+    }
+#else
+    gs = bc2(A.ew_s[0]);
+#pragma unroll
+    for (int k = 1; k <= EW_DEG_F; ++k) gs = __ffma2_rn(gs, u, bc2(A.ew_s[k]));
+#endif
+    const float2 sc = __ffma2_rn(r2, gs, rinv);
+    fscal = __fmul2_rn(__ffma2_rn(qq, sc, flj), rinv2);
+    if (ENERGY) {
+      const float2 qm = make_float2(inc0 ? qq.x : 0.f, inc1 ? qq.y : 0.f);
+      float2 gv = bc2(A.ew_v[0]);
+#pragma unroll
+      for (int k = 1; k <= EW_DEG_V; ++k) gv = __ffma2_rn(gv, u, bc2(A.ew_v[k]));
+      ec = __ffma2_rn(qm, __fadd2_rn(rinv, __ffma2_rn(bc2(-A.beta), gv, bc2(-A.ew_shift))), ec);
+    }
+  }
+  if (ENERGY) {
+    const float2 shm = make_float2(inc0 ? -sh.x : 0.f, inc1 ? -sh.y : 0.f);
+    const float2 e6 =
+        __fmul2_rn(rinv6, __ffma2_rn(__fmul2_rn(c12, bc2(1.f / 12.f)), rinv6, __fmul2_rn(c6n, bc2(1.f / 6.f))));
+    elj = __fadd2_rn(elj, __fadd2_rn(e6, shm));
+  }
+  return fscal;
+}
+
+// Bits of the lane mask words: member k at k*MB, atom s of the lane's pair
+// pp at (2 pp + s) * M (one j-atom per word: ma for a, mb for b).
+template <int M>
+__host__ __device__ constexpr int member_stride_bits() { return M == 4 ? 16 : 32; }
+
+template <int M, int ELEC, bool KRF, bool ENERGY, bool BAND, bool MI>
+__device__ __forceinline__ void sweep_h(const ForceArgs& A, const float4* __restrict__ s_xy,
+                                        const float4* __restrict__ s_zq, const float4* __restrict__ s_l2a,
+                                        const float4* __restrict__ s_l2b, const float2* __restrict__ s_sha,
+                                        const float2* __restrict__ s_shb, uint64_t ma, uint64_t mb, unsigned wpres,
+                                        int ih, const float4& xa, const float4& xb, float2 (&fi)[4][3],
+                                        float2 (&fa)[3], float2 (&fb)[3], float2& elj, float2& ec, uint32_t& near) {
+  constexpr int G = 16 / M, PP = M / 4, MB = member_stride_bits<M>();
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    if (!((wpres >> k) & 1u)) continue;
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      const int hl = k * PP + pp;
+      const int h = k * (M / 2) + ih * PP + pp;
+      const int p0 = k * MB + (2 * pp) * M, p1 = p0 + M;
+      const float4 xy = s_xy[h], zq = s_zq[h];
+      const float4 la = s_l2a[h], lb = s_l2b[h];
+      float2 sha = bc2(0.f), shb = bc2(0.f);
+      if (ENERGY) {
+        sha = s_sha[h];
+        shb = s_shb[h];
+      }
+      float2 dxa, dya, dza, dxb, dyb, dzb;
+      const float2 r2a = geom2<MI>(A, xy, zq, xa, dxa, dya, dza);
+      const float2 r2b = geom2<MI>(A, xy, zq, xb, dxb, dyb, dzb);
+      const float2 r2ma = make_float2(admit_r2(r2a.x, A.rc2, ma, p0), admit_r2(r2a.y, A.rc2, ma, p1));
+      const float2 r2mb = make_float2(admit_r2(r2b.x, A.rc2, mb, p0), admit_r2(r2b.y, A.rc2, mb, p1));
+      if (BAND) {
+        const bool ma0 = (ma >> p0) & 1ull, ma1 = (ma >> p1) & 1ull;
+        const bool mb0 = (mb >> p0) & 1ull, mb1 = (mb >> p1) & 1ull;
+        near |= (ma0 && fabsf(r2a.x - A.rc2) < A.band) ? (1u << (4 * hl + 0)) : 0u;
+        near |= (ma1 && fabsf(r2a.y - A.rc2) < A.band) ? (1u << (4 * hl + 2)) : 0u;
+        near |= (mb0 && fabsf(r2b.x - A.rc2) < A.band) ? (1u << (4 * hl + 1)) : 0u;
+        near |= (mb1 && fabsf(r2b.y - A.rc2) < A.band) ? (1u << (4 * hl + 3)) : 0u;
+      }
+      const float2 fsa = pair2_eval<ELEC, KRF, ENERGY>(A, zq, la, xa.w, r2a, r2ma, sha, elj, ec);
+      const float2 fsb = pair2_eval<ELEC, KRF, ENERGY>(A, zq, lb, xb.w, r2b, r2mb, shb, elj, ec);
+      fi[hl][0] = __ffma2_rn(fsa, dxa, fi[hl][0]);
+      fi[hl][1] = __ffma2_rn(fsa, dya, fi[hl][1]);
+      fi[hl][2] = __ffma2_rn(fsa, dza, fi[hl][2]);
+      fa[0] = __ffma2_rn(fsa, dxa, fa[0]);
+      fa[1] = __ffma2_rn(fsa, dya, fa[1]);
+      fa[2] = __ffma2_rn(fsa, dza, fa[2]);
+      fi[hl][0] = __ffma2_rn(fsb, dxb, fi[hl][0]);
+      fi[hl][1] = __ffma2_rn(fsb, dyb, fi[hl][1]);
+      fi[hl][2] = __ffma2_rn(fsb, dzb, fi[hl][2]);
+      fb[0] = __ffma2_rn(fsb, dxb, fb[0]);
+      fb[1] = __ffma2_rn(fsb, dyb, fb[1]);
+      fb[2] = __ffma2_rn(fsb, dzb, fb[2]);
+    }
+  }
+}
+
+// group i-atom of the lane's pair hl (s = 0, 1)
+template <int M>
+__device__ __forceinline__ int lane_atom(int hl, int s, int ih) {
+  constexpr int PP = M / 4;
+  const int k = hl / PP, pp = hl - k * PP;
+  return 2 * (k * (M / 2) + ih * PP + pp) + s;
+}
+
+// Band fixes for the two j-atoms of a lane: near bit 4hl + 2s + q = (atom s
+// of the lane's pair hl, j-atom q: 0 = a, 1 = b).  Corrections go to the
+// j-force sums fj[q] (+F on j) and, through shared-memory atomics, to the
+// i-atoms (+F on i).
+template <int M, int ELEC, bool KRF, bool ENERGY, bool MI>
+__device__ __forceinline__ void band_fix_h(const ForceArgs& A, const float4* __restrict__ s_xi,
+                                           const float4* __restrict__ s_lj, float* s_corr, uint32_t near,
+                                           const float4 (&xj)[2], const int (&tj)[2], const int (&bj)[2], int ih,
+                                           int32_t first, int32_t cj, float (&fj)[2][3], float& elj, float& ec) {
+  while (near) {
+    const int bit = __ffs(near) - 1;
+    near &= near - 1;
+    const int hl = bit >> 2, s = (bit >> 1) & 1, q = bit & 1;
+    const int ia = lane_atom<M>(hl, s, ih);
+    const int b = bj[q];
+    const float4 xi = s_xi[ia];
+    float dx, dy, dz;
+    const float r2 = pair_geom<MI>(A, xi, xj[q], dx, dy, dz);
+    const bool inc32 = r2 <= A.rc2;
+    const int ex = exact_inside(A, (int64_t)first * M + ia, (int64_t)cj * M + b);
+    if (ex < 0) record_bad(A.scalars, (int64_t)first * M + ia, (int64_t)cj * M + b);
+    const bool inc64 = ex > 0;
+    if (inc64 == inc32) continue;
+    float pe_lj = 0.f, pe_c = 0.f;
+    const float fscal = pair_eval<ELEC, KRF, ENERGY>(A, xi, s_lj[tj[q] * 16 + ia], xj[q].w, r2, true, pe_lj, pe_c);
+    const float sg = inc64 ? 1.f : -1.f;
+    atomicAdd(&s_corr[3 * ia + 0], sg * fscal * dx);
+    atomicAdd(&s_corr[3 * ia + 1], sg * fscal * dy);
+    atomicAdd(&s_corr[3 * ia + 2], sg * fscal * dz);
+    fj[q][0] -= sg * fscal * dx;
+    fj[q][1] -= sg * fscal * dy;
+    fj[q][2] -= sg * fscal * dz;
+    if (ENERGY) {
+      elj += sg * pe_lj;
+      ec += sg * pe_c;
+    }
+  }
+}
+
+#ifndef NBX_FORCEH_MINB
+#define NBX_FORCEH_MINB 4
+#endif
+constexpr int LJS = 9;  // row stride (float4 / float2) of the per-type LJ tables: no bank conflicts between types
+
+template <int M, int ELEC, bool KRF, bool ENERGY, bool BAND>
+__global__ void __launch_bounds__(FW * 32, NBX_FORCEH_MINB)
+k_force_h(const ForceArgs A) {
+  constexpr int G = 16 / M;
+  constexpr int R = 32 / M;   // entries per iteration
+  constexpr int IA = 16;      // i-atoms per group
+  constexpr int H = 8;        // i-atom pairs per group
+  constexpr int JP = M / 2;   // j-atom pairs per entry
+  constexpr int W = (G * M * M > 64) ? 2 : 1;
+  // dynamic: [FW][nt][LJS] float4 pair-interleaved LJ, [FW][nt][LJS] float2
+  // shifts, then (BAND) [FW][nt][IA] float4 scalar LJ
+  extern __shared__ float4 s_dyn[];
+  __shared__ float4 s_xi[FW][IA];
+  __shared__ float4 s_xy[FW][H];
+  __shared__ float4 s_zq[FW][H];
+  union Scratch {
+    StageH<M, W> st;
+    float red[32][25];
+  };
+  constexpr int CH = StageH<M, W>::CH;  // entries per chunk
+  constexpr int CJ = CH * JP;           // staged atoms per q plane
+  __shared__ Scratch s_ws[FW];
+  __shared__ float s_corr[FW][BAND ? IA * 3 : 1];
+
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ih = lane >> 4, r = (lane & 15) / JP, jp = (lane & 15) % JP;
+  const int ba = 2 * jp + ih, bb = 2 * jp + 1 - ih;  // this lane's a and b j-atoms
+  const size_t tn = (size_t)LJS * A.nt;
+  float4* s_l2 = s_dyn + (size_t)w * tn;
+  float2* s_sh = reinterpret_cast<float2*>(s_dyn + (size_t)FW * tn) + (size_t)w * tn;
+  float4* s_lj = s_dyn + (size_t)FW * tn + (FW * tn + 1) / 2 + (size_t)w * IA * A.nt;
+  StageH<M, W>& S = s_ws[w].st;
+
+  for (;;) {
+    int64_t wi = 0;
+    if (lane == 0) wi = (int64_t)atomicAdd(A.scalars + 4, 1u);
+    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if (wi >= A.n_work) break;
+    const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
+    const int32_t first = A.grp_first[g];
+    const int nmem = A.grp_nmem[g];
+    const int32_t e_beg = A.ent_off[g], e_end = A.ent_off[g + 1];
+    const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
+
+    // chunk staging: entry fields of chunk c (lanes < CH), j-atoms of chunk
+    // c (4 per lane, flat index f = u*32 + lane -> plane q, entry, pair)
+    auto stage_entries = [&](int slot, int32_t ec0) {
+      if (lane < CH) {
+        const int32_t e = min(ec0 + lane, e_last);
+        cp_async(&S.ed[slot][lane], A.ent_delta + e, 16);
+#pragma unroll
+        for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], A.ent_mask + (int64_t)e * W + q, 8);
+        cp_async(&S.cj[slot][lane], A.ent_j + e, 4);
+      }
+    };
+    auto stage_jatoms = [&](int xslot, int eslot) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = u * 32 + lane, q = f / CJ, rem = f - q * CJ;
+        const int ent = rem / JP, b = 2 * (rem - ent * JP) + q;
+        const int64_t src = (int64_t)S.cj[eslot][ent] * M + b;
+        cp_async(&S.xj[xslot][f], A.xyzq + src, 16);
+        cp_async(&S.tj[xslot][f], A.type + src, 4);
+      }
+    };
+    if (e_end > e_beg) {
+      stage_entries(0, e_beg);
+      stage_entries(1, e_beg + CH);
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncwarp();
+      stage_jatoms(0, 0);
+      cp_async_commit();
+    }
+
+    // the group's i-atoms: group frame (s_xi, band fixes), negated and
+    // pair-interleaved (s_xy, s_zq; charges positive), LJ rows per j-type
+    for (int ia = lane; ia < IA; ia += 32) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ia < nmem * M) {
+        v = A.xyzq[(int64_t)first * M + ia];
+        const int64_t c = first + ia / M;
+        v.x = (float)((A.bbox[6 * c + 0] - A.bbox[6 * (int64_t)first + 0]) + (double)v.x);
+        v.y = (float)((A.bbox[6 * c + 1] - A.bbox[6 * (int64_t)first + 1]) + (double)v.y);
+        v.z = (float)((A.bbox[6 * c + 2] - A.bbox[6 * (int64_t)first + 2]) + (double)v.z);
+        v.w *= A.coul;
+      }
+      s_xi[w][ia] = v;
+      float* xyf = reinterpret_cast<float*>(&s_xy[w][0]);
+      float* zqf = reinterpret_cast<float*>(&s_zq[w][0]);
+      const int h = ia >> 1, o = ia & 1;
+      xyf[4 * h + o] = -v.x;
+      xyf[4 * h + 2 + o] = -v.y;
+      zqf[4 * h + o] = -v.z;
+      zqf[4 * h + 2 + o] = v.w;
+    }
+    for (int idx = lane; idx < H * A.nt; idx += 32) {
+      const int t = idx / H, h = idx - t * H;
+      const int ti0 = 2 * h < nmem * M ? A.type[(int64_t)first * M + 2 * h] : 0;
+      const int ti1 = 2 * h + 1 < nmem * M ? A.type[(int64_t)first * M + 2 * h + 1] : 0;
+      const float4 a0 = __ldg(&A.lj[ti0 * A.nt + t]), a1 = __ldg(&A.lj[ti1 * A.nt + t]);
+      s_l2[t * LJS + h] = make_float4(-a0.x, -a1.x, a0.y, a1.y);
+      s_sh[t * LJS + h] = make_float2(a0.z, a1.z);
+    }
+    if (BAND) {
+      for (int idx = lane; idx < IA * A.nt; idx += 32) {
+        const int t = idx / IA, ia = idx - t * IA;
+        const int ti = ia < nmem * M ? A.type[(int64_t)first * M + ia] : 0;
+        s_lj[idx] = __ldg(&A.lj[ti * A.nt + t]);
+      }
+      for (int c = lane; c < IA * 3; c += 32) s_corr[w][c] = 0.f;
+    }
+    __syncwarp();
+
+    const float slack_thr = A.slack_base + 4.f * __uint_as_float(A.scalars[0]);
+    float2 fi[4][3];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) fi[h][0] = fi[h][1] = fi[h][2] = make_float2(0.f, 0.f);
+    double elj_acc = 0.0, ec_acc = 0.0;
+    float4* pj = A.part_j + (int64_t)(e_beg + r) * M + ba;
+    const int sha_ = 8 * ih * (W == 1) + 32 * ih * (W == 2) + 2 * jp;  // mask shift of the lane's pairs
+
+    int es = 0;
+    for (int32_t ec0 = e_beg, c = 0; ec0 < e_end; ec0 += CH, ++c) {
+      // chunk c's entries and j-atoms have landed; stage chunk c+1's
+      // j-atoms and chunk c+2's entries
+      cp_async_wait_all();
+      __syncwarp();
+      const int xs = c & 1;
+      {
+        const int es1 = es == 2 ? 0 : es + 1, es2 = es1 == 2 ? 0 : es1 + 1;
+        if (ec0 + CH < e_end) stage_jatoms(xs ^ 1, es1);
+        if (ec0 + 2 * CH < e_end) stage_entries(es2, ec0 + 2 * CH);
+        cp_async_commit();
+      }
+      const float4* c_ed = S.ed[es];
+      const uint64_t* c_em = &S.em[es][0][0];
+      const int32_t* c_cj = S.cj[es];
+      const float4* c_xa = &S.xj[xs][ih * CJ];
+      const float4* c_xb = &S.xj[xs][(1 - ih) * CJ];
+      const int32_t* c_ta = &S.tj[xs][ih * CJ];
+      const int32_t* c_tb = &S.tj[xs][(1 - ih) * CJ];
+      es = es == 2 ? 0 : es + 1;
+      const int32_t c_end = min(ec0 + CH, e_end);
+#pragma unroll 1
+    for (int32_t e0 = ec0, ci = 0; e0 < c_end; e0 += R, ci += R, pj += R * M) {
+      const bool valid = e0 + r < e_end;
+      const int ce = ci + r;  // entry within the chunk
+      const float4 d = c_ed[ce];
+      uint64_t ma, mb;
+      unsigned wpres = 0;
+      if constexpr (W == 2) {
+        const uint64_t w0 = valid ? c_em[ce * 2] : 0ull, w1 = valid ? c_em[ce * 2 + 1] : 0ull;
+        const uint32_t a0 = (uint32_t)(w0 >> (sha_ + ih)), a1 = (uint32_t)(w1 >> (sha_ + ih));
+        const uint32_t b0 = (uint32_t)(w0 >> (sha_ + 1 - ih)), b1 = (uint32_t)(w1 >> (sha_ + 1 - ih));
+        ma = (uint64_t)a0 | ((uint64_t)a1 << 32);
+        mb = (uint64_t)b0 | ((uint64_t)b1 << 32);
+        // member presence over the iteration's entries (uniform datapath)
+        const unsigned p0 = __reduce_or_sync(0xffffffffu, (uint32_t)w0 | (uint32_t)(w0 >> 32));
+        const unsigned p1 = __reduce_or_sync(0xffffffffu, (uint32_t)w1 | (uint32_t)(w1 >> 32));
+        wpres = (p0 ? 1u : 0u) | (p1 ? 2u : 0u);
+      } else {
+        const uint64_t w0 = valid ? c_em[ce] : 0ull;
+        ma = w0 >> (sha_ + ih);
+        mb = w0 >> (sha_ + 1 - ih);
+        const unsigned lo = __reduce_or_sync(0xffffffffu, (uint32_t)w0);
+        const unsigned hi = __reduce_or_sync(0xffffffffu, (uint32_t)(w0 >> 32));
+        wpres = ((lo & 0xffffu) ? 1u : 0u) | ((lo >> 16) ? 2u : 0u) | ((hi & 0xffffu) ? 4u : 0u) |
+                ((hi >> 16) ? 8u : 0u);
+      }
+      const int32_t cj = BAND ? c_cj[ce] : 0;
+      const int xo = ci * JP + (lane & 15);  // = (ci + r) * JP + jp
+      float4 xj[2];
+      int tj[2];
+      xj[0] = c_xa[xo];
+      xj[1] = c_xb[xo];
+      tj[0] = c_ta[xo];
+      tj[1] = c_tb[xo];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        xj[q].x += d.x;
+        xj[q].y += d.y;
+        xj[q].z += d.z;
+      }
+      const bool wunsafe = __any_sync(0xffffffffu, valid && d.w < slack_thr);
+      float2 fa[3], fb[3];
+      fa[0] = fa[1] = fa[2] = fb[0] = fb[1] = fb[2] = make_float2(0.f, 0.f);
+      float2 el2 = make_float2(0.f, 0.f), ec2 = el2;
+      uint32_t near = 0;
+      const float4* la = s_l2 + tj[0] * LJS;
+      const float4* lb = s_l2 + tj[1] * LJS;
+      const float2* sa = s_sh + tj[0] * LJS;
+      const float2* sbp = s_sh + tj[1] * LJS;
+      if (!wunsafe)
+        sweep_h<M, ELEC, KRF, ENERGY, BAND, false>(A, s_xy[w], s_zq[w], la, lb, sa, sbp, ma, mb, wpres, ih, xj[0],
+                                                   xj[1], fi, fa, fb, el2, ec2, near);
+      else
+        sweep_h<M, ELEC, KRF, ENERGY, BAND, true>(A, s_xy[w], s_zq[w], la, lb, sa, sbp, ma, mb, wpres, ih, xj[0],
+                                                  xj[1], fi, fa, fb, el2, ec2, near);
+      float fj[2][3] = {{fa[0].x + fa[0].y, fa[1].x + fa[1].y, fa[2].x + fa[2].y},
+                        {fb[0].x + fb[0].y, fb[1].x + fb[1].y, fb[2].x + fb[2].y}};
+      float elj = 0.f, ec = 0.f;
+      if (ENERGY) {
+        elj = el2.x + el2.y;
+        ec = ec2.x + ec2.y;
+      }
+      if (BAND && __any_sync(0xffffffffu, near != 0)) {
+        if (near) {
+          const int bj[2] = {ba, bb};
+          if (!wunsafe)
+            band_fix_h<M, ELEC, KRF, ENERGY, false>(A, s_xi[w], s_lj, s_corr[w], near, xj, tj, bj, ih, first, cj, fj,
+                                                    elj, ec);
+          else
+            band_fix_h<M, ELEC, KRF, ENERGY, true>(A, s_xi[w], s_lj, s_corr[w], near, xj, tj, bj, ih, first, cj, fj,
+                                                   elj, ec);
+        }
+        __syncwarp();
+      }
+      // the partner half's b-atom is this lane's a-atom
+      float out[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[c] = fj[0][c] + __shfl_xor_sync(0xffffffffu, fj[1][c], 16);
+      if (valid) *pj = make_float4(out[0], out[1], out[2], 0.f);
+      if (ENERGY) {
+        elj_acc += (double)elj;
+        ec_acc += (double)ec;
+      }
+    }
+    }
+
+    cp_async_wait_all();
+    __syncwarp();
+
+    // i-forces: lane holds -F of atoms lane_atom(hl, s, ih) at t = 2 hl + s;
+    // sum over the 16 lanes of each half in a fixed order
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s_ws[w].red[lane][3 * (2 * h) + c] = fi[h][c].x;
+        s_ws[w].red[lane][3 * (2 * h + 1) + c] = fi[h][c].y;
+      }
+    __syncwarp();
+    float acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int o = lane + 32 * u;  // output o = 3 ia + c
+      acc[u] = 0.f;
+      if (o < IA * 3) {
+        const int ia = o / 3, c = o - 3 * ia;
+        const int h = ia >> 1, km = h / (M / 2), wm = h - km * (M / 2);
+        const int hf = wm / (M / 4), t = 2 * (km * (M / 4) + wm % (M / 4)) + (ia & 1);
+        float sacc = 0.f;
+#pragma unroll 4
+        for (int l = 0; l < 16; ++l) sacc += s_ws[w].red[16 * hf + l][3 * t + c];
+        acc[u] = BAND ? s_corr[w][o] - sacc : -sacc;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int o = lane + 32 * u;
+      if (o < IA * 3) s_ws[w].red[0][o] = acc[u];
+    }
+    __syncwarp();
+    if (lane < nmem * M) {
+      A.part_i[(int64_t)first * M + lane] =
+          make_float4(s_ws[w].red[0][3 * lane], s_ws[w].red[0][3 * lane + 1], s_ws[w].red[0][3 * lane + 2], 0.f);
+    }
+    if (ENERGY) {
+      for (int o = 16; o; o >>= 1) {
+        elj_acc += __shfl_xor_sync(0xffffffffu, elj_acc, o);
+        ec_acc += __shfl_xor_sync(0xffffffffu, ec_acc, o);
+      }
+      if (lane == 0) {
+        A.e_grp[2 * wi] = elj_acc;
+        A.e_grp[2 * wi + 1] = ec_acc;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Gather positions for this evaluation: clustered FP32 coordinates placed in
 // the periodic image nearest to the build-time positions (so build-time shift
 // vectors stay valid), charges, types, and the max displacement since build.
@@ -849,13 +1383,80 @@ static cudaError_t launch_mg(const ForceArgs& A, int elec, bool krf, bool energy
   return energy ? launch_one<M, G, FE_RF, false, true, false>(A, s) : launch_one<M, G, FE_RF, false, false, false>(A, s);
 }
 
+template <int M, int ELEC, bool KRF, bool ENERGY, bool BAND>
+static cudaError_t launch_h(const ForceArgs& A, cudaStream_t s) {
+  constexpr int IA = 16;
+  const size_t tn = (size_t)LJS * A.nt;
+  const size_t dyn = sizeof(float4) * (FW * tn + (FW * tn + 1) / 2 + (BAND ? FW * IA * (size_t)A.nt : 0));
+  auto kern = k_force_h<M, ELEC, KRF, ENERGY, BAND>;
+  static size_t dyn_set = 0;
+  if (dyn > dyn_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    dyn_set = dyn;
+  }
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int dev = 0, n_sm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FW * 32, dyn);
+    max_blocks = n_sm * (per_sm > 0 ? per_sm : 1);
+  }
+  int64_t blocks = (A.n_work + FW - 1) / FW;
+  if (blocks > max_blocks) blocks = max_blocks;
+  if (blocks > 0) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool tm = timing_enabled();
+    if (tm) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+    count_launch();
+    kern<<<(unsigned)blocks, FW * 32, dyn, s>>>(A);
+    if (tm) {
+      cudaEventRecord(e1, s);
+      timing_record(e0, e1);
+    }
+  }
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t launch_mh(const ForceArgs& A, int elec, bool krf, bool energy, bool band, cudaStream_t s) {
+  if (elec == FE_EWALD)
+    return energy ? launch_h<M, FE_EWALD, false, true, false>(A, s) : launch_h<M, FE_EWALD, false, false, false>(A, s);
+  if (krf) {
+    if (band) return energy ? launch_h<M, FE_RF, true, true, true>(A, s) : launch_h<M, FE_RF, true, false, true>(A, s);
+    return energy ? launch_h<M, FE_RF, true, true, false>(A, s) : launch_h<M, FE_RF, true, false, false>(A, s);
+  }
+  if (band) return energy ? launch_h<M, FE_RF, false, true, true>(A, s) : launch_h<M, FE_RF, false, false, true>(A, s);
+  return energy ? launch_h<M, FE_RF, false, true, false>(A, s) : launch_h<M, FE_RF, false, false, false>(A, s);
+}
+
+// NBX_FORCE_KERNEL=legacy selects k_force (one j-atom per lane) for the
+// grouped layout at m = 4, 8 too (A/B measurements)
+static bool use_legacy_force() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NBX_FORCE_KERNEL");
+    v = (e && strcmp(e, "legacy") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static cudaError_t launch_force(int m, bool grouped, const ForceArgs& A, int elec, bool krf, bool energy, bool band,
                                 cudaStream_t s) {
   switch (m) {
     case 1: return grouped ? launch_mg<1, 16>(A, elec, krf, energy, band, s) : launch_mg<1, 1>(A, elec, krf, energy, band, s);
     case 2: return grouped ? launch_mg<2, 8>(A, elec, krf, energy, band, s) : launch_mg<2, 1>(A, elec, krf, energy, band, s);
-    case 4: return grouped ? launch_mg<4, 4>(A, elec, krf, energy, band, s) : launch_mg<4, 1>(A, elec, krf, energy, band, s);
-    default: return grouped ? launch_mg<8, 2>(A, elec, krf, energy, band, s) : launch_mg<8, 1>(A, elec, krf, energy, band, s);
+    case 4:
+      if (grouped && !use_legacy_force()) return launch_mh<4>(A, elec, krf, energy, band, s);
+      return grouped ? launch_mg<4, 4>(A, elec, krf, energy, band, s) : launch_mg<4, 1>(A, elec, krf, energy, band, s);
+    default:
+      if (grouped && !use_legacy_force()) return launch_mh<8>(A, elec, krf, energy, band, s);
+      return grouped ? launch_mg<8, 2>(A, elec, krf, energy, band, s) : launch_mg<8, 1>(A, elec, krf, energy, band, s);
   }
 }
 
@@ -878,7 +1479,8 @@ static double ew_gv(double w) {  // erf(z)/z
   const double z = sqrt(w);
   return erf(z) / z;
 }
-static void ew_fit(double (*f)(double), double wmax, int deg, float* out /* deg+1, highest first */) {
+static void ew_fit(double (*f)(double), double wmax, int deg, float* out /* deg+1, highest first */,
+                   double scale = 1.0) {
   const int N = deg + 1;
   double c[16] = {0};
   for (int k = 0; k < N; ++k) {
@@ -908,7 +1510,7 @@ static void ew_fit(double (*f)(double), double wmax, int deg, float* out /* deg+
       Tcur[i] = Tn[i];
     }
   }
-  for (int i = 0; i <= deg; ++i) out[i] = (float)p[deg - i];
+  for (int i = 0; i <= deg; ++i) out[i] = (float)(scale * p[deg - i]);
 }
 
 // transposed index: items (entries or rows) sorted by j-cluster, stable
@@ -1088,6 +1690,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
       A.ew_a = (float)(2.0 / wmax * p->ewald_beta * p->ewald_beta);
       ew_fit(ew_gf, wmax, EW_DEG_F, A.ew_f);
       ew_fit(ew_gv, wmax, EW_DEG_V, A.ew_v);
+      ew_fit(ew_gf, wmax, EW_DEG_F, A.ew_s, -(double)p->ewald_beta * p->ewald_beta * p->ewald_beta);
     }
     A.slack_base = (float)(2.0 * rc + 1e-3);
     double Lmax = fmax(box[0], fmax(box[1], box[2]));
