@@ -194,9 +194,18 @@ void nbx::ensure_pool() {
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     // pre-grow the pool once (kept: threshold = max) so rebuilds do not map
-    // new pages in the middle of a step
+    // new pages in the middle of a step.  A 1.5M-atom list generation needs
+    // several GB (54 M built rows, 18 M entries + their partial forces); the
+    // default reserve is 24 GB (NBX_POOL_GB), capped at 40 % of free memory.
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    double gb = 24.0;
+    if (const char* e = getenv("NBX_POOL_GB")) gb = atof(e);
+    size_t want = (size_t)(gb * (double)(size_t(1) << 30));
+    if (want > free_b / 10 * 4) want = free_b / 10 * 4;
     void* p = nullptr;
-    if (cudaMallocAsync(&p, size_t(2) << 30, 0) == cudaSuccess) cudaFreeAsync(p, 0);
+    if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
   }
   done_dev = dev;
 }

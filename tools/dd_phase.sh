@@ -1,0 +1,5 @@
+# per-phase DD timing at 1.5M atoms, N = 2 and 4
+for n in 2 4; do
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2954$n tools/dd_breakdown.py 1500000 > gpurun_out/ddb_n$n.log 2>&1
+  grep "N=" gpurun_out/ddb_n$n.log
+done
