@@ -181,16 +181,26 @@ namespace nbx {
 __global__ void k_dd_flags(const double* __restrict__ pos, int64_t n, double Lx, const double* __restrict__ bnd,
                            int nranks, int rank, double r_comm, uint8_t* __restrict__ f_home,
                            uint8_t* __restrict__ f_halo, uint8_t* __restrict__ f_send, int32_t* __restrict__ counts) {
+  // per-rank home counts: shared-memory tallies, one global atomic per rank
+  // per block (a global atomic per particle on N addresses serialises:
+  // ~1 ms at 1.5M particles)
+  __shared__ int32_t s_cnt[64];
+  for (int r = threadIdx.x; r < nranks; r += blockDim.x) s_cnt[r] = 0;
+  __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double x = wrap_coord(pos[3 * i], Lx);
-  int own = 0;  // searchsorted(bnd[1:-1], x, side="right"), clipped
-  while (own < nranks - 1 && x >= bnd[own + 1]) ++own;
-  const int nb = (rank + 1) % nranks;
-  f_home[i] = own == rank;
-  f_send[i] = own == rank && (x - bnd[rank]) < r_comm;
-  f_halo[i] = own == nb && (x - bnd[nb]) < r_comm;
-  atomicAdd(&counts[own], 1);
+  if (i < n) {
+    const double x = wrap_coord(pos[3 * i], Lx);
+    int own = 0;  // searchsorted(bnd[1:-1], x, side="right"), clipped
+    while (own < nranks - 1 && x >= bnd[own + 1]) ++own;
+    const int nb = (rank + 1) % nranks;
+    f_home[i] = own == rank;
+    f_send[i] = own == rank && (x - bnd[rank]) < r_comm;
+    f_halo[i] = own == nb && (x - bnd[nb]) < r_comm;
+    atomicAdd(&s_cnt[own], 1);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nranks; r += blockDim.x)
+    if (s_cnt[r]) atomicAdd(&counts[r], s_cnt[r]);
 }
 
 __global__ void k_iota64(int64_t* v, int64_t n) {
