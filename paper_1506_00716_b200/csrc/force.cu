@@ -49,6 +49,7 @@ struct ForceArgs {
   const int32_t* ent_j;
   const float4* ent_delta;    // j-local -> group-local offset (image included)
   const uint64_t* ent_mask;
+  const int32_t* ent_tpos;    // k_force_h: entry -> partial-force slot in j-cluster order (NULL: entry order)
   // per-slot inputs
   const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
   const double* bbox;         // grid bboxes (origins of the local frames)
@@ -685,6 +686,7 @@ struct StageH {
   float4 ed[3][CH];
   uint64_t em[3][CH][W];
   int32_t cj[3][CH];
+  int32_t tp[3][CH];
   float4 xj[2][128];
   int32_t tj[2][128];
 };
@@ -945,6 +947,7 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
         for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], A.ent_mask + (int64_t)e * W + q, 8);
         cp_async(&S.cj[slot][lane], A.ent_j + e, 4);
+        if (A.ent_tpos) cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
       }
     };
     auto stage_jatoms = [&](int xslot, int eslot) {
@@ -1030,6 +1033,7 @@ k_force_h(const ForceArgs A) {
       const float4* c_ed = S.ed[es];
       const uint64_t* c_em = &S.em[es][0][0];
       const int32_t* c_cj = S.cj[es];
+      const int32_t* c_tp = S.tp[es];
       const float4* c_xa = &S.xj[xs][ih * CJ];
       const float4* c_xb = &S.xj[xs][(1 - ih) * CJ];
       const int32_t* c_ta = &S.tj[xs][ih * CJ];
@@ -1114,7 +1118,11 @@ k_force_h(const ForceArgs A) {
       float out[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) out[c] = fj[0][c] + __shfl_xor_sync(0xffffffffu, fj[1][c], 16);
-      if (valid) *pj = make_float4(out[0], out[1], out[2], 0.f);
+      if (valid) {
+        // partials land in j-cluster order (t_pos), so k_reduce streams them
+        float4* dst = A.ent_tpos ? A.part_j + (int64_t)c_tp[ce] * M + ba : pj;
+        *dst = make_float4(out[0], out[1], out[2], 0.f);
+      }
       if (ENERGY) {
         elj_acc += (double)elj;
         ec_acc += (double)ec;
@@ -1226,7 +1234,7 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
   for (int32_t t0 = t_first[c] + sidx; t0 < t1; t0 += S * U) {
     int32_t it[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) it[u] = t0 + u * S < t1 ? __ldg(t_items + t0 + u * S) : -1;
+    for (int u = 0; u < U; ++u) it[u] = t0 + u * S < t1 ? (t_items ? __ldg(t_items + t0 + u * S) : t0 + u * S) : -1;
     float4 pj[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -1515,7 +1523,7 @@ static void ew_fit(double (*f)(double), double wmax, int deg, float* out /* deg+
 
 // transposed index: items (entries or rows) sorted by j-cluster, stable
 static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clusters, DBuf<int32_t>& first,
-                                   DBuf<int32_t>& items, cudaStream_t s);
+                                   DBuf<int32_t>& items, cudaStream_t s, DBuf<int32_t>* pos = nullptr);
 
 static int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
@@ -1534,8 +1542,13 @@ __global__ void k_first_sorted(const int32_t* __restrict__ keys, int64_t n, int6
   for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
 }
 
+__global__ void k_inverse(const int32_t* __restrict__ items, int64_t n, int32_t* __restrict__ pos) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) pos[items[i]] = (int32_t)i;
+}
+
 static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clusters, DBuf<int32_t>& first,
-                                   DBuf<int32_t>& items, cudaStream_t s) {
+                                   DBuf<int32_t>& items, cudaStream_t s, DBuf<int32_t>* pos) {
   DBuf<int32_t> vals, skeys;
   cudaError_t e;
   if ((e = first.alloc(n_clusters + 1, s)) || (e = items.alloc(n, s)) || (e = vals.alloc(n, s)) ||
@@ -1548,6 +1561,10 @@ static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clu
     if ((e = sort_pairs_i32(keys, skeys.p, vals.p, items.p, n, end_bit, s))) return e;
   }
   count_launch(), k_first_sorted<<<nb(n + 1, 256), 256, 0, s>>>(skeys.p, n, n_clusters, first.p);
+  if (pos) {
+    if ((e = pos->alloc(n, s))) return e;
+    if (n > 0) count_launch(), k_inverse<<<nb(n, 256), 256, 0, s>>>(items.p, n, pos->p);
+  }
   vals.release(s);
   skeys.release(s);
   return cudaGetLastError();
@@ -1614,7 +1631,8 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     wk.t_ready = false;
   }
   if (!canonical && !wk.t_ready) {
-    if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s))) goto cuda_fail;
+    if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos)))
+      goto cuda_fail;
     wk.t_ready = true;
   }
   if (canonical && (e = ensure_row_delta(l, s))) goto cuda_fail;
@@ -1657,6 +1675,9 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.ent_j = canonical ? l->j.p : l->ent_j.p;
     A.ent_delta = canonical ? l->delta.p : l->ent_delta.p;
     A.ent_mask = canonical ? l->mask.p : l->ent_mask.p;
+    // k_force_h (grouped, m = 4, 8) writes partials in j-cluster order
+    const bool sorted_j = !canonical && (m == 4 || m == 8) && !use_legacy_force();
+    A.ent_tpos = sorted_j ? wk.t_pos.p : nullptr;
     A.xyzq = wk.xyzq.p;
     A.bbox = grid->bbox.p;
     A.type = wk.type.p;
@@ -1708,7 +1729,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
       goto cuda_fail;
     if (ns > 0)
       count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
-                                           canonical ? wk.tc_items.p : wk.t_items.p, grid->perm.p,
+                                           canonical ? wk.tc_items.p : (sorted_j ? nullptr : wk.t_items.p), grid->perm.p,
                                            grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1);
     if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
       // nothing else to produce

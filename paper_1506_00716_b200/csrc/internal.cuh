@@ -80,6 +80,7 @@ struct ForceWork {
   // transposed index: entries (or rows) sorted by j-cluster
   DBuf<int32_t> t_first;  // (n_clusters + 1)
   DBuf<int32_t> t_items;  // (n_entries)
+  DBuf<int32_t> t_pos;    // (n_entries) inverse of t_items: entry -> its slot in j-cluster order
   bool t_ready = false;
   DBuf<int32_t> tc_first; // canonical-row transpose
   DBuf<int32_t> tc_items;

@@ -1194,7 +1194,7 @@ static void list_release(nbx_list* l, cudaStream_t s) {
   ForceWork& w = l->work;
   w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
   w.e_grp.release(s); w.scalars.release(s); w.lj.release(s); w.t_first.release(s);
-  w.t_items.release(s); w.tc_first.release(s); w.tc_items.release(s);
+  w.t_items.release(s); w.t_pos.release(s); w.tc_first.release(s); w.tc_items.release(s);
 }
 
 extern "C" void nbx_list_free(nbx_list_t* l) {
