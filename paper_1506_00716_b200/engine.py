@@ -359,13 +359,154 @@ def velocity_verlet_step(state: MDState, params: NonbondedParams, dt: float, for
 
 @dataclass
 class RunResult:
+    """engine.py:583-607: final state plus the per-interval series of one run."""
+
     state: MDState
     forces: ForcesEnergies
     steps: np.ndarray
     e_kinetic: np.ndarray
     e_potential: np.ndarray
+    temperature: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    max_drift: np.ndarray = field(default_factory=lambda: np.zeros(0))
     timing: TimingReport = field(default_factory=TimingReport)
+    wall_seconds: float = 0.0
+    log_lines: list = field(default_factory=list)
 
     @property
     def e_total(self) -> np.ndarray:
         return self.e_kinetic + self.e_potential
+
+    def energy_drift(self) -> tuple[float, float]:
+        """(max absolute, max relative) total-energy deviation from step 0."""
+        e = self.e_total
+        d = float(np.abs(e - e[0]).max()) if e.shape[0] else 0.0
+        scale = abs(float(e[0])) if e.shape[0] else 0.0
+        return d, d / scale if scale > 0 else d
+
+
+def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout, dt: float, n_steps: int, *,
+           supercluster_size: int = 1, policy: ListPolicy | None = None, workers: int = 1, n_slabs: int = 0,
+           slab_min_width: float | None = None, report_interval: int = 100, timer: TimingReport | None = None,
+           target_occupancy: float | None = None) -> RunResult:
+    """NVE velocity-Verlet run with the state resident on the GPU
+    (engine.py:610-706 semantics).
+
+    Positions, velocities and forces never leave the device between reports:
+    per step one fused half-kick + drift + wrap kernel (``nbx_vv_update``),
+    the drift guard as a device max-reduction (``nbx_max_displacement``; its
+    single scalar is the only per-step host read), the list lifecycle
+    (rebuild on interval or 2 d_max > r_list - r_c, grid built from the
+    device positions), the force pass (energies only on report steps, like
+    nstcalcenergy) and the second half kick.  Reports read back the
+    energies and the kinetic energy; a singular pair raises at the next
+    report (SingularityError, original indices) as the reference does at
+    the failing step."""
+    if dt <= 0.0:
+        raise ParameterError(f"dt must be positive, got {dt}")
+    if n_steps < 0:
+        raise ParameterError(f"n_steps must be >= 0, got {n_steps}")
+    if workers < 1:
+        raise ParameterError(f"workers must be >= 1, got {workers}")
+    if report_interval < 1:
+        raise ParameterError(f"report_interval must be >= 1, got {report_interval}")
+    from .kernels import _raise_if_singular, compute_nonbonded_device
+
+    policy = policy or ListPolicy()
+    timer = timer or TimingReport()
+    wall0 = time.perf_counter()
+    d = dev.require_cuda()
+    box = system.box
+    buffer = params.r_list - params.r_cut
+    with timer.section("setup"):
+        state = init_state(system, params, layout, supercluster_size=supercluster_size, policy=policy,
+                           n_slabs=n_slabs, slab_min_width=slab_min_width, target_occupancy=target_occupancy)
+        x = dev.to_device(system.positions, torch.float64).clone()
+        v = dev.to_device(system.velocities, torch.float64).clone()
+        m = dev.to_device(system.masses, torch.float64)
+        q = dev.to_device(system.charges, torch.float64)
+        ty = dev.to_device(system.lj_type, torch.int64)
+        ref = dev.to_device(state.drift.reference_positions, torch.float64).clone()
+        f = torch.empty_like(x)
+        e = torch.zeros(2, dtype=torch.float64, device=d)
+        bad = torch.empty(2, dtype=torch.int64, device=d)
+        d_max = 0.0
+
+        def force_pass(energy: bool):
+            compute_nonbonded_device(state.plist, state.grid, x, q, ty, params, box, energy=energy, out=f,
+                                     e_out=e, bad=bad)
+
+        force_pass(True)
+
+    steps, e_kin, e_pot, temps, drifts = [], [], [], [], []
+    log = ["# clustermd run log", "# step e_kinetic e_potential e_total temperature_K max_drift_nm"]
+    dof = 3 * system.n - 3 if system.n > 1 else 3
+
+    def record():
+        bad_h = bad.cpu().numpy()
+        _raise_if_singular(state.plist, state.grid, x, bad_h, params, box)
+        ke = 0.5 * float(torch.einsum("k,kd,kd->", m, v, v).item())
+        eh = e.cpu().numpy()
+        pe = float(eh[0] + eh[1])
+        steps.append(state.step)
+        e_kin.append(ke)
+        e_pot.append(pe)
+        temps.append(2.0 * ke / (dof * BOLTZMANN_KJ_MOL_K) if system.n else 0.0)
+        drifts.append(d_max)
+        log.append(f"{state.step} {ke:.10e} {pe:.10e} {ke + pe:.10e} {temps[-1]:.6f} {d_max:.6e}")
+
+    record()
+    for _ in range(n_steps):
+        with timer.section("step"):
+            with timer.section("integrate"):
+                vv_half_kick_device(x, v, f, m, dt, box, move=True)
+                state.step += 1
+            with timer.section("lifecycle"):
+                interval_due = state.step - state.plist.build_step >= policy.rebuild_interval
+                guard_due = False
+                if not interval_due:
+                    d_max = max(d_max, float(max_displacement_device(ref, x, box).item()))
+                    guard_due = 2.0 * d_max > buffer
+                if interval_due or guard_due:
+                    if guard_due:
+                        state.n_drift_rebuilds += 1
+                    with timer.section("rebuild"):
+                        state.grid = build_cluster_grid(_DeviceSystem(system, x), state.grid.m,
+                                                        state.target_occupancy, positions=x)
+                        state.plist = build_pair_list(state.grid, box, params.r_list,
+                                                      supercluster_size=state.plist.supercluster_size,
+                                                      n_lane=state.plist.n_lane, build_step=state.step)
+                        if policy.prune_on_build and policy.rebuild_interval > 1:
+                            state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box)
+                    ref.copy_(x)
+                    d_max = 0.0
+                    state.n_rebuilds += 1
+            report = state.step % report_interval == 0 or state.step == n_steps
+            with timer.section("forces"):
+                force_pass(report)
+            with timer.section("integrate"):
+                vv_half_kick_device(x, v, f, m, dt, box, move=False)
+            if report:
+                with timer.section("report"):
+                    record()
+    torch.cuda.synchronize()
+    state.system = replace(system, positions=x.cpu().numpy(), velocities=v.cpu().numpy())
+    state.drift = DriftTracker(reference_positions=ref.cpu().numpy(), max_displacement=d_max)
+    eh = e.cpu().numpy()
+    forces = ForcesEnergies(forces=f.cpu().numpy(), e_lj=float(eh[0]), e_coulomb=float(eh[1]))
+    wall = time.perf_counter() - wall0
+    res = RunResult(state=state, forces=forces, steps=np.asarray(steps, dtype=np.int64), e_kinetic=np.asarray(e_kin),
+                    e_potential=np.asarray(e_pot), temperature=np.asarray(temps), max_drift=np.asarray(drifts),
+                    timing=timer, wall_seconds=wall, log_lines=log)
+    dev_abs, dev_rel = res.energy_drift()
+    log.append(f"# energy drift: abs={dev_abs:.6e} kJ/mol rel={dev_rel:.6e}")
+    return res
+
+
+class _DeviceSystem:
+    """The ParticleSystem fields build_cluster_grid reads (n, box), with the
+    positions supplied separately as a device tensor."""
+
+    def __init__(self, system: ParticleSystem, positions: torch.Tensor):
+        self.n = system.n
+        self.box = system.box
+        self.positions = positions

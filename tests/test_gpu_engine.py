@@ -79,3 +79,45 @@ def test_velocity_verlet_step_matches_reference_formula():
     v1 = vh + f1.forces * inv_mass
     assert np.array_equal(st.system.velocities, v1)
     assert st.step == 1
+
+
+def test_run_md_device_resident_matches_host_loop():
+    """run_md (state on the GPU, engine.py:610-706) against the step-by-step
+    host loop of velocity_verlet_step + lifecycle_tick on the same system."""
+    nbx, g, s, params = _fluid("lj_fluid400")
+    layout = nbx.KernelLayout(4, 4)
+    policy = nbx.ListPolicy(rebuild_interval=7)
+    dt, n_steps = 0.002, 30
+    res = nbx.run_md(s, params, layout, dt, n_steps, policy=policy, report_interval=10)
+    assert list(res.steps) == [0, 10, 20, 30]
+    st = nbx.init_state(s, params, layout, policy=policy)
+    f = nbx.parallel_forces(st, params, layout)
+    ke, pe = [nbx.kinetic_energy(st.system)], [f.e_lj + f.e_coulomb]
+    for k in range(1, n_steps + 1):
+        f = nbx.velocity_verlet_step(st, params, dt, f, layout, policy=policy)
+        if k % 10 == 0:
+            ke.append(nbx.kinetic_energy(st.system))
+            pe.append(f.e_lj + f.e_coulomb)
+    assert res.state.step == st.step == n_steps
+    assert res.state.n_rebuilds == st.n_rebuilds
+    dx = nbx.minimum_image(res.state.system.positions - st.system.positions, s.box)
+    assert np.abs(dx).max() < 1e-8
+    assert np.allclose(res.state.system.velocities, st.system.velocities, rtol=1e-6, atol=1e-8)
+    assert np.allclose(res.e_kinetic, ke, rtol=1e-9)
+    assert np.allclose(res.e_potential, pe, rtol=1e-6)
+    assert np.allclose(res.forces.forces, f.forces, rtol=1e-5, atol=1e-6)
+    assert len(res.log_lines) == 2 + 4 + 1 and res.log_lines[-1].startswith("# energy drift")
+
+
+def test_run_md_drift_guard_rebuilds():
+    nbx, g, s, params = _fluid("lj_fluid400")
+    layout = nbx.KernelLayout(4, 4)
+    fast = nbx.ParticleSystem(positions=s.positions, velocities=s.velocities * 40.0, masses=s.masses,
+                              charges=s.charges, lj_type=s.lj_type, box=s.box)
+    res = nbx.run_md(fast, params, layout, 0.002, 20, policy=nbx.ListPolicy(rebuild_interval=1000),
+                     report_interval=20)
+    assert res.state.n_drift_rebuilds >= 1
+    assert res.state.n_rebuilds == 1 + res.state.n_drift_rebuilds
+    assert np.all(res.max_drift <= 0.5 * (params.r_list - params.r_cut) + 1e-12)
+    with pytest.raises(nbx.ParameterError):
+        nbx.run_md(s, params, layout, -1.0, 5)
