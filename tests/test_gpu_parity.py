@@ -269,3 +269,60 @@ def test_moved_positions_use_current_coordinates():
                                      of.Physics(r_cut=1.0, lj_table=table, shift_potential=True))
     assert rel_rms(res.forces, search.scatter_to_original(og, fc)) <= FORCE_RTOL
     assert rel(res.e_lj, elj) <= ENERGY_RTOL and rel(res.e_coulomb, ec) <= ENERGY_RTOL
+
+
+def test_spc96k_bench_config_vs_oracle():
+    """BASELINE config 3 (the bench workload): 96k SPC, tuned grid, LJ + Ewald
+    real space -- grid and pruned list identical to the oracle's C port,
+    forces / energies within the north_star tolerances."""
+    from oracle import forces as of
+    from oracle import native, search
+
+    nbx, s, table, occ = _spc(96000, "tuned")
+    L = s.box.lengths
+    grid = nbx.build_cluster_grid(s, 4, occ)
+    og = search.build_grid(s.positions, L, 4, occ)
+    assert np.array_equal(grid.perm, og["perm"]) and np.array_equal(grid.bboxes, og["bboxes"])
+    pruned = nbx.prune_pair_list(nbx.build_pair_list(grid, s.box, 1.1), grid.clustered_positions_device, s.box)
+    op = native.prune_list(native.search_list(og, L, 1.1), og["clustered_positions"], L)
+    assert np.array_equal(pruned.offsets, op["offsets"]) and np.array_equal(pruned.j_idx, op["j_idx"])
+    assert np.array_equal(pruned.mask_bits, search.pack_masks(op["masks"]))
+    beta = nbx.ewald_beta(1.0)
+    params = nbx.NonbondedParams(r_cut=1.0, r_list=1.1, lj_table=table, shift_potential=True, elec="ewald",
+                                 ewald_beta=beta)
+    phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True, elec="ewald", ewald_beta=beta)
+    res = nbx.compute_nonbonded_original(pruned, grid, s.positions, s.charges, s.lj_type, params, s.box,
+                                         nbx.KernelLayout(4, 4))
+    fc, elj, ec = native.list_forces(op, og, s.positions, s.charges, s.lj_type, L, phys)
+    fref = search.scatter_to_original(og, fc)
+    assert rel_rms(res.forces, fref) <= FORCE_RTOL
+    assert rel(res.e_lj, elj) <= ENERGY_RTOL and rel(res.e_coulomb, ec) <= ENERGY_RTOL
+
+
+def test_spc1p5m_forces_vs_oracle_and_newton():
+    """BASELINE config 4 size (1.5M atoms) on one GPU: forces on the GPU list
+    against the oracle's C force pass over the same list, and the
+    size-independent property sum_i F_i = 0 (every pair enters twice with
+    opposite sign)."""
+    from oracle import forces as of
+    from oracle import native, search
+
+    nbx, s, table, occ = _spc(1500000, "tuned")
+    L = s.box.lengths
+    grid = nbx.build_cluster_grid(s, 4, occ)
+    pruned = nbx.prune_pair_list(nbx.build_pair_list(grid, s.box, 1.1), grid.clustered_positions_device, s.box)
+    beta = nbx.ewald_beta(1.0)
+    params = nbx.NonbondedParams(r_cut=1.0, r_list=1.1, lj_table=table, shift_potential=True, elec="ewald",
+                                 ewald_beta=beta)
+    res = nbx.compute_nonbonded_original(pruned, grid, s.positions, s.charges, s.lj_type, params, s.box,
+                                         nbx.KernelLayout(4, 4))
+    net = np.abs(res.forces.sum(axis=0)).max()
+    assert net <= 1e-6 * np.abs(res.forces).sum(axis=0).max()
+    og = search.build_grid(s.positions, L, 4, occ)
+    assert np.array_equal(grid.perm, og["perm"])
+    ol = dict(m=4, offsets=pruned.offsets, j_idx=pruned.j_idx, masks=pruned.masks, r_list=1.1)
+    phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True, elec="ewald", ewald_beta=beta)
+    fc, elj, ec = native.list_forces(ol, og, s.positions, s.charges, s.lj_type, L, phys)
+    fref = search.scatter_to_original(og, fc)
+    assert rel_rms(res.forces, fref) <= FORCE_RTOL
+    assert rel(res.e_lj, elj) <= ENERGY_RTOL and rel(res.e_coulomb, ec) <= ENERGY_RTOL
