@@ -988,15 +988,18 @@ __global__ void k_fill_i32(int32_t* __restrict__ v, int64_t n, int32_t x) {
   if (i < n) v[i] = x;
 }
 
-__global__ void k_group_keys(const int32_t* __restrict__ ent_off, int64_t n_groups, int32_t* __restrict__ keys,
-                             int32_t* __restrict__ vals) {
+__global__ void k_group_keys(const int32_t* __restrict__ ent_off, const int32_t* __restrict__ nmem,
+                             int64_t n_groups, int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= n_groups) return;
-  keys[g] = 0x3fffffff - (ent_off[g + 1] - ent_off[g]);  // ascending key = descending size
+  // estimated force-kernel cost: per entry ~1/8 of an iteration's fixed work
+  // plus up to nmem member sweeps (measured ratio ~1 : 5 per present member)
+  const int64_t cost = (int64_t)(ent_off[g + 1] - ent_off[g]) * (2 + 5 * (nmem ? nmem[g] : 1));
+  keys[g] = 0x3fffffff - (int32_t)min(cost, (int64_t)0x3ffffffe);  // ascending key = descending cost
   vals[g] = (int32_t)g;
 }
 
-// force-kernel work order: groups by descending entry count (LPT)
+// force-kernel work order: groups by descending estimated cost (LPT)
 static cudaError_t order_groups(List* l, cudaStream_t s) {
   DBuf<int32_t> keys, keys2, vals;
   cudaError_t e;
@@ -1005,7 +1008,8 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
   if ((e = keys.alloc(l->n_groups, s)) || (e = keys2.alloc(l->n_groups, s)) || (e = vals.alloc(l->n_groups, s)))
     return e;
   count_launch();
-  k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->n_groups, keys.p, vals.p);
+  k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->group_nmem.p, l->n_groups, keys.p,
+                                                     vals.p);
   e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, 30, s);
   keys.release(s); keys2.release(s); vals.release(s);
   return e;
