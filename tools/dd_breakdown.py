@@ -49,4 +49,19 @@ for rep in range(4):
     if rank == 0:
         print(f"N={world} rep {rep}: allgather {t_ag:.3f} ms | assign {t_as:.3f} | rebuild(incl assign) {t_rb:.3f} | "
               f"force#1 {t_f1:.3f} | force {t_f2:.3f} | home {lay.n_home} halo {lay.n_local - lay.n_home}")
+
+# host enqueue cost vs device time of force-only steps (host-bound if close)
+torch.cuda.synchronize()
+dist.barrier()
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record()
+h0 = time.perf_counter()
+for _ in range(50):
+    df.forces(energy=False)
+h1 = time.perf_counter()
+ev1.record()
+torch.cuda.synchronize()
+if rank == 0:
+    print(f"N={world} force steps: host enqueue {1e6 * (h1 - h0) / 50:.1f} us/step, "
+          f"device {1e3 * ev0.elapsed_time(ev1) / 50:.1f} us/step")
 dist.destroy_process_group()
