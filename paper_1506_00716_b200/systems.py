@@ -25,7 +25,7 @@ import math
 
 import numpy as np
 
-from .model import BOLTZMANN_KJ_MOL_K, ParticleSystem, SimBox, wrap_position
+from .model import BOLTZMANN_KJ_MOL_K, ParameterError, ParticleSystem, SimBox, wrap_position
 
 SPC_DENSITY_MOL_NM3 = 33.43
 SPC_OH = 0.1
@@ -107,3 +107,103 @@ def tuned_occupancy(n_atoms: int, box_edge: float, m: int) -> float:
     target_occupancy (gridder.py:69-71)."""
     rho = n_atoms / box_edge ** 3
     return m ** (2.0 / 3.0) * rho ** (1.0 / 3.0) * box_edge
+
+
+# ---------------------------------------------------------------- reference fluids and system files
+# SURVEY §8(f) #3: the reference's generators (cli.py:158-250) and JSON system
+# files (model.py:232-277), so fixtures and CLI-style workflows run unchanged.
+ARGON_EPSILON = 0.996   # kJ/mol (cli.py:52)
+ARGON_SIGMA = 0.34      # nm
+ARGON_MASS = 39.948     # u
+NEON_MASS = 20.180      # u (second species of the charged fluid)
+
+
+class GenerationError(RuntimeError):
+    """The requested density cannot host the lattice with the minimum separation (cli.py:59)."""
+
+
+def _fluid_species(kind: str, n: int, charge: float):
+    """(lj_table, lj_type, masses, charges) of the reference's two fluids."""
+    if kind == "lj_fluid":
+        return (np.array([[[ARGON_EPSILON, ARGON_SIGMA]]]), np.zeros(n, dtype=np.int64),
+                np.full(n, ARGON_MASS), np.zeros(n))
+    if kind == "charged_fluid":
+        eps, sig = (ARGON_EPSILON, 0.8), (ARGON_SIGMA, 0.30)
+        mix = (math.sqrt(eps[0] * eps[1]), 0.5 * (sig[0] + sig[1]))   # geometric eps, arithmetic sigma
+        table = np.array([[[eps[0], sig[0]], list(mix)], [list(mix), [eps[1], sig[1]]]])
+        alt = np.arange(n) % 2
+        q = charge * np.where(alt == 0, 1.0, -1.0)
+        if n % 2:
+            q[-1] = 0.0  # neutral box for odd counts
+        return table, alt.astype(np.int64), np.where(alt == 0, ARGON_MASS, NEON_MASS), q
+    raise ParameterError(f"unknown system kind {kind!r}")
+
+
+def generate_system(kind: str, n: int, density: float, temperature: float, seed: int,
+                    charge: float = 0.2) -> tuple[ParticleSystem, np.ndarray]:
+    """Deterministic lattice-plus-jitter fluid in a cubic box (cli.py:158-250):
+    same arguments, same random stream, same system as the reference."""
+    if n < 1:
+        raise ParameterError(f"n must be >= 1, got {n}")
+    if density <= 0.0:
+        raise ParameterError(f"density must be positive, got {density}")
+    if temperature < 0.0:
+        raise ParameterError(f"temperature must be >= 0, got {temperature}")
+    table, types, masses, charges = _fluid_species(kind, n, charge)
+    edge = (n / density) ** (1.0 / 3.0)
+    k = max(1, int(round(n ** (1.0 / 3.0))))
+    while k ** 3 < n:
+        k += 1
+    spacing = edge / k
+    min_sep = 0.8 * float(table[:, :, 1].max())
+    if spacing <= min_sep:
+        raise GenerationError(f"density {density} nm^-3 packs lattice spacing {spacing:.4f} nm "
+                              f"below the minimum separation {min_sep:.4f} nm")
+    i = np.arange(n)
+    pos = np.stack([i // (k * k), (i // k) % k, i % k], axis=1).astype(np.float64) * spacing
+    rng = np.random.default_rng(seed)
+    if n > 1:
+        jitter = 0.45 * (spacing - min_sep)
+        pos = pos + rng.uniform(-jitter, jitter, (n, 3))
+    if temperature > 0.0:
+        vel = np.sqrt(BOLTZMANN_KJ_MOL_K * temperature / masses)[:, None] * rng.standard_normal((n, 3))
+        if n > 1:
+            total = masses.sum()
+            for _ in range(2):  # the second pass removes the rounding residue
+                vel = vel - np.einsum("k,kd->d", masses, vel) / total
+    else:
+        vel = np.zeros((n, 3))
+    box = SimBox([edge, edge, edge])
+    return ParticleSystem(positions=pos, velocities=vel, masses=masses, charges=charges, lj_type=types,
+                          box=box), table
+
+
+_SYSTEM_KEYS = ("box", "positions", "velocities", "masses", "charges", "lj_type", "lj_table")
+
+
+def save_system(path, system: ParticleSystem, lj_table) -> None:
+    """System + LJ table as deterministic JSON, the reference's file format (model.py:232-246)."""
+    import json
+
+    doc = dict(zip(_SYSTEM_KEYS, (system.box.lengths.tolist(), system.positions.tolist(),
+                                  system.velocities.tolist(), system.masses.tolist(), system.charges.tolist(),
+                                  system.lj_type.tolist(), np.asarray(lj_table, dtype=np.float64).tolist())))
+    with open(path, "w") as fh:
+        json.dump(doc, fh, indent=1)
+        fh.write("\n")
+
+
+def load_system(path) -> tuple[ParticleSystem, np.ndarray]:
+    """Inverse of save_system (model.py:249-277); ParameterError on missing keys."""
+    import json
+
+    with open(path) as fh:
+        doc = json.load(fh)
+    missing = [k for k in _SYSTEM_KEYS if k not in doc]
+    if missing:
+        raise ParameterError(f"system file {path} missing keys: {missing}")
+    system = ParticleSystem(positions=doc["positions"], velocities=doc["velocities"], masses=doc["masses"],
+                            charges=doc["charges"], lj_type=doc["lj_type"], box=SimBox(doc["box"]))
+    table = np.array(doc["lj_table"], dtype=np.float64)
+    table.setflags(write=False)
+    return system, table
