@@ -31,6 +31,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "internal.cuh"
@@ -1706,12 +1707,28 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.beta3 = (float)(p->ewald_beta * p->ewald_beta * p->ewald_beta);
     A.ew_shift = p->shift_potential ? (float)(erfc(p->ewald_beta * rc) / rc) : 0.f;
     if (ewald) {
-      // fit range: r^2 up to (r_c^2 + band) with margin
-      const double wmax = p->ewald_beta * p->ewald_beta * rc * rc * 1.02;
-      A.ew_a = (float)(2.0 / wmax * p->ewald_beta * p->ewald_beta);
-      ew_fit(ew_gf, wmax, EW_DEG_F, A.ew_f);
-      ew_fit(ew_gv, wmax, EW_DEG_V, A.ew_v);
-      ew_fit(ew_gf, wmax, EW_DEG_F, A.ew_s, -(double)p->ewald_beta * p->ewald_beta * p->ewald_beta);
+      // fit range: r^2 up to (r_c^2 + band) with margin.  The fits cost ~600
+      // transcendental host calls: cached per (beta, r_c) (thread-local).
+      struct EwCache {
+        double beta = -1.0, rc = -1.0;
+        float a, f[16], v[16], sc[16];
+      };
+      static thread_local EwCache ec;
+      if (ec.beta != p->ewald_beta || ec.rc != rc) {
+        const double wmax = p->ewald_beta * p->ewald_beta * rc * rc * 1.02;
+        ec.a = (float)(2.0 / wmax * p->ewald_beta * p->ewald_beta);
+        ew_fit(ew_gf, wmax, EW_DEG_F, ec.f);
+        ew_fit(ew_gv, wmax, EW_DEG_V, ec.v);
+        ew_fit(ew_gf, wmax, EW_DEG_F, ec.sc, -(double)p->ewald_beta * p->ewald_beta * p->ewald_beta);
+        ec.beta = p->ewald_beta;
+        ec.rc = rc;
+      }
+      A.ew_a = ec.a;
+      for (int k = 0; k < 16; ++k) {
+        A.ew_f[k] = ec.f[k];
+        A.ew_v[k] = ec.v[k];
+        A.ew_s[k] = ec.sc[k];
+      }
     }
     A.slack_base = (float)(2.0 * rc + 1e-3);
     double Lmax = fmax(box[0], fmax(box[1], box[2]));
