@@ -411,6 +411,7 @@ def run_dd(args, world, rank, local):
     box = system.box
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
     dd.enable_native()
+    p2p = dd.enable_p2p(system.n)  # per-step halo exchanges as NVLink peer stores (NBX_DD_P2P=0: NCCL)
     df = DomainForces(dd, system, params, M, occ)
     pos_glob = torch.from_numpy(np.array(system.positions)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -495,7 +496,8 @@ def run_dd(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (pair math; fp64 energy + final force accumulation)",
             "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
-            "config": config(args, occ, {"parallelism": f"slab DD x{world} (NCCL p2p half-shell halo, r_comm=r_list)"}),
+            "config": config(args, occ, {"parallelism": f"slab DD x{world} (half-shell halo, r_comm=r_list, "
+                                                         f"{'NVLink peer stores' if p2p else 'NCCL send/recv'})"}),
             "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
             "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted},
             "e2e": {"value": n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",

@@ -201,6 +201,17 @@ int nbx_dd_assign(nbx_dd_t* dd, const double* positions, int64_t n, double box_x
  * (id, x, y, z) records padded to cap >= max home count. */
 int nbx_dd_allgather_home(nbx_dd_t* dd, const int64_t* home_ids, const double* home_pos, int64_t n_home,
                           int64_t cap, double* positions_global, void* stream);
+/* NVLink peer path for the two per-step exchanges (replaces NCCL send/recv):
+ * every rank calls nbx_dd_p2p_alloc (capacity = max halo / face particles,
+ * e.g. the global particle count), all-gathers the 64-byte CUDA IPC handles,
+ * then nbx_dd_p2p_open with the handles of rank-1 and rank+1.  Afterwards
+ * nbx_dd_exchange_positions / nbx_dd_reduce_forces store straight into the
+ * neighbour's memory and synchronise through release/acquire flags.
+ * Passing NULL handles to nbx_dd_p2p_open switches back to NCCL.
+ * nbx_dd_p2p_error reports a timed-out peer wait (syncs). */
+int nbx_dd_p2p_alloc(nbx_dd_t* dd, int64_t capacity, uint8_t handle_out[64]);
+int nbx_dd_p2p_open(nbx_dd_t* dd, const uint8_t down_handle[64], const uint8_t up_handle[64]);
+int nbx_dd_p2p_error(nbx_dd_t* dd, int32_t* out);
 void nbx_dd_free(nbx_dd_t* dd);
 
 /* Exact FP64 scan of every admitted pair for a coincident in-range pair

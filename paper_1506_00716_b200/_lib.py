@@ -29,7 +29,7 @@ EXPORTS = (
     "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
     "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
-    "nbx_dd_assign", "nbx_dd_allgather_home",
+    "nbx_dd_assign", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error",
 )
 
 
@@ -100,6 +100,9 @@ def load():
         "nbx_dd_free": (None, [P]),
         "nbx_dd_assign": (ctypes.c_int, [P, P, I64, D, P, D, P, P, P, P, P]),
         "nbx_dd_allgather_home": (ctypes.c_int, [P, P, P, I64, I64, P, P]),
+        "nbx_dd_p2p_alloc": (ctypes.c_int, [P, I64, P]),
+        "nbx_dd_p2p_open": (ctypes.c_int, [P, P, P]),
+        "nbx_dd_p2p_error": (ctypes.c_int, [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -9,6 +9,8 @@
 //       forces rank-1 computed on our face particles, add them (one kernel).
 #include <nccl.h>
 
+#include <cstring>
+
 #include "internal.cuh"
 
 struct nbx_dd {
@@ -18,6 +20,15 @@ struct nbx_dd {
   nbx::DBuf<int64_t> send_local;  // indices (in the local array) of particles sent to rank-1
   nbx::DBuf<double> sendbuf;      // packed coordinates (n_send x 3)
   nbx::DBuf<double> recvbuf;      // forces from rank-1 (n_send x 3)
+  // NVLink peer path (nbx_dd_p2p_*): one cudaMalloc'd, IPC-exported region
+  // per rank = [halo positions in (cap x 3)][halo forces in (cap x 3)][flags]
+  int p2p = 0;
+  int64_t cap = 0;
+  char* p2p_base = nullptr;       // own region
+  char* peer_down = nullptr;      // rank-1's region (positions go there)
+  char* peer_up = nullptr;        // rank+1's region (halo forces go there)
+  unsigned long long seq_pos = 0, seq_f = 0;
+  unsigned int* err = nullptr;    // device: set when a wait timed out
 };
 
 namespace nbx {
@@ -40,6 +51,72 @@ __global__ void k_unpack_add(double* __restrict__ f, const int64_t* __restrict__
   f[3 * s] += in[3 * i];
   f[3 * s + 1] += in[3 * i + 1];
   f[3 * s + 2] += in[3 * i + 2];
+}
+
+// ---- NVLink peer path: the sender stores straight into the receiver's
+// region (P2P stores over NVLink), then publishes a sequence number with a
+// system-scope release; the receiver's kernel acquires it and consumes the
+// data in place (copy into the halo rows / add into the face atoms).  No
+// NCCL kernel, proxy thread or host involvement per step.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// gather rows idx (or the contiguous rows [0, n) when idx == NULL) of x into
+// the peer buffer, then the last block to finish publishes `seq`
+__global__ void k_p2p_put(const double* __restrict__ x, const int64_t* __restrict__ idx, int64_t n,
+                          double* __restrict__ peer_buf, unsigned long long* peer_flag, unsigned long long seq,
+                          unsigned int* __restrict__ done) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx ? idx[i] : i;
+    peer_buf[3 * i] = x[3 * r];
+    peer_buf[3 * i + 1] = x[3 * r + 1];
+    peer_buf[3 * i + 2] = x[3 * r + 2];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {  // every block's stores are fenced
+      *done = 0u;
+      __threadfence_system();
+      st_release_sys(peer_flag, seq);
+    }
+  }
+}
+
+// wait for `seq` in the own flag (bounded spin), then consume the received
+// rows: mode 0 copies them to out[0:n), mode 1 adds them to out[idx[i]]
+__global__ void k_p2p_take(const unsigned long long* flag, unsigned long long seq, const double* __restrict__ buf,
+                           int64_t n, const int64_t* __restrict__ idx, double* __restrict__ out, int mode,
+                           unsigned int* err) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    // bounded wait: ~5 s of SM clock, then flag the error instead of hanging
+    const long long t0 = clock64();
+    while (ld_acquire_sys(flag) < seq && clock64() - t0 < 10000000000ll) __nanosleep(100);
+    ok = ld_acquire_sys(flag) >= seq;
+    if (!ok) atomicOr(err, 1u);
+  }
+  __syncthreads();
+  if (!ok) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mode == 0) {
+      out[3 * i] = __ldcv(buf + 3 * i);  // written by the peer: bypass L1
+      out[3 * i + 1] = __ldcv(buf + 3 * i + 1);
+      out[3 * i + 2] = __ldcv(buf + 3 * i + 2);
+    } else {
+      const int64_t r = idx[i];  // unique per i: deterministic, no atomics
+      out[3 * r] += __ldcv(buf + 3 * i);
+      out[3 * r + 1] += __ldcv(buf + 3 * i + 1);
+      out[3 * r + 2] += __ldcv(buf + 3 * i + 2);
+    }
+  }
 }
 
 }  // namespace nbx
@@ -113,6 +190,24 @@ extern "C" int nbx_dd_exchange_positions(nbx_dd_t* d, double* local_pos, void* s
   }
   if (d->nranks == 1) return NBX_OK;
   cudaStream_t s = to_stream(stream);
+  if (d->p2p) {
+    const unsigned long long seq = ++d->seq_pos;
+    const int64_t cap = d->cap;
+    double* peer_pos = reinterpret_cast<double*>(d->peer_down);
+    unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_down + 48 * cap);
+    unsigned int* done = d->err + 1;
+    count_launch(2);
+    k_p2p_put<<<16, 256, 0, s>>>(local_pos, d->send_local.p, d->n_send, peer_pos, peer_flag, seq, done);
+    const double* own = reinterpret_cast<const double*>(d->p2p_base);
+    const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap);
+    k_p2p_take<<<16, 256, 0, s>>>(flag, seq, own, d->n_halo, nullptr, local_pos + 3 * d->n_home, 0, d->err);
+    cudaError_t e = cudaGetLastError();
+    if (e) {
+      set_error("nbx_dd_exchange_positions: %s", cudaGetErrorString(e));
+      return NBX_ERR_CUDA;
+    }
+    return NBX_OK;
+  }
   if (d->n_send > 0) {
     count_launch();
     k_pack<<<(unsigned)((d->n_send + 255) / 256), 256, 0, s>>>(local_pos, d->send_local.p, d->n_send, d->sendbuf.p);
@@ -138,6 +233,24 @@ extern "C" int nbx_dd_reduce_forces(nbx_dd_t* d, double* local_f, void* stream) 
   }
   if (d->nranks == 1) return NBX_OK;
   cudaStream_t s = to_stream(stream);
+  if (d->p2p) {
+    const unsigned long long seq = ++d->seq_f;
+    const int64_t cap = d->cap;
+    double* peer_f = reinterpret_cast<double*>(d->peer_up + 24 * cap);
+    unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_up + 48 * cap) + 1;
+    unsigned int* done = d->err + 2;
+    count_launch(2);
+    k_p2p_put<<<16, 256, 0, s>>>(local_f + 3 * d->n_home, nullptr, d->n_halo, peer_f, peer_flag, seq, done);
+    const double* own = reinterpret_cast<const double*>(d->p2p_base + 24 * cap);
+    const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap) + 1;
+    k_p2p_take<<<16, 256, 0, s>>>(flag, seq, own, d->n_send, d->send_local.p, local_f, 1, d->err);
+    cudaError_t e = cudaGetLastError();
+    if (e) {
+      set_error("nbx_dd_reduce_forces: %s", cudaGetErrorString(e));
+      return NBX_ERR_CUDA;
+    }
+    return NBX_OK;
+  }
   const int down = (d->rank - 1 + d->nranks) % d->nranks, up = (d->rank + 1) % d->nranks;
   NCCL_TRY(ncclGroupStart());
   if (d->n_halo > 0) NCCL_TRY(ncclSend(local_f + 3 * d->n_home, (size_t)(3 * d->n_halo), ncclDouble, up, d->comm, s));
@@ -166,8 +279,71 @@ extern "C" int nbx_dd_allreduce_sum(nbx_dd_t* d, double* buf, int64_t n, void* s
   return NBX_OK;
 }
 
+// NVLink peer path, step 1 (every rank): allocate the own region for up to
+// `cap` halo / face particles and export its CUDA IPC handle (64 bytes).
+extern "C" int nbx_dd_p2p_alloc(nbx_dd_t* d, int64_t cap, uint8_t handle_out[64]) {
+  if (!d || cap < 1 || !handle_out) {
+    set_error("nbx_dd_p2p_alloc: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaError_t e;
+  cudaIpcMemHandle_t h;
+  const size_t bytes = (size_t)48 * cap + 64;
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&d->p2p_base), bytes)) ||
+      (e = cudaMemset(d->p2p_base, 0, bytes)) ||
+      (e = cudaMalloc(reinterpret_cast<void**>(&d->err), 16)) || (e = cudaMemset(d->err, 0, 16)) ||
+      (e = cudaIpcGetMemHandle(&h, d->p2p_base))) {
+    set_error("nbx_dd_p2p_alloc: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  memcpy(handle_out, &h, 64);
+  d->cap = cap;
+  return NBX_OK;
+}
+
+// step 2: map the neighbours' regions (rank-1 receives our face positions,
+// rank+1 our halo forces) and switch the per-step exchanges to P2P stores.
+extern "C" int nbx_dd_p2p_open(nbx_dd_t* d, const uint8_t down_handle[64], const uint8_t up_handle[64]) {
+  if (d && !down_handle && !up_handle) {  // collective fallback: back to NCCL send/recv
+    d->p2p = 0;
+    return NBX_OK;
+  }
+  if (!d || !d->p2p_base || !down_handle || !up_handle) {
+    set_error("nbx_dd_p2p_open: call nbx_dd_p2p_alloc first");
+    return NBX_ERR_PARAM;
+  }
+  cudaIpcMemHandle_t hd, hu;
+  memcpy(&hd, down_handle, 64);
+  memcpy(&hu, up_handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(reinterpret_cast<void**>(&d->peer_down), hd, cudaIpcMemLazyEnablePeerAccess);
+  if (!e) {
+    if (memcmp(down_handle, up_handle, 64) == 0) d->peer_up = d->peer_down;  // N = 2: one neighbour
+    else e = cudaIpcOpenMemHandle(reinterpret_cast<void**>(&d->peer_up), hu, cudaIpcMemLazyEnablePeerAccess);
+  }
+  if (e) {
+    set_error("nbx_dd_p2p_open: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  d->p2p = 1;
+  return NBX_OK;
+}
+
+// non-zero when a peer wait timed out (the exchanged data is then invalid)
+extern "C" int nbx_dd_p2p_error(nbx_dd_t* d, int32_t* out) {
+  if (!d || !out) return NBX_ERR_PARAM;
+  unsigned int h = 0;
+  if (d->err) cudaMemcpy(&h, d->err, 4, cudaMemcpyDeviceToHost);
+  *out = (int32_t)h;
+  return NBX_OK;
+}
+
 extern "C" void nbx_dd_free(nbx_dd_t* d) {
   if (!d) return;
+  if (d->peer_down) cudaIpcCloseMemHandle(d->peer_down);
+  if (d->peer_up && d->peer_up != d->peer_down) cudaIpcCloseMemHandle(d->peer_up);
+  if (d->p2p_base) cudaFree(d->p2p_base);
+  if (d->err) cudaFree(d->err);
   if (d->comm) ncclCommDestroy(d->comm);
   d->send_local.release(0);
   d->sendbuf.release(0);

@@ -121,6 +121,51 @@ class SlabDecomposition:
         _lib.check(lib.nbx_dd_create(_lib.ptr(uid), self.N, self.rank, ctypes.byref(h)), "dd_create")
         self._native = h
 
+    def enable_p2p(self, capacity: int) -> bool:
+        """Switch the per-step exchanges to NVLink peer stores (libnbx
+        ``nbx_dd_p2p_*``): each rank exports a CUDA IPC region for up to
+        ``capacity`` halo / face particles (the global particle count is
+        always enough), the handles are all-gathered once, and rank-1 /
+        rank+1 map each other's regions.  Collective; needs enable_native().
+        Returns False (NCCL path kept) when NBX_DD_P2P=0 or there is one rank."""
+        import os
+
+        if self.N == 1 or self._native is None or os.environ.get("NBX_DD_P2P", "1") == "0":
+            return False
+        import torch.distributed as dist
+
+        from . import _lib
+
+        lib = _lib.load()
+        h = np.zeros(64, dtype=np.uint8)
+        _lib.check(lib.nbx_dd_p2p_alloc(self._native, int(capacity), _lib.ptr(h)), "dd_p2p_alloc")
+        allh = [None] * self.N
+        dist.all_gather_object(allh, h.tobytes(), group=self.group)
+        down = np.frombuffer(allh[(self.rank - 1) % self.N], dtype=np.uint8).copy()
+        up = np.frombuffer(allh[(self.rank + 1) % self.N], dtype=np.uint8).copy()
+        st = lib.nbx_dd_p2p_open(self._native, _lib.ptr(down), _lib.ptr(up))
+        # every rank must take the same path: fall back together if any failed
+        ok = torch.tensor([1 if st == _lib.NBX_OK else 0], device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if int(ok.item()) == 0:
+            lib.nbx_dd_p2p_open(self._native, None, None)
+            self.p2p = False
+            return False
+        self.p2p = True
+        return True
+
+    def p2p_error(self) -> bool:
+        """True when a peer wait timed out (host sync)."""
+        if not getattr(self, "p2p", False):
+            return False
+        import ctypes
+
+        from . import _lib
+
+        out = ctypes.c_int32(0)
+        _lib.check(_lib.load().nbx_dd_p2p_error(self._native, ctypes.byref(out)), "dd_p2p_error")
+        return out.value != 0
+
     def __del__(self):
         h = getattr(self, "_native", None)
         if h is not None:

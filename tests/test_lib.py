@@ -10,7 +10,7 @@ REPO = Path(__file__).resolve().parents[1]
 def declared_symbols():
     text = (REPO / "include" / "nbx.h").read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return set(re.findall(r"\b(nbx_[a-z_]+)\s*\(", text))
+    return set(re.findall(r"\b(nbx_[a-z0-9_]+)\s*\(", text))
 
 
 def test_library_exports_every_declared_symbol():
