@@ -599,10 +599,28 @@ constexpr int PRUNE_WARPS = 4;
 // skipped warp-uniformly.  MI = per-pair minimum image (entries whose slack
 // cannot guarantee the single shift at the current displacements).
 template <int M, int G, int W, bool MI>
+__device__ __forceinline__ float prune_r2(const float4& xi, const float4& xj, const float (&Lf)[3],
+                                          const float (&iLf)[3]) {
+  float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
+  if (MI) {
+    dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
+    dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
+    dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
+  }
+  return fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+}
+
+// Per member: the minimum FP32 r^2 over this lane's admitted pairs decides
+// (min < lo: kept; min > hi: no pair of the lane within r_list); only a
+// member whose minimum falls inside the +-1e-4 band lists its band pairs for
+// the exact FP64 replay -- the same decisions as testing every pair, with a
+// select + min per pair instead of two compares and two selects.
+template <int M, int G, int W, bool MI>
 __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, const uint32_t (&wd)[2 * W],
                                             const float4& xj, float lo, float hi, const float (&Lf)[3],
                                             const float (&iLf)[3], uint32_t& inbits, uint32_t& amb) {
   constexpr int MM = M * M;
+  const float inf = __int_as_float(0x7f800000);
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int p0 = W == 2 ? k * 64 : k * MM;
@@ -610,19 +628,20 @@ __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, con
 #pragma unroll
     for (int a = 0; a < M; ++a) cb |= (wd[(p0 + a * M) >> 5] >> ((p0 + a * M) & 31)) & 1u ? (1u << a) : 0u;
     if (!__any_sync(0xffffffffu, cb != 0u)) continue;
+    float fmin = inf;
 #pragma unroll
     for (int a = 0; a < M; ++a) {
-      const float4 xi = s_xi[k * M + a];
-      float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
-      if (MI) {
-        dx = fmaf(-Lf[0], rintf(dx * iLf[0]), dx);
-        dy = fmaf(-Lf[1], rintf(dy * iLf[1]), dy);
-        dz = fmaf(-Lf[2], rintf(dz * iLf[2]), dz);
+      const float f = prune_r2<M, G, W, MI>(s_xi[k * M + a], xj, Lf, iLf);
+      fmin = fminf(fmin, ((cb >> a) & 1u) ? f : inf);
+    }
+    if (fmin < lo) {
+      inbits |= 1u << k;
+    } else if (fmin <= hi) {  // rare: list the band pairs of this member
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        const float f = prune_r2<M, G, W, MI>(s_xi[k * M + a], xj, Lf, iLf);
+        amb |= (((cb >> a) & 1u) && f >= lo && f <= hi) ? (1u << (k * M + a)) : 0u;
       }
-      const float f = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const bool adm = (cb >> a) & 1u;
-      inbits |= (adm && f < lo) ? (1u << k) : 0u;
-      amb |= (adm && f >= lo && f <= hi) ? (1u << (k * M + a)) : 0u;
     }
   }
 }
