@@ -1,7 +1,7 @@
 """Benchmark: nbnxn search + force on synthetic SPC water (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--atoms 96000] [--elec ewald|rf|cutoff] [--nstlist 10]
+                    [--atoms 96000] [--elec ewald|rf|cutoff] [--nstlist 10] [--rlist 1.1]
 
 One STEP = one MD step of the non-bonded hot path: every `nstlist` steps the
 grid, the cluster-pair search and the prune are redone from scratch at the
@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--atoms", type=int, default=96000)
     ap.add_argument("--elec", default="ewald", choices=["ewald", "rf", "cutoff"])
     ap.add_argument("--nstlist", type=int, default=10)
+    ap.add_argument("--rlist", type=float, default=1.1, help="buffered list cutoff r_list in nm (config 5 sweep)")
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -515,7 +516,9 @@ def run_dd(args, world, rank, local):
 
 
 def main():
+    global R_LIST
     args = parse()
+    R_LIST = args.rlist
     if args.impl == "reference":
         run_reference(args)
     else:
