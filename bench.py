@@ -16,8 +16,11 @@ e2e     = the same metric with host (pinned) positions/charges/types copied
           H2D and forces + energies copied D2H inside every timed step.
 roofline= the force kernel (k_force) against the FP32 pipe peak
           (148 SMs x 128 lanes x 2 flop x sm_max_mhz from MEASURED_PEAKS.json),
-          flops = admitted slot pairs x per-pair cost (kernels.FLOPS_PER_PAIR
-          = 40, +12 for Ewald).
+          flops = admitted slot pairs the kernel evaluates x per-pair cost
+          (kernels.FLOPS_PER_PAIR = 40, +12 for Ewald).  With dynamic
+          pruning (--rinner, default r_c + 0.02 nm; 0 = off) those are the
+          inner list's pairs (pairs_per_step.force_kernel), not the r_list
+          list's (pairs_per_step.admitted).
 cpu_baseline = the reference algorithm's CPU port (oracle/, FP64, all host
           threads) on the same system: one rebuild + one force pass.
 --impl reference: that CPU port timed for W + K steps (rank 0 only).
@@ -53,6 +56,8 @@ def parse():
     ap.add_argument("--elec", default="ewald", choices=["ewald", "rf", "cutoff"])
     ap.add_argument("--nstlist", type=int, default=10)
     ap.add_argument("--rlist", type=float, default=1.1, help="buffered list cutoff r_list in nm (config 5 sweep)")
+    ap.add_argument("--rinner", type=float, default=None,
+                    help="dynamic-pruning inner radius in nm (default r_c + 0.02; 0 = off)")
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -82,8 +87,10 @@ def make_params(args, table):
 def config(args, occ, extra=None):
     c = {"workload": f"SPC water {args.atoms // 1000}k atoms, LJ+{ {'ewald': 'Ewald real-space (erfc, beta: erfc(beta rc)=1e-5)', 'rf': 'reaction-field (eps_rf=inf)', 'cutoff': 'shifted cutoff Coulomb (= RF eps_rf=1, reference physics)'}[args.elec]}",
          "n_atoms": args.atoms, "r_cut_nm": R_CUT, "r_list_nm": R_LIST, "cluster_size": M,
-         "nstlist": args.nstlist, "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
+         "nstlist": args.nstlist, "r_inner_nm": getattr(args, "rinner", 0.0) or 0.0, "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
          "positions": "static (search+prune from scratch every nstlist steps, forces every step, energies every nstlist steps)",
+         "dynamic_pruning": ("off" if not getattr(args, "rinner", 0.0) else
+                             "inner force list at r_inner, used while 2 d_max <= r_inner - r_c (device check per call)"),
          "l2": "flushed between steps by a 256 MiB write outside the timed events",
          "parallelism": f"{'replicas' if args.gpus > 1 else 'single'} x{args.gpus}"}
     if extra:
@@ -244,7 +251,8 @@ def run_ours(args):
     def rebuild(pos, q, t, out):
         grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
         st["grid"] = grid
-        st["plist"] = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box)
+        st["plist"] = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box,
+                                          r_inner=args.rinner)
 
     def step(k, pos, q, t, out):
         if k % args.nstlist == 0 or "plist" not in st:
@@ -265,6 +273,9 @@ def run_ours(args):
         raise RuntimeError("singular pair in the benchmark system")
     stats = nbx.interaction_stats(st["plist"], st["grid"], st["grid"].clustered_positions_device, box, R_CUT)
     n_within, n_admitted = stats.n_within_cutoff, stats.n_admitted
+    # pairs the force kernel evaluates (the inner list's under dynamic pruning;
+    # the positions are static, so the inner list stays valid every step)
+    n_force = st["plist"].force_pairs(inner=True)
 
     # ---- device-resident timed region
     W = max(3, args.warmup)
@@ -344,7 +355,7 @@ def run_ours(args):
     peak_tf = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
     fpp = flops_per_pair(params)
     fk_avg_ms = float(fk_ms[0]) / max(1, int(fk_n[0]))
-    achieved = n_admitted * fpp / (fk_avg_ms * 1e-3) / 1e12
+    achieved = n_force * fpp / (fk_avg_ms * 1e-3) / 1e12
     traffic = None
     prof = REPO / "profiles" / "force_kernel_ncu.json"
     if prof.exists():
@@ -361,7 +372,7 @@ def run_ours(args):
         "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
         "config": config(args, occ),
         "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
-        "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted,
+        "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted, "force_kernel": n_force,
                            "admitted_per_s": world * n_admitted * args.steps / (t_ms * 1e-3)},
         "e2e": {"value": world * n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -369,7 +380,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp32", "kernel": "k_force", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
-                     "kernel_ms": fk_avg_ms, "flops_per_pair": fpp,
+                     "kernel_ms": fk_avg_ms, "flops_per_pair": fpp, "pairs": "force_kernel (admitted pairs the kernel evaluates)",
                      "peak_note": f"nominal FP32: {n_sm} SMs x 128 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)"},
         "clocks": clk,
         "wall_s_timed": wall,
@@ -413,7 +424,7 @@ def run_dd(args, world, rank, local):
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
     dd.enable_native()
     p2p = dd.enable_p2p(system.n)  # per-step halo exchanges as NVLink peer stores (NBX_DD_P2P=0: NCCL)
-    df = DomainForces(dd, system, params, M, occ)
+    df = DomainForces(dd, system, params, M, occ, r_inner=args.rinner)
     pos_glob = torch.from_numpy(np.array(system.positions)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     lay = df.rebuild(pos_glob)
@@ -438,6 +449,7 @@ def run_dd(args, world, rank, local):
     cnt = torch.tensor([st.n_within_cutoff, st.n_admitted], dtype=torch.int64, device=dev)
     dist.all_reduce(cnt)
     n_within, n_admitted = int(cnt[0].item()), int(cnt[1].item())
+    n_force_rank = df.plist.force_pairs(inner=True)  # this rank's kernel work (inner list if any)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(local)
     lib.nbx_timing_query(None, None)
@@ -488,7 +500,7 @@ def run_dd(args, world, rank, local):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_tf = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
     fk_avg_ms = float(fk_ms[0]) / max(1, int(fk_n[0]))
-    achieved = st.n_admitted * flops_per_pair(params) / (fk_avg_ms * 1e-3) / 1e12
+    achieved = n_force_rank * flops_per_pair(params) / (fk_avg_ms * 1e-3) / 1e12
     if rank == 0:
         line = {
             "metric": "nonbonded pair-interactions/s (useful, r<=r_c)",
@@ -507,7 +519,8 @@ def run_dd(args, world, rank, local):
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp32", "kernel": "k_force (rank 0)", "achieved": achieved, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None, "kernel_ms": fk_avg_ms,
-                         "flops_per_pair": flops_per_pair(params)},
+                         "flops_per_pair": flops_per_pair(params),
+                         "pairs": "force_kernel of rank 0 (admitted pairs the kernel evaluates)"},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -519,6 +532,8 @@ def main():
     global R_LIST
     args = parse()
     R_LIST = args.rlist
+    if args.rinner is None:
+        args.rinner = min(R_CUT + 0.02, R_LIST)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -117,6 +117,20 @@ int nbx_pairlist_build_pruned(const nbx_grid_t* grid, const double box[3], doubl
 int nbx_pairlist_prune(const nbx_list_t* list, const nbx_grid_t* grid,
                        const double* clustered_positions, const double box[3], void* stream,
                        nbx_list_t** out);
+/* Extension (dynamic pruning, GROMACS-style inner list): the same pruned
+ * list, plus force masks restricted to rows whose FP32 minimum distance at
+ * these positions is <= r_inner (conservative one-sided test).  The canonical
+ * rows are unchanged; nbx_force uses the inner masks while the maximum
+ * displacement since the build satisfies 2 d_max <= r_inner - r_c (checked
+ * on the device every call, full masks otherwise).  r_inner = 0: off
+ * (== nbx_pairlist_prune).  NBX_ERR_PARAM unless 0 < r_inner <= r_list. */
+int nbx_pairlist_prune_inner(const nbx_list_t* list, const nbx_grid_t* grid,
+                             const double* clustered_positions, const double box[3], double r_inner,
+                             void* stream, nbx_list_t** out);
+/* Admitted slot pairs the force kernel evaluates (popcount of the force
+ * masks: the inner list when one exists and `inner` != 0, else the
+ * canonical list); syncs. */
+int nbx_list_force_pairs(nbx_list_t* list, int32_t inner, void* stream, int64_t* n_pairs);
 /* out = {n_i_clusters, n_rows, m, n_groups, n_entries}; never syncs.
  * n_rows is -1 until the canonical rows are materialised (lists hold the
  * grouped entries; the canonical CSR is derived from them on first use,

@@ -30,6 +30,7 @@ EXPORTS = (
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
     "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
     "nbx_dd_assign", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error",
+    "nbx_pairlist_prune_inner", "nbx_list_force_pairs",
 )
 
 
@@ -76,6 +77,8 @@ def load():
         "nbx_pairlist_build_ex": (ctypes.c_int, [P, P, D, P, P, PP]),
         "nbx_pairlist_build_pruned": (ctypes.c_int, [P, P, D, P, P, P, PP]),
         "nbx_pairlist_prune": (ctypes.c_int, [P, P, P, P, P, PP]),
+        "nbx_pairlist_prune_inner": (ctypes.c_int, [P, P, P, P, ctypes.c_double, P, PP]),
+        "nbx_list_force_pairs": (ctypes.c_int, [P, ctypes.c_int32, P, P]),
         "nbx_list_info": (ctypes.c_int, [P, P]),
         "nbx_list_rows": (ctypes.c_int, [P, P, P]),
         "nbx_list_entries": (ctypes.c_int, [P, P, P]),

@@ -50,6 +50,9 @@ struct ForceArgs {
   const int32_t* ent_j;
   const float4* ent_delta;    // j-local -> group-local offset (image included)
   const uint64_t* ent_mask;
+  const uint64_t* ent_fmask;  // k_force_h: inner-list masks (dynamic pruning; NULL: none)
+  const int32_t* ent_fend;    // group -> end of its entries with an inner member
+  float inner_dmax;           // inner masks valid while d_max (scalars[0]) <= this
   const int32_t* ent_tpos;    // k_force_h: entry -> partial-force slot in j-cluster order (NULL: entry order)
   // per-slot inputs
   const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
@@ -927,6 +930,10 @@ k_force_h(const ForceArgs A) {
   float2* s_sh = reinterpret_cast<float2*>(s_dyn + (size_t)FW * tn) + (size_t)w * tn;
   float4* s_lj = s_dyn + (size_t)FW * tn + (FW * tn + 1) / 2 + (size_t)w * IA * A.nt;
   StageH<M, W>& S = s_ws[w].st;
+  // dynamic pruning: the inner list while the atoms have not moved far enough
+  // (since the build) for a dropped row to reach r_c; else the full masks
+  const bool use_inner = A.ent_fmask && __uint_as_float(A.scalars[0]) <= A.inner_dmax;
+  const uint64_t* emask = use_inner ? A.ent_fmask : A.ent_mask;
 
   for (;;) {
     int64_t wi = 0;
@@ -936,7 +943,10 @@ k_force_h(const ForceArgs A) {
     const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
     const int32_t first = A.grp_first[g];
     const int nmem = A.grp_nmem[g];
-    const int32_t e_beg = A.ent_off[g], e_end = A.ent_off[g + 1];
+    // inner list: entries past ent_fend have no member within r_inner, their
+    // j-partials are zero (written below without evaluating them)
+    const int32_t e_beg = A.ent_off[g], e_all = A.ent_off[g + 1];
+    const int32_t e_end = use_inner ? A.ent_fend[g] : e_all;
     const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
 
     // chunk staging: entry fields of chunk c (lanes < CH), j-atoms of chunk
@@ -946,7 +956,7 @@ k_force_h(const ForceArgs A) {
         const int32_t e = min(ec0 + lane, e_last);
         cp_async(&S.ed[slot][lane], A.ent_delta + e, 16);
 #pragma unroll
-        for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], A.ent_mask + (int64_t)e * W + q, 8);
+        for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], emask + (int64_t)e * W + q, 8);
         cp_async(&S.cj[slot][lane], A.ent_j + e, 4);
         if (A.ent_tpos) cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
       }
@@ -1140,6 +1150,13 @@ k_force_h(const ForceArgs A) {
 
     cp_async_wait_all();
     __syncwarp();
+    for (int32_t t = lane; t < (e_all - e_end) * M; t += 32) {  // inner-list tail: zero partials
+      const int32_t e = e_end + t / M;
+      float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)A.ent_tpos[e] * M + t % M) * 3;
+      dst[0] = 0.f;
+      dst[1] = 0.f;
+      dst[2] = 0.f;
+    }
 
     // i-forces: lane holds -F of atoms lane_atom(hl, s, ih) at t = 2 hl + s;
     // sum over the 16 lanes of each half in a fixed order
@@ -1696,6 +1713,11 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     // k_force_h (grouped, m = 4, 8) writes partials in j-cluster order
     const bool sorted_j = !canonical && (m == 4 || m == 8) && !use_legacy_force();
     A.ent_tpos = sorted_j ? wk.t_pos.p : nullptr;
+    // inner list only where it is safe by a margin over FP32 rounding
+    // (r_inner >= r_c + 2e-4 nm); validity is decided on the device
+    A.ent_fmask = (sorted_j && l->r_inner >= p->r_cut + 2e-4 && l->ent_fmask.p) ? l->ent_fmask.p : nullptr;
+    A.ent_fend = l->ent_fend.p;
+    A.inner_dmax = (float)(0.5 * (l->r_inner - p->r_cut) - 5e-5);
     A.xyzq = wk.xyzq.p;
     A.bbox = grid->bbox.p;
     A.type = wk.type.p;

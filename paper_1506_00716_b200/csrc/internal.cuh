@@ -119,6 +119,12 @@ struct List {
   DBuf<float4> ent_delta;    // (n_entries) j-local -> group-local offset, w = slack
   DBuf<uint64_t> ent_mask;    // (n_entries * W), W = 2 for m == 8 else 1
   DBuf<uint16_t> ent_pres;    // (n_entries) members holding a (canonical) row with this j-cluster
+  // dynamic pruning (r_inner > 0): force masks of the inner list -- members
+  // with a pair within r_inner at the prune positions; entries are then
+  // ordered by the inner pattern.  ent_mask stays the canonical r_list list.
+  double r_inner = 0.0;
+  DBuf<uint64_t> ent_fmask;   // (n_entries * W) or empty
+  DBuf<int32_t> ent_fend;     // (n_groups) end of the group's entries with an inner member
   // entries are stored in force order (member pattern) once ordered; the
   // t-th entry of a group in ascending-j order is ent_jorder[t] (empty: identity)
   DBuf<int32_t> ent_jorder;

@@ -615,10 +615,14 @@ __device__ __forceinline__ float prune_r2(const float4& xi, const float4& xj, co
 // member whose minimum falls inside the +-1e-4 band lists its band pairs for
 // the exact FP64 replay -- the same decisions as testing every pair, with a
 // select + min per pair instead of two compares and two selects.
+// hi_in (dynamic pruning, 0: off): a member whose minimum is <= hi_in also
+// gets its bit in `ibits` -- the inner (force) list.  The test is one-sided
+// and conservative (hi_in = r_inner^2 (1 + 1e-4), no FP64 replay): a member
+// left out has no pair within r_inner.
 template <int M, int G, int W, bool MI>
 __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, const uint32_t (&wd)[2 * W],
-                                            const float4& xj, float lo, float hi, const float (&Lf)[3],
-                                            const float (&iLf)[3], uint32_t& inbits, uint32_t& amb) {
+                                            const float4& xj, float lo, float hi, float hi_in, const float (&Lf)[3],
+                                            const float (&iLf)[3], uint32_t& inbits, uint32_t& ibits, uint32_t& amb) {
   constexpr int MM = M * M;
   const float inf = __int_as_float(0x7f800000);
 #pragma unroll
@@ -634,6 +638,7 @@ __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, con
       const float f = prune_r2<M, G, W, MI>(s_xi[k * M + a], xj, Lf, iLf);
       fmin = fminf(fmin, ((cb >> a) & 1u) ? f : inf);
     }
+    if (fmin <= hi_in) ibits |= 1u << k;
     if (fmin < lo) {
       inbits |= 1u << k;
     } else if (fmin <= hi) {  // rare: list the band pairs of this member
@@ -652,7 +657,7 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
                 const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
                 const float4* __restrict__ ent_delta, const uint64_t* __restrict__ ent_mask,
                 const float4* __restrict__ xl, const double* __restrict__ bbox, const double* __restrict__ pos,
-                Box box, double r2, const unsigned int* __restrict__ dmax_bits, float slack_base,
+                Box box, double r2, double r2_inner, const unsigned int* __restrict__ dmax_bits, float slack_base,
                 uint32_t* __restrict__ ent_keep, int32_t* __restrict__ grp_alive) {
   constexpr int R = 32 / M;
   constexpr int IA = G * M;
@@ -663,6 +668,7 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane / M, b = lane % M;
   const float lo = (float)(r2 * (1.0 - 1e-4)), hi = (float)(r2 * (1.0 + 1e-4));
+  const float hi_in = r2_inner > 0.0 ? (float)(r2_inner * (1.0 + 1e-4)) : -1.f;
   const float Lf[3] = {(float)box.L[0], (float)box.L[1], (float)box.L[2]};
   const float iLf[3] = {(float)box.invL[0], (float)box.invL[1], (float)box.invL[2]};
   const float slack_thr = slack_base + 4.f * __uint_as_float(*dmax_bits);
@@ -715,11 +721,11 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (!__any_sync(0xffffffffu, valid[u])) break;
-        uint32_t inbits = 0, amb = 0;
+        uint32_t inbits = 0, ibits = 0, amb = 0;
         if (!__any_sync(0xffffffffu, valid[u] && xj[u].w < slack_thr))
-          prune_batch<M, G, W, false>(s_xi, wd[u], xj[u], lo, hi, Lf, iLf, inbits, amb);
+          prune_batch<M, G, W, false>(s_xi, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
         else
-          prune_batch<M, G, W, true>(s_xi, wd[u], xj[u], lo, hi, Lf, iLf, inbits, amb);
+          prune_batch<M, G, W, true>(s_xi, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
         while (amb) {  // rare: exact FP64 replay of the reference decision
           const int ia = __ffs(amb) - 1;
           amb &= amb - 1;
@@ -727,12 +733,14 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
           if ((inbits >> k) & 1u) continue;
           if (exact_within(pos, (int64_t)first * M + ia, (int64_t)cj[u] * M + b, box, r2)) inbits |= 1u << k;
         }
-        // OR over the entry's M lanes
+        // OR over the entry's M lanes (canonical bits 0..15, inner bits 16..31)
+        uint32_t both = inbits | (ibits << 16);
 #pragma unroll
-        for (int o = 1; o < M; o <<= 1) inbits |= __shfl_xor_sync(0xffffffffu, inbits, o);
+        for (int o = 1; o < M; o <<= 1) both |= __shfl_xor_sync(0xffffffffu, both, o);
+        inbits = both & 0xffffu;
         if (valid[u] && b == 0) {
           if (cj[u] >= first && cj[u] < first + nmem) inbits |= 1u << (cj[u] - first);  // diagonal rows survive
-          ent_keep[e0 + u * PRUNE_WARPS * R + r] = inbits;
+          ent_keep[e0 + u * PRUNE_WARPS * R + r] = inbits | (inbits ? (both & ~0xffffu) : 0u);
         }
         alive += __popc(__ballot_sync(0xffffffffu, valid[u] && b == 0 && inbits != 0u));
       }
@@ -810,7 +818,7 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
                 const uint32_t* __restrict__ ent_keep, const int32_t* __restrict__ ej, const float4* __restrict__ ed, const uint64_t* __restrict__ em,
                 int m, int G, const int32_t* __restrict__ off_out, int32_t* __restrict__ ej2,
                 float4* __restrict__ ed2, uint64_t* __restrict__ em2, uint16_t* __restrict__ ep2,
-                int32_t* __restrict__ jorder2) {
+                int32_t* __restrict__ jorder2, uint64_t* __restrict__ fm2, int32_t* __restrict__ fend) {
   __shared__ uint32_t s_key[ORDER_WARPS][SORT_SMEM];
   __shared__ int32_t s_pos[ORDER_WARPS][SORT_SMEM];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -823,9 +831,12 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
   if (sorted) {
     for (int t = lane; t < n; t += 32) {
       const int64_t e = jorder_in ? jorder_in[e0 + t] : e0 + t;  // t-th entry in ascending j
-      const uint32_t kb = ent_keep[e];
+      const uint32_t kw = ent_keep[e], kb0 = kw & 0xffffu;
+      // fm2 (dynamic pruning): order by the inner (force) pattern, entries
+      // with no inner member last
+      const uint32_t kb = fm2 ? (kw >> 16) & kb0 : kb0;
       uint32_t key = 0xffffffffu;
-      if (kb) {
+      if (kb0) {
         uint64_t mk[2];
         for (int q = 0; q < W; ++q) mk[q] = em[e * W + q];
         if (W == 2) {
@@ -835,6 +846,7 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
           mk[0] &= keep_mask(kb, m, G);
         }
         key = mask_pattern(mk, m, G);
+        if (fm2 && key == 0u) key = 1u << 16;
       }
       s_key[w][t] = key;
     }
@@ -843,10 +855,11 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
     __syncwarp();
   }
   int32_t jr = 0;  // live entries before this chunk (ascending j)
+  int32_t ni = 0;  // live entries with an inner member (sorted before the others)
   for (int base = 0; base < n; base += 32) {
     const int t = base + lane;
     const int64_t e = t < n ? (jorder_in ? jorder_in[e0 + t] : e0 + t) : 0;
-    const uint32_t kb = t < n ? ent_keep[e] : 0u;
+    const uint32_t kw = t < n ? ent_keep[e] : 0u, kb = kw & 0xffffu, ib = (kw >> 16) & kb;
     const unsigned bal = __ballot_sync(0xffffffffu, kb != 0u);
     if (kb) {
       const int32_t rank = jr + __popc(bal & lt);
@@ -854,15 +867,23 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
       ej2[p] = ej[e];
       ed2[p] = ed[e];
       if (W == 2) {
-        for (int q = 0; q < 2; ++q) em2[(int64_t)p * 2 + q] = ((kb >> q) & 1u) ? em[e * 2 + q] : 0ull;
+        for (int q = 0; q < 2; ++q) {
+          em2[(int64_t)p * 2 + q] = ((kb >> q) & 1u) ? em[e * 2 + q] : 0ull;
+          if (fm2) fm2[(int64_t)p * 2 + q] = ((ib >> q) & 1u) ? em[e * 2 + q] : 0ull;
+        }
       } else {
         em2[p] = em[e] & keep_mask(kb, m, G);
+        if (fm2) fm2[p] = em[e] & keep_mask(ib, m, G);
       }
       ep2[p] = (uint16_t)kb;
       jorder2[o0 + rank] = p;
     }
     jr += __popc(bal);
+    ni += __popc(__ballot_sync(0xffffffffu, ib != 0u));
   }
+  // inner-list end of the group: entries past it have no inner member (only
+  // when the group was sorted; very long groups keep j order, no tail)
+  if (fend && lane == 0) fend[g] = o0 + (sorted ? ni : jr);
 }
 
 template <int MODE>
@@ -1008,12 +1029,16 @@ __global__ void k_fill_i32(int32_t* __restrict__ v, int64_t n, int32_t x) {
 }
 
 __global__ void k_group_keys(const int32_t* __restrict__ ent_off, const int32_t* __restrict__ nmem,
-                             int64_t n_groups, int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+                             const int32_t* __restrict__ fend, int64_t n_groups, int32_t* __restrict__ keys,
+                             int32_t* __restrict__ vals) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= n_groups) return;
   // estimated force-kernel cost: per entry ~1/8 of an iteration's fixed work
-  // plus up to nmem member sweeps (measured ratio ~1 : 5 per present member)
-  const int64_t cost = (int64_t)(ent_off[g + 1] - ent_off[g]) * (2 + 5 * (nmem ? nmem[g] : 1));
+  // plus up to nmem member sweeps (measured ratio ~1 : 5 per present member);
+  // with an inner list only its entries are evaluated (the tail is stores)
+  const int32_t e_end = fend ? fend[g] : ent_off[g + 1];
+  const int64_t cost = (int64_t)(e_end - ent_off[g]) * (2 + 5 * (nmem ? nmem[g] : 1)) +
+                       (fend ? (ent_off[g + 1] - e_end) / 4 : 0);
   keys[g] = 0x3fffffff - (int32_t)min(cost, (int64_t)0x3ffffffe);  // ascending key = descending cost
   vals[g] = (int32_t)g;
 }
@@ -1027,8 +1052,8 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
   if ((e = keys.alloc(l->n_groups, s)) || (e = keys2.alloc(l->n_groups, s)) || (e = vals.alloc(l->n_groups, s)))
     return e;
   count_launch();
-  k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->group_nmem.p, l->n_groups, keys.p,
-                                                     vals.p);
+  k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->group_nmem.p, l->ent_fend.p, l->n_groups,
+                                                     keys.p, vals.p);
   e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, 30, s);
   keys.release(s); keys2.release(s); vals.release(s);
   return e;
@@ -1213,6 +1238,7 @@ static void list_release(nbx_list* l, cudaStream_t s) {
   l->group_first.release(s);
   l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
   l->ent_delta.release(s); l->ent_mask.release(s); l->ent_pres.release(s); l->ent_jorder.release(s);
+  l->ent_fmask.release(s); l->ent_fend.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
   w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
@@ -1371,8 +1397,23 @@ fail:
 extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
                                   const double* pos, const double box[3], void* stream,
                                   nbx_list_t** out) {
+  return nbx_pairlist_prune_inner(in, grid, pos, box, 0.0, stream, out);
+}
+
+extern "C" int nbx_pairlist_prune_inner(const nbx_list_t* in, const nbx_grid_t* grid,
+                                        const double* pos, const double box[3], double r_inner, void* stream,
+                                        nbx_list_t** out) {
   if (!in || !grid || !pos || !box || !out) {
     set_error("nbx_pairlist_prune: null argument");
+    return NBX_ERR_PARAM;
+  }
+  if (r_inner != 0.0 && !(r_inner > 0.0 && r_inner <= in->r_list)) {
+    set_error("r_inner must be 0 (off) or in (0, r_list=%g], got %g", in->r_list, r_inner);
+    return NBX_ERR_PARAM;
+  }
+  if (in->m < 4) r_inner = 0.0;  // the inner list feeds k_force_h (m = 4, 8) only
+  if (r_inner != 0.0 && pos != grid->cpos.p) {  // the force pass measures d_max against the build positions
+    set_error("dynamic pruning (r_inner) needs the grid's own build positions");
     return NBX_ERR_PARAM;
   }
   if (grid->n_clusters != in->n_clusters || grid->m != in->m) {
@@ -1387,6 +1428,7 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   l->n_clusters = in->n_clusters;
   l->n_groups = in->n_groups;
   l->r_list = in->r_list;
+  l->r_inner = r_inner;
   l->bbox = in->bbox;
   for (int d = 0; d < 3; ++d) l->L[d] = in->L[d];
   const int W = in->mask_words();
@@ -1408,12 +1450,12 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
                                                        dmax.p);
     const int pblocks = (int)std::min<int64_t>(ng, 148 * 64);
     const float slack_base = (float)(2.0 * in->r_list + 1e-3);
-    const double r2 = in->r_list * in->r_list;
+    const double r2 = in->r_list * in->r_list, r2i = r_inner * r_inner;
 #define NBX_PRUNE(MM, GG)                                                                                     \
   k_prune_entries<MM, GG><<<pblocks, PRUNE_WARPS * 32, 0, s>>>(in->group_first.p, in->group_nmem.p, ng,        \
                                                                in->ent_offsets.p, in->ent_j.p, in->ent_delta.p, \
                                                                in->ent_mask.p, xl.p, grid->bbox.p, pos, bx, r2,  \
-                                                               dmax.p, slack_base, ekeep.p, alive.p)
+                                                               r2i, dmax.p, slack_base, ekeep.p, alive.p)
     switch (in->m) {
       case 1: NBX_PRUNE(1, 16); break;
       case 2: NBX_PRUNE(2, 8); break;
@@ -1438,6 +1480,10 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
   TRY(l->ent_mask.alloc(l->n_entries * W, s));
   TRY(l->ent_pres.alloc(l->n_entries, s));
   TRY(l->ent_jorder.alloc(l->n_entries, s));
+  if (r_inner > 0.0) {
+    TRY(l->ent_fmask.alloc(l->n_entries * W, s));
+    TRY(l->ent_fend.alloc(ng, s));
+  }
   if (ne) count_launch(), k_fill_i32<<<nb(ne, 256), 256, 0, s>>>(l->ent_j.p, ne, (int32_t)nc);
   if (ng) {
     TRY(cudaMemcpyAsync(l->group_first.p, in->group_first.p, 4 * ng, cudaMemcpyDeviceToDevice, s));
@@ -1445,7 +1491,8 @@ extern "C" int nbx_pairlist_prune(const nbx_list_t* in, const nbx_grid_t* grid,
     count_launch();
     k_compact_order<<<nb(ng, ORDER_WARPS), ORDER_WARPS * 32, 0, s>>>(
         in->ent_offsets.p, ng, in->ent_jorder.p, ekeep.p, in->ent_j.p, in->ent_delta.p, in->ent_mask.p, in->m, in->G,
-        l->ent_offsets.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p, l->ent_pres.p, l->ent_jorder.p);
+        l->ent_offsets.p, l->ent_j.p, l->ent_delta.p, l->ent_mask.p, l->ent_pres.p, l->ent_jorder.p,
+        r_inner > 0.0 ? l->ent_fmask.p : nullptr, r_inner > 0.0 ? l->ent_fend.p : nullptr);
   }
   TRY(cudaGetLastError());
   l->entries_ordered = true;
@@ -1489,6 +1536,45 @@ extern "C" int nbx_list_entries(nbx_list_t* l, void* stream, int64_t* n_entries)
     l->entries_exact = true;
   }
   *n_entries = l->n_live >= 0 ? l->n_live : l->n_entries;
+  return NBX_OK;
+}
+
+__global__ void k_popcount_live(const uint64_t* __restrict__ words, int64_t cap, int W,
+                                const int32_t* __restrict__ live, unsigned long long* __restrict__ out) {
+  const int64_t n = min((int64_t)*live * W, cap);
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += __popcll(words[i]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+extern "C" int nbx_list_force_pairs(nbx_list_t* l, int32_t inner, void* stream, int64_t* n_pairs) {
+  if (!l || !n_pairs) {
+    set_error("nbx_list_force_pairs: null argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  const int W = l->mask_words();
+  const uint64_t* words = (inner && l->r_inner > 0.0 && l->ent_fmask.p) ? l->ent_fmask.p : l->ent_mask.p;
+  DBuf<unsigned long long> cnt;
+  unsigned long long h = 0;
+  cudaError_t e;
+  if ((e = cnt.alloc(1, s)) || (e = cudaMemsetAsync(cnt.p, 0, 8, s))) goto out;
+  if (l->n_entries > 0 && l->n_groups > 0) {
+    count_launch();
+    k_popcount_live<<<148 * 4, 256, 0, s>>>(words, l->n_entries * W, W, l->ent_offsets.p + l->n_groups, cnt.p);
+  }
+  if ((e = cudaGetLastError()) || (e = cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaStreamSynchronize(s)))
+    goto out;
+  *n_pairs = (int64_t)h;
+out:
+  cnt.release(s);
+  if (e) {
+    set_error("nbx_list_force_pairs: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
   return NBX_OK;
 }
 

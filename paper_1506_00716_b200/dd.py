@@ -375,7 +375,9 @@ class DomainForces:
     """GPU non-bonded pass of one rank: local grid + halo-masked list, rebuilt
     every nstlist steps; per step halo exchange, force pass, halo reduction."""
 
-    def __init__(self, dd: SlabDecomposition, system, params, m: int = 4, target_occupancy: float | None = None):
+    def __init__(self, dd: SlabDecomposition, system, params, m: int = 4, target_occupancy: float | None = None,
+                 r_inner: float = 0.0):
+        self.r_inner = r_inner  # dynamic pruning (pairlist.prune_pair_list); 0 = off
         self.dd = dd
         self.system = system
         self.params = params
@@ -408,7 +410,8 @@ class DomainForces:
             occ = local_occupancy(occ, n, self.system.n, self.system.box.lengths, w, self.dd.r_comm)
         self.grid = build_cluster_grid(sys_local, self.m, occ, positions=self.local_pos)
         built = build_pair_list(self.grid, self.system.box, self.params.r_list, halo=self.halo)
-        self.plist = prune_pair_list(built, self.grid.clustered_positions_device, self.system.box)
+        self.plist = prune_pair_list(built, self.grid.clustered_positions_device, self.system.box,
+                                     r_inner=self.r_inner)
         self.f = torch.empty((n, 3), dtype=torch.float64, device=dev)
         self.e = torch.zeros(2, dtype=torch.float64, device=dev)
         self.bad = torch.empty(2, dtype=torch.int64, device=dev)

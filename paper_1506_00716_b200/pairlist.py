@@ -72,6 +72,15 @@ class ClusterPairList:
             self._n_entries = int(n.value)
         return self._n_entries
 
+    def force_pairs(self, inner: bool = True) -> int:
+        """Admitted slot pairs the grouped force kernel evaluates: the inner
+        list's when the list was pruned with ``r_inner`` (and ``inner``),
+        else the canonical admitted count (extension; syncs)."""
+        n = ctypes.c_int64()
+        _lib.check(_lib.load().nbx_list_force_pairs(self._h, int(bool(inner)), dev.stream(), ctypes.byref(n)),
+                   "list_force_pairs")
+        return int(n.value)
+
     @property
     def n_pairs(self) -> int:
         if self._n_rows < 0:  # canonical rows are derived from the entries on first use
@@ -221,20 +230,30 @@ def _positions_ptr(plist: ClusterPairList, positions):
     return _lib.ptr(t), t
 
 
-def prune_pair_list(plist: ClusterPairList, positions, box: SimBox) -> ClusterPairList:
+def prune_pair_list(plist: ClusterPairList, positions, box: SimBox, *, r_inner: float = 0.0) -> ClusterPairList:
     """Drop rows whose exact min admitted-slot distance exceeds r_list
-    (pairlist.py:242-282); positions are clustered (n_slots, 3)."""
+    (pairlist.py:242-282); positions are clustered (n_slots, 3).
+
+    ``r_inner`` (extension, dynamic pruning; 0 = off): the force pass also
+    gets an inner list of the rows with a pair within r_inner at these
+    positions (which must be the grid's build positions).  It is used while
+    2 d_max <= r_inner - r_c (checked on the device every force call; the
+    full list otherwise).  The list itself -- offsets, j_idx, masks -- is the
+    same as without it."""
     shape = tuple(positions.shape)
     if shape != (plist.grid.n_slots, 3):
         raise ParameterError(f"positions shape {shape} does not match the list's slot layout "
                              f"{(plist.grid.n_slots, 3)}")
+    if r_inner and not (0.0 < r_inner <= plist.r_list):
+        raise ParameterError(f"r_inner must be 0 (off) or in (0, r_list={plist.r_list}], got {r_inner}")
     if plist._n_entries == 0:  # (-1: pruned list, count on the device -- never empty)
         return plist
     p, keep_alive = _positions_ptr(plist, positions)
     h = ctypes.c_void_p()
     L = _lib.box3(box.lengths)
-    _lib.check(_lib.load().nbx_pairlist_prune(plist.handle, plist.grid.handle, p, _lib.ptr(L), dev.stream(),
-                                              ctypes.byref(h)), "pairlist_prune")
+    _lib.check(_lib.load().nbx_pairlist_prune_inner(plist.handle, plist.grid.handle, p, _lib.ptr(L),
+                                                    float(r_inner), dev.stream(), ctypes.byref(h)),
+               "pairlist_prune")
     del keep_alive
     return ClusterPairList(h, plist.grid, plist.r_list, plist.n_lane, plist.build_step,
                            plist.supercluster_size, plist._build_positions)
