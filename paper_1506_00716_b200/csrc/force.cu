@@ -943,8 +943,9 @@ k_force_h(const ForceArgs A) {
     const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
     const int32_t first = A.grp_first[g];
     const int nmem = A.grp_nmem[g];
-    // inner list: entries past ent_fend have no member within r_inner, their
-    // j-partials are zero (written below without evaluating them)
+    // inner list: entries past ent_fend have no member within r_inner; they
+    // are not evaluated and k_reduce skips their (unwritten) partials (split
+    // transpose: per j-cluster the entries with an inner member come first)
     const int32_t e_beg = A.ent_off[g], e_all = A.ent_off[g + 1];
     const int32_t e_end = use_inner ? A.ent_fend[g] : e_all;
     const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
@@ -1150,13 +1151,6 @@ k_force_h(const ForceArgs A) {
 
     cp_async_wait_all();
     __syncwarp();
-    for (int32_t t = lane; t < (e_all - e_end) * M; t += 32) {  // inner-list tail: zero partials
-      const int32_t e = e_end + t / M;
-      float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)A.ent_tpos[e] * M + t % M) * 3;
-      dst[0] = 0.f;
-      dst[1] = 0.f;
-      dst[2] = 0.f;
-    }
 
     // i-forces: lane holds -F of atoms lane_atom(hl, s, ih) at t = 2 hl + s;
     // sum over the 16 lanes of each half in a fixed order
@@ -1245,18 +1239,29 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
                          const int32_t* __restrict__ t_first, const int32_t* __restrict__ t_items,
                          const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
                          int64_t n_clusters, int m, int flags, double* __restrict__ f_out,
-                         unsigned int* __restrict__ flag) {
+                         unsigned int* __restrict__ flag, int split, float inner_dmax) {
   const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= n_clusters) return;
   const int S = 32 / m;
   const int sidx = lane / m, b = lane - sidx * m;
   double fx = 0.0, fy = 0.0, fz = 0.0;
-  const int32_t t1 = t_first[c + 1];
+  // split transpose (dynamic pruning): 2 n_clusters + 1 bounds, [2c, 2c+1)
+  // the entries with an inner member, [2c+1, 2c+2) the others -- those are
+  // read only when k_force_h evaluated them (full masks: d_max, flag[-1] =
+  // scalars[0], above the inner list's margin)
+  int32_t tb, t1;
+  if (split) {
+    tb = t_first[2 * c];
+    t1 = __uint_as_float(flag[-1]) <= inner_dmax ? t_first[2 * c + 1] : t_first[2 * c + 2];
+  } else {
+    tb = t_first[c];
+    t1 = t_first[c + 1];
+  }
   // U transposed items per lane in flight (index loads, then partial loads);
   // the summation order is unchanged (ascending t per lane)
   constexpr int U = 4;
-  for (int32_t t0 = t_first[c] + sidx; t0 < t1; t0 += S * U) {
+  for (int32_t t0 = tb + sidx; t0 < t1; t0 += S * U) {
     int32_t it[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) it[u] = t0 + u * S < t1 ? (t_items ? __ldg(t_items + t0 + u * S) : t0 + u * S) : -1;
@@ -1577,6 +1582,17 @@ __global__ void k_first_sorted(const int32_t* __restrict__ keys, int64_t n, int6
   for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
 }
 
+// split-transpose keys: 2 j + 1 for entries without an inner member (unused
+// storage slots hold j = n_clusters and sort last either way)
+__global__ void k_split_keys(const int32_t* __restrict__ ej, const uint64_t* __restrict__ fmask, int64_t n, int W,
+                             int32_t* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t any = fmask[i * W];
+  if (W == 2) any |= fmask[i * W + 1];
+  keys[i] = 2 * ej[i] + (any ? 0 : 1);
+}
+
 __global__ void k_inverse(const int32_t* __restrict__ items, int64_t n, int32_t* __restrict__ pos) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) pos[items[i]] = (int32_t)i;
@@ -1666,8 +1682,22 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     wk.t_ready = false;
   }
   if (!canonical && !wk.t_ready) {
-    if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos)))
+    // with an inner list (k_force_h only): key 2 j + (no inner member), so
+    // that k_reduce can stop before the entries k_force_h skipped
+    wk.t_split = l->ent_fmask.p && (m == 4 || m == 8) && !use_legacy_force() && l->n_entries > 0;
+    if (wk.t_split) {
+      DBuf<int32_t> tkeys;
+      if ((e = tkeys.alloc(l->n_entries, s))) goto cuda_fail;
+      count_launch();
+      k_split_keys<<<nb(l->n_entries, 256), 256, 0, s>>>(l->ent_j.p, l->ent_fmask.p, l->n_entries,
+                                                          l->mask_words(), tkeys.p);
+      e = build_transpose(tkeys.p, l->n_entries, 2 * l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos);
+      tkeys.release(s);
+      if (e) goto cuda_fail;
+    } else if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s,
+                                    &wk.t_pos))) {
       goto cuda_fail;
+    }
     wk.t_ready = true;
   }
   if (canonical && (e = ensure_row_delta(l, s))) goto cuda_fail;
@@ -1786,7 +1816,8 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     if (ns > 0)
       count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
                                            canonical ? wk.tc_items.p : (sorted_j ? nullptr : wk.t_items.p), grid->perm.p,
-                                           grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1);
+                                           grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1,
+                                           !canonical && wk.t_split, A.ent_fmask ? A.inner_dmax : -1.f);
     if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
       // nothing else to produce
     } else {

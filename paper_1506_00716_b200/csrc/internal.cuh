@@ -82,6 +82,7 @@ struct ForceWork {
   DBuf<int32_t> t_items;  // (n_entries)
   DBuf<int32_t> t_pos;    // (n_entries) inverse of t_items: entry -> its slot in j-cluster order
   bool t_ready = false;
+  bool t_split = false;   // t_first has 2 n_clusters + 1 bounds (inner-list split, k_reduce)
   DBuf<int32_t> tc_first; // canonical-row transpose
   DBuf<int32_t> tc_items;
   bool tc_ready = false;
