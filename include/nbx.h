@@ -40,8 +40,11 @@ enum {
   NBX_FORCE_ENERGY = 1,      /* compute e_lj / e_coulomb (else e_out untouched)         */
   NBX_FORCE_ACCUMULATE = 2,  /* f_out += forces (compute_nonbonded_into semantics)      */
   NBX_FORCE_CLUSTERED = 4,   /* f_out is (n_slots, 3) in slot order, else (n, 3) original */
-  NBX_FORCE_CANONICAL = 8    /* evaluate the canonical CSR rows (generic kernel) even
+  NBX_FORCE_CANONICAL = 8,   /* evaluate the canonical CSR rows (generic kernel) even
                                 when the grouped fast layout exists (testing aid)      */
+  NBX_FORCE_REPRUNE = 16     /* dynamic pruning, rolling prune: after this pass, redo the
+                                list's inner masks at this call's positions (GROMACS
+                                nstlistPrune); validity is then measured from them  */
 };
 
 typedef struct nbx_grid nbx_grid_t;

@@ -17,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libnbx.so"
 
 NBX_OK, NBX_ERR_PARAM, NBX_ERR_SINGULAR, NBX_ERR_CUDA = 0, 1, 2, 3
 ELEC = {"cutoff": 0, "reaction_field": 1, "ewald": 2}
-FORCE_ENERGY, FORCE_ACCUMULATE, FORCE_CLUSTERED, FORCE_CANONICAL = 1, 2, 4, 8
+FORCE_ENERGY, FORCE_ACCUMULATE, FORCE_CLUSTERED, FORCE_CANONICAL, FORCE_REPRUNE = 1, 2, 4, 8, 16
 
 # every symbol include/nbx.h declares (tests check the exports)
 EXPORTS = (

@@ -52,7 +52,8 @@ struct ForceArgs {
   const uint64_t* ent_mask;
   const uint64_t* ent_fmask;  // k_force_h: inner-list masks (dynamic pruning; NULL: none)
   const int32_t* ent_fend;    // group -> end of its entries with an inner member
-  float inner_dmax;           // inner masks valid while d_max (scalars[0]) <= this
+  float inner_dmax;           // inner masks valid while d_max (scalars[inner_slot]) <= this
+  int inner_slot;             // 0: displacement since the build, 5: since the rolling prune
   const int32_t* ent_tpos;    // k_force_h: entry -> partial-force slot in j-cluster order (NULL: entry order)
   // per-slot inputs
   const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
@@ -932,7 +933,7 @@ k_force_h(const ForceArgs A) {
   StageH<M, W>& S = s_ws[w].st;
   // dynamic pruning: the inner list while the atoms have not moved far enough
   // (since the build) for a dropped row to reach r_c; else the full masks
-  const bool use_inner = A.ent_fmask && __uint_as_float(A.scalars[0]) <= A.inner_dmax;
+  const bool use_inner = A.ent_fmask && __uint_as_float(A.scalars[A.inner_slot]) <= A.inner_dmax;
   const uint64_t* emask = use_inner ? A.ent_fmask : A.ent_mask;
 
   for (;;) {
@@ -1210,9 +1211,10 @@ __global__ void k_gather(const double* __restrict__ pos, const double* __restric
                          const uint8_t* __restrict__ fill, const double* __restrict__ cpos,
                          const double* __restrict__ bbox, int m, int64_t n_slots, Box box,
                          float4* __restrict__ xyzq,
-                         int32_t* __restrict__ type_out, unsigned int* __restrict__ scalars) {
+                         int32_t* __restrict__ type_out, unsigned int* __restrict__ scalars,
+                         const float4* __restrict__ xprune) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  float disp = 0.f;
+  float disp = 0.f, dpr = 0.f;
   if (s < n_slots) {
     const int64_t o = perm[s];
     float v[3];
@@ -1224,11 +1226,20 @@ __global__ void k_gather(const double* __restrict__ pos, const double* __restric
       d2 += (xu - xb) * (xu - xb);
     }
     disp = (float)sqrt(d2);
+    if (xprune) {  // same frames (float), rounded up past the FP32 error
+      const float4 xp = xprune[s];
+      const float ex = v[0] - xp.x, ey = v[1] - xp.y, ez = v[2] - xp.z;
+      dpr = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) * 1.0001f + 1e-6f;
+    }
     xyzq[s] = make_float4(v[0], v[1], v[2], fill[s] ? 0.f : (float)q[o]);
     type_out[s] = (int32_t)typ[o];
   }
   for (int o = 16; o; o >>= 1) disp = fmaxf(disp, __shfl_xor_sync(0xffffffffu, disp, o));
   if ((threadIdx.x & 31) == 0 && disp > 0.f) atomicMax(&scalars[0], __float_as_uint(disp));
+  if (xprune) {
+    for (int o = 16; o; o >>= 1) dpr = fmaxf(dpr, __shfl_xor_sync(0xffffffffu, dpr, o));
+    if ((threadIdx.x & 31) == 0 && dpr > 0.f) atomicMax(&scalars[5], __float_as_uint(dpr));
+  }
 }
 
 // Final per-atom forces: own i-partial + j-partials of every entry whose
@@ -1239,7 +1250,8 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
                          const int32_t* __restrict__ t_first, const int32_t* __restrict__ t_items,
                          const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
                          int64_t n_clusters, int m, int flags, double* __restrict__ f_out,
-                         unsigned int* __restrict__ flag, int split, float inner_dmax) {
+                         unsigned int* __restrict__ flag, int split, float inner_dmax,
+                         const unsigned int* __restrict__ dref) {
   const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= n_clusters) return;
@@ -1248,12 +1260,12 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
   double fx = 0.0, fy = 0.0, fz = 0.0;
   // split transpose (dynamic pruning): 2 n_clusters + 1 bounds, [2c, 2c+1)
   // the entries with an inner member, [2c+1, 2c+2) the others -- those are
-  // read only when k_force_h evaluated them (full masks: d_max, flag[-1] =
-  // scalars[0], above the inner list's margin)
+  // read only when k_force_h evaluated them (full masks: d_max = *dref above
+  // the inner list's margin; inner_dmax < 0 after a rolling prune)
   int32_t tb, t1;
   if (split) {
     tb = t_first[2 * c];
-    t1 = __uint_as_float(flag[-1]) <= inner_dmax ? t_first[2 * c + 1] : t_first[2 * c + 2];
+    t1 = __uint_as_float(*dref) <= inner_dmax ? t_first[2 * c + 1] : t_first[2 * c + 2];
   } else {
     tb = t_first[c];
     t1 = t_first[c + 1];
@@ -1356,7 +1368,8 @@ __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __
 
 __global__ void k_init_scalars(unsigned int* scalars) {
   // [0] max displacement, [1] non-finite flag, [2..3] bad key, [4] work counter
-  if (threadIdx.x < 5) scalars[threadIdx.x] = (threadIdx.x == 2 || threadIdx.x == 3) ? 0xffffffffu : 0u;
+  // [5] max displacement since the rolling prune
+  if (threadIdx.x < 6) scalars[threadIdx.x] = (threadIdx.x == 2 || threadIdx.x == 3) ? 0xffffffffu : 0u;
 }
 
 __global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, int shift,
@@ -1726,7 +1739,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     if (ns > 0)
       count_launch(), k_gather<<<nb(ns, 256), 256, 0, s>>>(positions, charges, lj_type, grid->perm.p, grid->fill.p,
                                            grid->cpos.p, grid->bbox.p, m, ns, bx, wk.xyzq.p, wk.type.p,
-                                           wk.scalars.p);
+                                           wk.scalars.p, canonical ? nullptr : l->xprune.p);
     if (canonical) {
       if (ns > 0 && (e = cudaMemsetAsync(wk.part_i.p, 0, sizeof(float4) * ns, s))) goto cuda_fail;
       if (i_sel && n_items > 0 && (e = cudaMemsetAsync(wk.part_j.p, 0, sizeof(float4) * n_items * m, s))) goto cuda_fail;
@@ -1748,6 +1761,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.ent_fmask = (sorted_j && l->r_inner >= p->r_cut + 2e-4 && l->ent_fmask.p) ? l->ent_fmask.p : nullptr;
     A.ent_fend = l->ent_fend.p;
     A.inner_dmax = (float)(0.5 * (l->r_inner - p->r_cut) - 5e-5);
+    A.inner_slot = l->inner_ref;
     A.xyzq = wk.xyzq.p;
     A.bbox = grid->bbox.p;
     A.type = wk.type.p;
@@ -1817,7 +1831,9 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
       count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
                                            canonical ? wk.tc_items.p : (sorted_j ? nullptr : wk.t_items.p), grid->perm.p,
                                            grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1,
-                                           !canonical && wk.t_split, A.ent_fmask ? A.inner_dmax : -1.f);
+                                           !canonical && wk.t_split,
+                                           (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
+                                           wk.scalars.p + A.inner_slot);
     if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
       // nothing else to produce
     } else {
@@ -1828,6 +1844,10 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
       }
     }
     if ((e = cudaGetLastError())) goto cuda_fail;
+    // rolling prune at this call's coordinates (after the pass that used the old masks)
+    if ((flags & NBX_FORCE_REPRUNE) && sorted_j && l->ent_fmask.p && ns > 0 &&
+        (e = reprune_inner(l, wk.xyzq.p, wk.scalars.p, grid->bbox.p, grid->cpos.p, box, s)))
+      goto cuda_fail;
   }
   return NBX_OK;
 cuda_fail:

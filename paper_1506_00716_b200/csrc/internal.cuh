@@ -126,6 +126,12 @@ struct List {
   double r_inner = 0.0;
   DBuf<uint64_t> ent_fmask;   // (n_entries * W) or empty
   DBuf<int32_t> ent_fend;     // (n_groups) end of the group's entries with an inner member
+  // rolling prune (NBX_FORCE_REPRUNE): inner masks redone in place at later
+  // positions (xprune, the force-frame coordinates of that call); validity is
+  // then measured from xprune (scalars[5]) and no entry tail is skipped
+  DBuf<float4> xprune;
+  int inner_ref = 0;          // scalar slot of the inner list's displacement: 0 build, 5 rolling prune
+  bool tail_sorted = true;    // entries without an inner member sit past ent_fend
   // entries are stored in force order (member pattern) once ordered; the
   // t-th entry of a group in ascending-j order is ent_jorder[t] (empty: identity)
   DBuf<int32_t> ent_jorder;
@@ -150,6 +156,10 @@ struct List;
 cudaError_t finalize_force_layout(List* l, cudaStream_t s);
 cudaError_t ensure_row_delta(List* l, cudaStream_t s);
 cudaError_t ensure_rows(List* l, cudaStream_t s);
+// rolling prune: inner masks of `l` at the force-frame coordinates xyzq
+// (k_gather output; scalars[0] = their max displacement since the build)
+cudaError_t reprune_inner(List* l, const float4* xyzq, const unsigned int* scalars, const double* bbox,
+                          const double* cpos, const double box[3], cudaStream_t s);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

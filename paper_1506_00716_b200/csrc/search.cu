@@ -740,7 +740,7 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
         inbits = both & 0xffffu;
         if (valid[u] && b == 0) {
           if (cj[u] >= first && cj[u] < first + nmem) inbits |= 1u << (cj[u] - first);  // diagonal rows survive
-          ent_keep[e0 + u * PRUNE_WARPS * R + r] = inbits | (inbits ? (both & ~0xffffu) : 0u);
+          ent_keep[e0 + u * PRUNE_WARPS * R + r] = inbits | (both & ~0xffffu);
         }
         alive += __popc(__ballot_sync(0xffffffffu, valid[u] && b == 0 && inbits != 0u));
       }
@@ -1229,6 +1229,63 @@ cudaError_t finalize_force_layout(List* l, cudaStream_t s) {
   return cudaSuccess;
 }
 
+// rolling prune: force masks = canonical masks of the inner members
+__global__ void k_reprune_apply(const uint64_t* __restrict__ em, const uint32_t* __restrict__ keep, int64_t cap,
+                                const int32_t* __restrict__ live, int m, int G, uint64_t* __restrict__ fm) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= cap || e >= *live) return;
+  const uint32_t ib = keep[e] >> 16;
+  if (m == 8) {
+    for (int q = 0; q < 2; ++q) fm[2 * e + q] = ((ib >> q) & 1u) ? em[2 * e + q] : 0ull;
+  } else {
+    fm[e] = em[e] & keep_mask(ib, m, G);
+  }
+}
+
+cudaError_t reprune_inner(List* l, const float4* xyzq, const unsigned int* scalars, const double* bbox,
+                          const double* cpos, const double box[3], cudaStream_t s) {
+  if (!l->ent_fmask.p || l->r_inner <= 0.0 || l->n_groups == 0 || l->n_entries == 0) return cudaSuccess;
+  const int64_t ne = l->n_entries, ng = l->n_groups, ns = l->n_clusters * l->m;
+  DBuf<uint32_t> keep;
+  DBuf<int32_t> alive;
+  cudaError_t e;
+  if ((e = keep.alloc(ne + 1, s)) || (e = alive.alloc(ng + 1, s))) goto out;
+  {
+    Box bx;
+    for (int d = 0; d < 3; ++d) {
+      bx.L[d] = box[d];
+      bx.invL[d] = 1.0 / box[d];
+    }
+    const int pblocks = (int)std::min<int64_t>(ng, 148 * 64);
+    const float slack_base = (float)(2.0 * l->r_list + 1e-3);
+    const double r2i = l->r_inner * l->r_inner;
+    // r2 = 0: only the inner bits are wanted (no canonical decisions, no FP64 replays)
+    count_launch(2);
+#define NBX_REPRUNE(MM, GG)                                                                                   \
+  k_prune_entries<MM, GG><<<pblocks, PRUNE_WARPS * 32, 0, s>>>(l->group_first.p, l->group_nmem.p, ng,         \
+                                                               l->ent_offsets.p, l->ent_j.p, l->ent_delta.p,  \
+                                                               l->ent_mask.p, xyzq, bbox, cpos, bx, 0.0, r2i, \
+                                                               scalars, slack_base, keep.p, alive.p)
+    if (l->m == 4) NBX_REPRUNE(4, 4);
+    else NBX_REPRUNE(8, 2);
+#undef NBX_REPRUNE
+    k_reprune_apply<<<nb(ne, 256), 256, 0, s>>>(l->ent_mask.p, keep.p, ne, l->ent_offsets.p + ng, l->m, l->G,
+                                                 l->ent_fmask.p);
+  }
+  if ((e = cudaGetLastError())) goto out;
+  // every entry is evaluated from now on (the inner pattern changed, the
+  // order did not); validity counts from these coordinates
+  if ((e = cudaMemcpyAsync(l->ent_fend.p, l->ent_offsets.p + 1, 4 * ng, cudaMemcpyDeviceToDevice, s))) goto out;
+  if (!l->xprune.p && (e = l->xprune.alloc(ns, s))) goto out;
+  if ((e = cudaMemcpyAsync(l->xprune.p, xyzq, sizeof(float4) * ns, cudaMemcpyDeviceToDevice, s))) goto out;
+  l->tail_sorted = false;
+  l->inner_ref = 5;
+out:
+  keep.release(s);
+  alive.release(s);
+  return e;
+}
+
 }  // namespace nbx
 
 using namespace nbx;
@@ -1238,7 +1295,7 @@ static void list_release(nbx_list* l, cudaStream_t s) {
   l->group_first.release(s);
   l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
   l->ent_delta.release(s); l->ent_mask.release(s); l->ent_pres.release(s); l->ent_jorder.release(s);
-  l->ent_fmask.release(s); l->ent_fend.release(s);
+  l->ent_fmask.release(s); l->ent_fend.release(s); l->xprune.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
   w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);

@@ -211,10 +211,18 @@ class ListPolicy:
 
     rebuild_interval: int = 10
     prune_on_build: bool = True
+    # dynamic pruning (extension, run_md): inner force list at r_inner built
+    # with each pruned list, redone at the current positions every
+    # prune_interval steps (rolling prune); 0 = off
+    r_inner: float = 0.0
+    prune_interval: int = 0
 
     def __post_init__(self):
         if self.rebuild_interval < 1:
             raise ParameterError(f"rebuild_interval must be >= 1, got {self.rebuild_interval}")
+        if self.r_inner < 0.0 or self.prune_interval < 0:
+            raise ParameterError(f"r_inner and prune_interval must be >= 0, got {self.r_inner}, "
+                                 f"{self.prune_interval}")
 
 
 @dataclass
@@ -432,8 +440,10 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
         d_max = 0.0
 
         def force_pass(energy: bool):
+            age = state.step - state.plist.build_step
+            rp = policy.r_inner > 0.0 and policy.prune_interval > 0 and age > 0 and age % policy.prune_interval == 0
             compute_nonbonded_device(state.plist, state.grid, x, q, ty, params, box, energy=energy, out=f,
-                                     e_out=e, bad=bad)
+                                     e_out=e, bad=bad, reprune=rp)
 
         force_pass(True)
 
@@ -476,7 +486,8 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                                                       supercluster_size=state.plist.supercluster_size,
                                                       n_lane=state.plist.n_lane, build_step=state.step)
                         if policy.prune_on_build and policy.rebuild_interval > 1:
-                            state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box)
+                            state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box,
+                                                          r_inner=min(policy.r_inner, params.r_list))
                     ref.copy_(x)
                     d_max = 0.0
                     state.n_rebuilds += 1

@@ -141,9 +141,14 @@ def compute_nonbonded_device(plist: ClusterPairList, grid: ClusterGrid, position
                              box: SimBox, *, energy: bool = True, clustered: bool = False,
                              out: torch.Tensor | None = None, accumulate: bool = False,
                              e_out: torch.Tensor | None = None, bad: torch.Tensor | None = None,
-                             i_clusters: torch.Tensor | None = None, canonical: bool = False):
+                             i_clusters: torch.Tensor | None = None, canonical: bool = False,
+                             reprune: bool = False):
     """Device-resident force pass.  CUDA tensors in (original order), CUDA
-    tensors out; nothing synchronises.  Returns (forces, energies[2], bad[2])."""
+    tensors out; nothing synchronises.  Returns (forces, energies[2], bad[2]).
+
+    ``reprune`` (dynamic pruning, lists pruned with ``r_inner``): after the
+    pass, redo the inner force list at these positions (rolling prune,
+    GROMACS' nstlistPrune); its validity is then measured from them."""
     d = dev.require_cuda()
     n_out = grid.n_slots if clustered else grid.n
     if out is None:
@@ -156,7 +161,8 @@ def compute_nonbonded_device(plist: ClusterPairList, grid: ClusterGrid, position
     p, table = _params_struct(params)
     L = _lib.box3(box.lengths)
     flags = ((_lib.FORCE_ENERGY if energy else 0) | (_lib.FORCE_ACCUMULATE if accumulate else 0)
-             | (_lib.FORCE_CLUSTERED if clustered else 0) | (_lib.FORCE_CANONICAL if canonical else 0))
+             | (_lib.FORCE_CLUSTERED if clustered else 0) | (_lib.FORCE_CANONICAL if canonical else 0)
+             | (_lib.FORCE_REPRUNE if reprune else 0))
     n_sel = 0 if i_clusters is None else int(i_clusters.numel())
     _lib.check(_lib.load().nbx_force(
         plist.handle, grid.handle, _lib.ptr(positions), _lib.ptr(charges), _lib.ptr(lj_types),

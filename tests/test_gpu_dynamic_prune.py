@@ -107,3 +107,50 @@ def test_inner_list_parameter_errors():
     other = np.array(grid.clustered_positions) + 0.001
     with pytest.raises(nbx.ParameterError):
         nbx.prune_pair_list(built, other, s.box, r_inner=R_INNER)
+
+
+def test_rolling_prune_vs_oracle():
+    """Rolling prune (NBX_FORCE_REPRUNE): after atoms moved past the inner
+    list's margin (fallback pass), the inner list is redone at those
+    positions; a later small move uses it, a large one falls back again --
+    every pass against the oracle on the same canonical list."""
+    import torch
+
+    from oracle import forces as of
+    from oracle import native, search
+
+    nbx, s, table, occ = _spc(24000)
+    L = s.box.lengths
+    grid = nbx.build_cluster_grid(s, 4, occ)
+    pl = nbx.prune_pair_list(nbx.build_pair_list(grid, s.box, 1.1), grid.clustered_positions_device, s.box,
+                             r_inner=R_INNER)
+    n_full = pl.force_pairs(inner=False)
+    params = _params(nbx, table, "ewald")
+    og = search.build_grid(s.positions, L, 4, occ)
+    ol = dict(m=4, offsets=pl.offsets, j_idx=pl.j_idx, masks=pl.masks, r_list=1.1)
+    phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True, elec="ewald",
+                      ewald_beta=of.ewald_beta_for(1.0))
+    dev = torch.device("cuda", 0)
+    q = torch.as_tensor(np.array(s.charges), device=dev)
+    t = torch.as_tensor(np.array(s.lj_type), device=dev)
+    rng = np.random.default_rng(3)
+
+    def moved(base, d):
+        st = rng.normal(size=(s.n, 3))
+        return base + st * (d / np.linalg.norm(st, axis=1, keepdims=True))
+
+    def check(p, reprune=False):
+        f, e, _ = nbx.compute_nonbonded_device(pl, grid, torch.as_tensor(p, device=dev), q, t, params, s.box,
+                                               reprune=reprune)
+        fc, elj, ec = native.list_forces(ol, og, p, s.charges, s.lj_type, L, phys)
+        eh = e.cpu().numpy()
+        assert rel_rms(f.cpu().numpy(), search.scatter_to_original(og, fc)) <= FORCE_RTOL
+        assert rel(eh[0], elj) <= ENERGY_RTOL and rel(eh[1], ec) <= ENERGY_RTOL
+
+    p1 = moved(s.positions, 0.03)
+    check(p1, reprune=True)            # fallback pass, then the inner list is redone at p1
+    assert pl.force_pairs(inner=True) < n_full
+    check(moved(p1, 0.004))            # inner list (from p1) in use
+    p3 = moved(p1, 0.004)
+    check(p3, reprune=True)            # in use, and redone at p3
+    check(moved(p3, 0.03))             # fallback from the p3 prune

@@ -27,6 +27,8 @@ ap.add_argument("--steps", type=int, default=500)
 ap.add_argument("--nstlist", type=int, default=10)
 ap.add_argument("--rlist", type=float, default=1.1)
 ap.add_argument("--json", action="store_true", help="print one JSON summary line last")
+ap.add_argument("--rinner", type=float, default=0.0, help="dynamic pruning inner radius (0 = off)")
+ap.add_argument("--prune-interval", type=int, default=0, help="rolling prune every N steps (0 = off)")
 a = ap.parse_args()
 w, table = spc_water(a.atoms, temperature=300.0)
 o = np.arange(0, w.n, 3)
@@ -35,7 +37,7 @@ s = nbx.ParticleSystem(positions=w.positions[o], velocities=w.velocities[o], mas
 params = nbx.NonbondedParams(r_cut=1.0, r_list=a.rlist, lj_table=table[:1, :1], shift_potential=True)
 layout = nbx.KernelLayout(4, 4)
 occ = tuned_occupancy(s.n, float(s.box.lengths[0]), 4)
-pol = nbx.ListPolicy(rebuild_interval=a.nstlist)
+pol = nbx.ListPolicy(rebuild_interval=a.nstlist, r_inner=a.rinner, prune_interval=a.prune_interval)
 nbx.run_md(s, params, layout, 0.002, 20, policy=pol, report_interval=10, target_occupancy=occ)  # warm-up
 torch.cuda.synchronize()
 t0 = time.perf_counter()
@@ -52,6 +54,6 @@ for k, (cnt, t) in res.timing.sections.items():
 if a.json:
     import json
     print(json.dumps({"tool": "md_bench", "n_atoms": int(s.n), "nstlist": a.nstlist, "r_list_nm": a.rlist,
-                      "steps": a.steps, "ms_per_step": ms, "ns_per_day": 0.002 * a.steps / wall * 86.4,
+                      "steps": a.steps, "r_inner_nm": a.rinner, "prune_interval": a.prune_interval, "ms_per_step": ms, "ns_per_day": 0.002 * a.steps / wall * 86.4,
                       "rebuilds": int(res.state.n_rebuilds), "drift_rebuilds": int(res.state.n_drift_rebuilds),
                       "energy_drift_rel": float(res.energy_drift()[1])}))
