@@ -268,7 +268,8 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
          int64_t cells, Box box, double r_list, SearchOut out, const uint8_t* __restrict__ halo) {
   __shared__ double s_bb[SEARCH_WARPS][GMAX][6];
   __shared__ float4 s_bf[SEARCH_WARPS][GMAX][2];
-  __shared__ int32_t s_q[SEARCH_WARPS][64];
+  constexpr int ZU = 4;  // z-prefilter chunks per pass
+  __shared__ int32_t s_q[SEARCH_WARPS][32 * ZU + 32];
   __shared__ float4 s_xi[SEARCH_WARPS][16];  // fused prune: the group's i-atoms in the group frame
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = blockIdx.x * (int64_t)SEARCH_WARPS + w;
@@ -352,24 +353,39 @@ k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ gr
         const int32_t c0 = col_first[ix * cells + RY.lo[sy]];
         const int32_t c1 = col_first[ix * cells + RY.hi[sy] + 1];
         const int32_t start = c0 > C.first ? c0 : C.first;
-        for (int32_t base = start; base < c1; base += 32) {
-          const int32_t cj = base + lane;
-          bool keep = false;
-          if (cj < c1) {  // conservative FP32 z prefilter against the whole group
-            const float2 z = __ldg(zr + cj);
-            const float gz = gap1f(gzlo, gzhi, z.x, z.y, C.Lf[2]);
-            keep = gz * gz <= r2_pre;
+        // ZU chunks of 32 candidates per pass: their z loads are in flight
+        // together (the scan is a latency chain otherwise); survivors keep
+        // ascending order in the queue, batches of 32 from its front
+        for (int32_t base = start; base < c1; base += 32 * ZU) {
+          bool keep[ZU];
+#pragma unroll
+          for (int u = 0; u < ZU; ++u) {
+            const int32_t cj = base + 32 * u + lane;
+            keep[u] = false;
+            if (cj < c1) {  // conservative FP32 z prefilter against the whole group
+              const float2 z = __ldg(zr + cj);
+              const float gz = gap1f(gzlo, gzhi, z.x, z.y, C.Lf[2]);
+              keep[u] = gz * gz <= r2_pre;
+            }
           }
-          const unsigned kb = __ballot_sync(0xffffffffu, keep);
-          if (keep) s_q[w][qn + __popc(kb & lt)] = cj;
-          qn += __popc(kb);
+#pragma unroll
+          for (int u = 0; u < ZU; ++u) {
+            const unsigned kb = __ballot_sync(0xffffffffu, keep[u]);
+            if (keep[u]) s_q[w][qn + __popc(kb & lt)] = base + 32 * u + lane;
+            qn += __popc(kb);
+          }
           __syncwarp();
-          if (qn >= 32) {
+          while (qn >= 32) {
             process(32);
             __syncwarp();
-            if (lane < qn - 32) s_q[w][lane] = s_q[w][32 + lane];
+            for (int t0 = 0; t0 < qn - 32; t0 += 32) {  // shift the rest to the front
+              const int t = t0 + lane;
+              const int32_t v = t < qn - 32 ? s_q[w][32 + t] : 0;
+              __syncwarp();
+              if (t < qn - 32) s_q[w][t] = v;
+              __syncwarp();
+            }
             qn -= 32;
-            __syncwarp();
           }
         }
       }
