@@ -121,3 +121,22 @@ def test_run_md_drift_guard_rebuilds():
     assert np.all(res.max_drift <= 0.5 * (params.r_list - params.r_cut) + 1e-12)
     with pytest.raises(nbx.ParameterError):
         nbx.run_md(s, params, layout, -1.0, 5)
+
+
+def test_run_md_with_dynamic_pruning_matches_plain_run():
+    """run_md with the inner force list and rolling prunes every 2 steps
+    follows the same trajectory as without (same pairs within r_c; only the
+    FP32 summation order may differ)."""
+    nbx, g, s, params = _fluid("lj_fluid400")
+    layout = nbx.KernelLayout(4, 4)
+    r_inner = params.r_cut + 0.5 * (params.r_list - params.r_cut)
+    a = nbx.run_md(s, params, layout, 0.002, 30, policy=nbx.ListPolicy(rebuild_interval=7), report_interval=10)
+    b = nbx.run_md(s, params, layout, 0.002, 30, report_interval=10,
+                   policy=nbx.ListPolicy(rebuild_interval=7, r_inner=r_inner, prune_interval=2))
+    assert a.state.n_rebuilds == b.state.n_rebuilds
+    dx = nbx.minimum_image(a.state.system.positions - b.state.system.positions, s.box)
+    assert np.abs(dx).max() < 1e-7
+    assert np.allclose(a.e_potential, b.e_potential, rtol=1e-6)
+    assert np.allclose(a.forces.forces, b.forces.forces, rtol=1e-4, atol=1e-5)
+    with pytest.raises(nbx.ParameterError):
+        nbx.ListPolicy(r_inner=-0.1)
