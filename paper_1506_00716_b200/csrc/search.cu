@@ -826,6 +826,42 @@ __device__ __forceinline__ void warp_order(const uint32_t* s_key, int32_t* s_pos
   }
 }
 
+// Same result as warp_order for small key sets (G <= 4: member patterns
+// < 2^G, plus the inner-list tail key 1 << 16): a stable counting sort --
+// per 32-entry chunk one __match_any_sync groups equal keys, bin leaders
+// count, an exclusive scan over the <= 17 bins, then the same pass places.
+// Two passes over the keys instead of two per distinct key.
+__device__ __forceinline__ void warp_order_bins(const uint32_t* s_key, int32_t* s_pos, int n, int lane, int G,
+                                                int32_t* s_cnt) {
+  const int K = (1 << G) + 1;
+  const unsigned lt = (1u << lane) - 1u;
+  if (lane < K) s_cnt[lane] = 0;
+  __syncwarp();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int base = 0; base < n; base += 32) {
+      const int t = base + lane;
+      const uint32_t k = t < n ? s_key[t] : 0xffffffffu;
+      const int bin = k == 0xffffffffu ? -1 : (k >= (1u << G) ? K - 1 : (int)k);
+      const unsigned mm = __match_any_sync(0xffffffffu, bin);
+      if (pass == 1 && bin >= 0) s_pos[t] = s_cnt[bin] + __popc(mm & lt);
+      __syncwarp();
+      if (bin >= 0 && (mm & lt) == 0u) s_cnt[bin] += __popc(mm);  // one leader per bin
+      __syncwarp();
+    }
+    if (pass == 0) {
+      if (lane == 0) {
+        int32_t run = 0;
+        for (int b = 0; b < K; ++b) {
+          const int32_t c = s_cnt[b];
+          s_cnt[b] = run;
+          run += c;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // Pruned list from the keep words: surviving entries of each group written
 // in force order (member pattern of the pruned masks), their masks reduced to
 // the kept members, and the ascending-j index ent_jorder.  One warp per group.
@@ -837,6 +873,7 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
                 int32_t* __restrict__ jorder2, uint64_t* __restrict__ fm2, int32_t* __restrict__ fend) {
   __shared__ uint32_t s_key[ORDER_WARPS][SORT_SMEM];
   __shared__ int32_t s_pos[ORDER_WARPS][SORT_SMEM];
+  __shared__ int32_t s_cnt[ORDER_WARPS][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = blockIdx.x * (int64_t)ORDER_WARPS + w;
   if (g >= n_groups) return;
@@ -867,7 +904,8 @@ k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int3
       s_key[w][t] = key;
     }
     __syncwarp();
-    warp_order(s_key[w], s_pos[w], n, lane);
+    if (G <= 4) warp_order_bins(s_key[w], s_pos[w], n, lane, G, s_cnt[w]);
+    else warp_order(s_key[w], s_pos[w], n, lane);
     __syncwarp();
   }
   int32_t jr = 0;  // live entries before this chunk (ascending j)
