@@ -260,8 +260,11 @@ __device__ __forceinline__ uint32_t prune_bits(uint32_t bits, int32_t cj, const 
 
 // MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
 // by re-running the search for groups whose hits overflowed it).
+#ifndef NBX_SEARCH_MINB
+#define NBX_SEARCH_MINB 6
+#endif
 template <int MODE, bool PRUNE>
-__global__ void __launch_bounds__(SEARCH_WARPS * 32, 6)
+__global__ void __launch_bounds__(SEARCH_WARPS * 32, NBX_SEARCH_MINB)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
          int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
          const float2* __restrict__ zr, const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first,
@@ -667,8 +670,13 @@ __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, con
   }
 }
 
+// 8 resident blocks (<= 64 registers): the kernel is a chain of dependent
+// loads per group, so occupancy hides it (96k: 105 -> 77 us, 1.5M: 1.69 -> 1.12 ms)
+#ifndef NBX_PRUNE_MINB
+#define NBX_PRUNE_MINB 8
+#endif
 template <int M, int G>
-__global__ void __launch_bounds__(PRUNE_WARPS * 32)
+__global__ void __launch_bounds__(PRUNE_WARPS * 32, NBX_PRUNE_MINB)
 k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem, int64_t n_groups,
                 const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
                 const float4* __restrict__ ent_delta, const uint64_t* __restrict__ ent_mask,
@@ -865,7 +873,10 @@ __device__ __forceinline__ void warp_order_bins(const uint32_t* s_key, int32_t* 
 // Pruned list from the keep words: surviving entries of each group written
 // in force order (member pattern of the pruned masks), their masks reduced to
 // the kept members, and the ascending-j index ent_jorder.  One warp per group.
-__global__ void __launch_bounds__(ORDER_WARPS * 32)
+#ifndef NBX_ORDER_MINB
+#define NBX_ORDER_MINB 1
+#endif
+__global__ void __launch_bounds__(ORDER_WARPS * 32, NBX_ORDER_MINB)
 k_compact_order(const int32_t* __restrict__ off_in, int64_t n_groups, const int32_t* __restrict__ jorder_in,
                 const uint32_t* __restrict__ ent_keep, const int32_t* __restrict__ ej, const float4* __restrict__ ed, const uint64_t* __restrict__ em,
                 int m, int G, const int32_t* __restrict__ off_out, int32_t* __restrict__ ej2,
