@@ -109,10 +109,19 @@ k_colsort(const int32_t* __restrict__ sorted, const int32_t* __restrict__ col_at
     const int32_t idx = in_smem ? s_i[w][t] : sorted[a0 + t];
     const double z = in_smem ? s_z[w][t] : wpos[3 * (int64_t)idx + 2];
     int32_t rank = 0;
-    for (int u = 0; u < k; ++u) {
-      const int32_t iu = in_smem ? s_i[w][u] : sorted[a0 + u];
-      const double zu = in_smem ? s_z[w][u] : wpos[3 * (int64_t)iu + 2];
-      rank += (zu < z) || (zu == z && iu < idx);
+    if (in_smem) {  // broadcast shared-memory reads, 8 independent compares in flight
+#pragma unroll 8
+      for (int u = 0; u < k; ++u) {
+        const int32_t iu = s_i[w][u];
+        const double zu = s_z[w][u];
+        rank += (zu < z) || (zu == z && iu < idx);
+      }
+    } else {
+      for (int u = 0; u < k; ++u) {
+        const int32_t iu = sorted[a0 + u];
+        const double zu = wpos[3 * (int64_t)iu + 2];
+        rank += (zu < z) || (zu == z && iu < idx);
+      }
     }
     const int64_t base = (int64_t)cl0 * m;
     const double x0 = wpos[3 * (int64_t)idx], y0 = wpos[3 * (int64_t)idx + 1];
