@@ -39,7 +39,9 @@ __global__ void k_bin(const double* __restrict__ pos, int64_t n, Box box, int64_
   iy = iy < cells - 1 ? iy : cells - 1;
   int32_t cid = (int32_t)(ix * cells + iy);
   cell[i] = cid;
-  atomicAdd(&col_count[cid], 1);
+  // warp-aggregated count: neighbouring atoms mostly share a column
+  const unsigned mm = __match_any_sync(__activemask(), cid);
+  if ((threadIdx.x & 31) == __ffs(mm) - 1) atomicAdd(&col_count[cid], __popc(mm));
 }
 
 __global__ void k_col_clusters(const int32_t* __restrict__ col_count, int64_t n_cols, int m, int G,
@@ -73,8 +75,14 @@ __global__ void k_scatter(const int32_t* __restrict__ cell, int64_t n,
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t c = cell[i];
-  int32_t p = col_atom_first[c] + atomicAdd(&col_fill[c], 1);
-  sorted[p] = (int32_t)i;
+  // warp-aggregated slot claim (the order inside a column is arbitrary here:
+  // k_colsort ranks by (z, index))
+  const unsigned mm = __match_any_sync(__activemask(), c);
+  const int lane = threadIdx.x & 31, leader = __ffs(mm) - 1;
+  int32_t base = 0;
+  if (lane == leader) base = atomicAdd(&col_fill[c], __popc(mm));
+  base = __shfl_sync(mm, base, leader);
+  sorted[col_atom_first[c] + base + __popc(mm & ((1u << lane) - 1u))] = (int32_t)i;
 }
 
 constexpr int COLSORT_WARPS = 4;
