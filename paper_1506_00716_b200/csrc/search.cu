@@ -260,11 +260,13 @@ __device__ __forceinline__ uint32_t prune_bits(uint32_t bits, int32_t cj, const 
 
 // MODE 0: search + count (+ stash hits);  MODE 1: emit (from the stash, or
 // by re-running the search for groups whose hits overflowed it).
+// pass 0 (the scan) at 6 resident blocks; pass 1 (emit from the stash, a
+// load/store chain) at 10 (1.5M: 582 -> ~535 us; pass 0 is slower at 10)
 #ifndef NBX_SEARCH_MINB
 #define NBX_SEARCH_MINB 6
 #endif
 template <int MODE, bool PRUNE>
-__global__ void __launch_bounds__(SEARCH_WARPS * 32, NBX_SEARCH_MINB)
+__global__ void __launch_bounds__(SEARCH_WARPS * 32, MODE == 1 ? 10 : NBX_SEARCH_MINB)
 k_search(const int32_t* __restrict__ group_first, const int32_t* __restrict__ group_nmem,
          int64_t n_groups, int m, int G, const double* __restrict__ bbox, const float4* __restrict__ bbf,
          const float2* __restrict__ zr, const int8_t* __restrict__ nreal, const int32_t* __restrict__ col_first,
