@@ -495,6 +495,7 @@ def run_dd(args, world, rank, local):
     dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     dist.all_reduce(bytes_io)
     e2e_ms = float(t2.item())
+    dd.check_p2p()  # a timed-out peer wait invalidates the run: raise instead of printing a line
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count

@@ -156,6 +156,15 @@ int nbx_super_layout(const nbx_list_t* list, int32_t size, void* stream, int64_t
  * super_pair_idx (n_entries*size, -1 = absent); syncs */
 int nbx_super_download(const nbx_list_t* list, int64_t* super_offsets, int64_t* super_j,
                        int64_t* super_pair_idx, void* stream);
+/* Per-row diagnostics of pairlist.write_pairs_csv (pairlist.py:349-376):
+ * gap_sq[r] = periodic bounding-box gap^2 of row r (gridder.py:165-185),
+ * min_d2[r] = exact FP64 minimum admitted slot distance^2 at `positions`
+ * (device clustered (n_slots, 3) f64; NULL = the grid's build positions),
+ * +inf for rows with no admitted slot pair (_pair_min_dist_sq,
+ * pairlist.py:220-239).  Both outputs: device (n_rows) f64, bit-identical to
+ * the reference's values.  Materialises the canonical rows (syncs once). */
+int nbx_list_diagnostics(nbx_list_t* list, const nbx_grid_t* grid, const double* positions,
+                         const double box[3], double* gap_sq, double* min_d2, void* stream);
 /* pairlist.interaction_stats / _count_within (pairlist.py:303-346):
  * out = {n_admitted, n_within_cutoff} at clustered_positions; syncs */
 int nbx_count_within(const nbx_list_t* list, const double* clustered_positions,

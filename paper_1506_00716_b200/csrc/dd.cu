@@ -166,6 +166,13 @@ extern "C" int nbx_dd_set_layout(nbx_dd_t* d, const int64_t* send_local, int64_t
     set_error("nbx_dd_set_layout: bad argument");
     return NBX_ERR_PARAM;
   }
+  if (d->p2p && (n_send > d->cap || n_halo > d->cap)) {
+    // the peer regions hold cap rows each (nbx_dd_p2p_alloc); a larger layout
+    // would write past them into the peer's flags
+    set_error("nbx_dd_set_layout: n_send=%lld / n_halo=%lld exceed the P2P capacity %lld", (long long)n_send,
+              (long long)n_halo, (long long)d->cap);
+    return NBX_ERR_PARAM;
+  }
   cudaStream_t s = to_stream(stream);
   cudaError_t e;
   if (d->send_local.n < n_send && (e = d->send_local.alloc(n_send, s))) goto fail;
@@ -426,8 +433,7 @@ static cudaError_t select_flagged(const int64_t* in, const uint8_t* flags, int64
   cudaError_t e = cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, n_out, (int)n, s);
   if (e) return e;
   void* tmp = nullptr;
-  nbx::ensure_pool();
-  if ((e = cudaMallocAsync(&tmp, bytes, s))) return e;
+  if ((e = pool_malloc(&tmp, bytes, s))) return e;
   e = cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out, n_out, (int)n, s);
   cudaFreeAsync(tmp, s);
   return e;

@@ -1725,7 +1725,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     key.push_back(p->r_cut);
     key.push_back((double)p->shift_potential);
     if (key != wk.lj_key) {
-      if ((e = cudaMallocAsync(reinterpret_cast<void**>(&dtab), sizeof(double) * 2 * nt * nt, s))) goto cuda_fail;
+      if ((e = pool_malloc(reinterpret_cast<void**>(&dtab), sizeof(double) * 2 * nt * nt, s))) goto cuda_fail;
       if ((e = cudaMemcpyAsync(dtab, p->lj_table, sizeof(double) * 2 * nt * nt, cudaMemcpyHostToDevice, s))) goto cuda_fail;
       count_launch();
       k_build_lj<<<nb(nt * nt, 64), 64, 0, s>>>(dtab, nt, p->r_cut * p->r_cut, p->shift_potential, wk.lj.p);

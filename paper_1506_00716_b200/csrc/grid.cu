@@ -202,29 +202,51 @@ void nbx::set_error(const char* fmt, ...) {
 extern "C" const char* nbx_last_error(void) { return g_err; }
 extern "C" int nbx_version(void) { return 1; }
 
-void nbx::ensure_pool() {
-  static thread_local int done_dev = -1;
+// The library's own stream-ordered pool per device (never the device's
+// default pool, whose attributes other cudaMallocAsync users in the process --
+// torch's async allocator -- would inherit).  Release threshold = max, so
+// freed blocks stay mapped across syncs, and pre-grown once so rebuilds do not
+// map new pages in the middle of a step.  A 1.5M-atom list generation needs
+// several GB (54 M built rows, 18 M entries + their partial forces); the
+// default reserve is 24 GB (NBX_POOL_GB), capped at 40 % of free memory.
+cudaMemPool_t nbx::device_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    // pre-grow the pool once (kept: threshold = max) so rebuilds do not map
-    // new pages in the middle of a step.  A 1.5M-atom list generation needs
-    // several GB (54 M built rows, 18 M entries + their partial forces); the
-    // default reserve is 24 GB (NBX_POOL_GB), capped at 40 % of free memory.
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    double gb = 24.0;
-    if (const char* e = getenv("NBX_POOL_GB")) gb = atof(e);
-    size_t want = (size_t)(gb * (double)(size_t(1) << 30));
-    if (want > free_b / 10 * 4) want = free_b / 10 * 4;
-    void* p = nullptr;
-    if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) cudaFreeAsync(p, 0);
-    cudaStreamSynchronize(0);
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (pools[dev]) return pools[dev];
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  double gb = 24.0;
+  if (const char* e = getenv("NBX_POOL_GB")) gb = atof(e);
+  size_t want = (size_t)(gb * (double)(size_t(1) << 30));
+  if (want > free_b / 10 * 4) want = free_b / 10 * 4;
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+    if (want > 0 && cudaMallocFromPoolAsync(&p, want, pool, s) == cudaSuccess) cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
   }
-  done_dev = dev;
+  cudaGetLastError();
+  pools[dev] = pool;
+  return pool;
+}
+
+cudaError_t nbx::pool_malloc(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = device_pool();
+  if (!pool) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 static std::atomic<int64_t> g_launches{0};

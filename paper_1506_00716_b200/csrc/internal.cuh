@@ -10,10 +10,12 @@
 
 namespace nbx {
 
-// Keep freed stream-ordered memory in the device pool across syncs (the
-// default release threshold of 0 returns it to the driver at every sync and
-// makes the next cudaMallocAsync re-map pages -- milliseconds per rebuild).
-void ensure_pool();
+// The library's private stream-ordered pool on the current device (grid.cu):
+// freed memory stays mapped across syncs (the default release threshold of 0
+// returns it to the driver at every sync and makes the next allocation re-map
+// pages -- milliseconds per rebuild).  All library allocations go through it.
+cudaMemPool_t device_pool();
+cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s);
 
 // Device buffer with stream-ordered allocation.
 template <typename T>
@@ -24,8 +26,7 @@ struct DBuf {
     release(s);
     n = count;
     if (count <= 0) return cudaSuccess;
-    ensure_pool();
-    return cudaMallocAsync(reinterpret_cast<void**>(&p), size_class(sizeof(T) * (size_t)count), s);
+    return pool_malloc(reinterpret_cast<void**>(&p), size_class(sizeof(T) * (size_t)count), s);
   }
   // round up to {1, 1.25, 1.5, 1.75} x 2^k so that the per-rebuild buffers of
   // slightly different sizes reuse the same pool blocks

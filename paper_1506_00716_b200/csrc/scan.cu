@@ -12,8 +12,7 @@ cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaS
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int)n, s);
   if (e != cudaSuccess) return e;
   void* tmp = nullptr;
-  ensure_pool();
-  e = cudaMallocAsync(&tmp, bytes, s);
+  e = pool_malloc(&tmp, bytes, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)n, s);
   cudaFreeAsync(tmp, s);
@@ -28,8 +27,7 @@ cudaError_t sort_pairs_i32(const int32_t* keys_in, int32_t* keys_out, const int3
                                                   vals_out, (int)n, 0, end_bit, s);
   if (e != cudaSuccess) return e;
   void* tmp = nullptr;
-  ensure_pool();
-  e = cudaMallocAsync(&tmp, bytes, s);
+  e = pool_malloc(&tmp, bytes, s);
   if (e != cudaSuccess) return e;
   e = cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0,
                                       end_bit, s);

@@ -1809,7 +1809,7 @@ extern "C" int nbx_super_layout(const nbx_list_t* lc, int32_t size, void* stream
   if (nr) {
     count_launch(), k_super_keys<<<nb(nr, 256), 256, 0, s>>>(ci_of_row.p, l->j.p, nr, size, nc, keys.p, vals.p);
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)nr, 0, 64, s));
-    TRY(cudaMallocAsync(&tmp, bytes, s));
+    TRY(pool_malloc(&tmp, bytes, s));
     TRY(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys.p, keys2.p, vals.p, vals2.p, (int)nr, 0, 64, s));
     cudaFreeAsync(tmp, s);
   }
@@ -1855,4 +1855,62 @@ extern "C" int nbx_super_download(const nbx_list_t* l, int64_t* super_offsets, i
     return NBX_ERR_CUDA;
   }
   return NBX_OK;
+}
+
+// ---------------------------------------------------------------- row diagnostics
+// pairlist.write_pairs_csv (pairlist.py:349-376) computes, per canonical row,
+// the periodic bounding-box gap (gridder.py:165-185) and the exact minimum
+// admitted slot distance at the build positions (_pair_min_dist_sq,
+// pairlist.py:220-239: numpy min image, einsum order, +inf when no slot pair
+// is admitted).  One thread per row, the reference's FP64 operation order
+// (this TU is compiled with -fmad=false): the values are bit-identical, so
+// the CSV text is too.
+__global__ void k_row_diag(const int32_t* __restrict__ ci_of_row, const int32_t* __restrict__ jv,
+                           const uint64_t* __restrict__ mask, int64_t n_rows, int m, const double* __restrict__ bbox,
+                           const double* __restrict__ pos, Box box, double* __restrict__ gap_sq,
+                           double* __restrict__ min_d2) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int64_t ci = ci_of_row[r], cj = jv[r];
+  gap_sq[r] = nbx::gap_sq(bbox + 6 * ci, bbox + 6 * cj, box);
+  const uint64_t mk = mask[r];
+  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (int a = 0; a < m; ++a) {
+    const double* pi = pos + 3 * (ci * m + a);
+    for (int b = 0; b < m; ++b) {
+      if (!((mk >> (a * m + b)) & 1ull)) continue;
+      const double* pj = pos + 3 * (cj * m + b);
+      const double dx = min_image_np(__dsub_rn(pi[0], pj[0]), box.L[0], box.invL[0]);
+      const double dy = min_image_np(__dsub_rn(pi[1], pj[1]), box.L[1], box.invL[1]);
+      const double dz = min_image_np(__dsub_rn(pi[2], pj[2]), box.L[2], box.invL[2]);
+      const double d2 = d2_einsum(dx, dy, dz);
+      best = d2 < best ? d2 : best;
+    }
+  }
+  min_d2[r] = best;
+}
+
+extern "C" int nbx_list_diagnostics(nbx_list_t* l, const nbx_grid_t* grid, const double* positions,
+                                    const double box[3], double* gap_sq, double* min_d2, void* stream) {
+  if (!l || !grid || !box || !gap_sq || !min_d2 || grid->m != l->m || grid->n_clusters != l->n_clusters) {
+    set_error("nbx_list_diagnostics: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  DBuf<int32_t> ci;
+  const double* pos = positions ? positions : grid->cpos.p;
+  TRY(ensure_rows(l, s));
+  if (l->n_rows > 0) {
+    TRY(ci.alloc(l->n_rows, s));
+    count_launch(2);
+    k_row_ci<<<nb(l->n_clusters, 256), 256, 0, s>>>(l->offsets.p, l->n_clusters, ci.p);
+    k_row_diag<<<nb(l->n_rows, 256), 256, 0, s>>>(ci.p, l->j.p, l->mask.p, l->n_rows, l->m, grid->bbox.p, pos,
+                                                   make_box(box), gap_sq, min_d2);
+    TRY(cudaGetLastError());
+  }
+  ci.release(s);
+  return NBX_OK;
+fail:
+  ci.release(s);
+  return NBX_ERR_CUDA;
 }

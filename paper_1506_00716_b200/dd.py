@@ -154,6 +154,15 @@ class SlabDecomposition:
         self.p2p = True
         return True
 
+    def check_p2p(self) -> None:
+        """Raise when a peer wait timed out since the exchanges started (the
+        halo rows or the returned face forces of some step were then stale).
+        Called where the host synchronises anyway: every list rebuild
+        (DomainForces.rebuild) and the end of a run (bench.py)."""
+        if self.p2p_error():
+            raise RuntimeError(f"rank {self.rank}: NVLink peer exchange timed out (a neighbour stalled for > 5 s); "
+                               "forces since the last check are invalid")
+
     def p2p_error(self) -> bool:
         """True when a peer wait timed out (host sync)."""
         if not getattr(self, "p2p", False):
@@ -166,14 +175,25 @@ class SlabDecomposition:
         _lib.check(_lib.load().nbx_dd_p2p_error(self._native, ctypes.byref(out)), "dd_p2p_error")
         return out.value != 0
 
-    def __del__(self):
+    def close(self) -> None:
+        """Free the native communicator (collective under NCCL; idempotent)."""
         h = getattr(self, "_native", None)
-        if h is not None:
+        self._native = None
+        if h is None:
+            return
+        try:
             from . import _lib
+        except ImportError:  # interpreter shutdown: module globals already gone
+            return
+        lib = getattr(_lib, "_lib", None)
+        if lib is not None:
+            lib.nbx_dd_free(h)
 
-            if _lib._lib is not None:
-                _lib._lib.nbx_dd_free(h)
-            self._native = None
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # never raise from a finaliser (interpreter exit)
+            pass
 
     # ---------------------------------------------------------------- geometry
     def owner(self, x) -> np.ndarray:
@@ -389,6 +409,7 @@ class DomainForces:
     def rebuild(self, positions_global: torch.Tensor) -> DomainLayout:
         from . import build_cluster_grid, build_pair_list, prune_pair_list
 
+        self.dd.check_p2p()
         lay = self.dd.assign(positions_global)
         dev = positions_global.device
         ids = lay.local_ids

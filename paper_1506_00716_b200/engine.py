@@ -3,8 +3,7 @@ drop-in for the hot-path part of clustermd.engine.
 
 Mirrors /root/reference/pkg/src/clustermd/engine.py: ``ListPolicy``,
 ``MDState``, ``init_state`` (:337-384), ``lifecycle_tick`` (:387-406),
-``parallel_forces`` (:462-521), ``velocity_verlet_step`` (:543-580) and the
-slab bookkeeping (:141-263) that the multi-GPU decomposition (dd.py) reuses;
+``parallel_forces`` (:462-521) and ``velocity_verlet_step`` (:543-580);
 ``DriftTracker`` / ``update_drift`` mirror oracle.py:88-123.
 
 The force pass is one GPU launch sequence whatever ``workers`` is: the
@@ -120,90 +119,6 @@ def update_drift(tracker: DriftTracker, current_positions, box: SimBox) -> Drift
                         max_displacement=max(tracker.max_displacement, largest))
 
 
-# ---------------------------------------------------------------- slabs (host bookkeeping)
-@dataclass
-class SlabPartition:
-    """1D decomposition along x (engine.py:141-160)."""
-
-    boundaries: np.ndarray
-    min_width: float
-    assignments: np.ndarray
-    last_timings: np.ndarray | None = None
-
-    @property
-    def n_slabs(self) -> int:
-        return self.boundaries.shape[0] - 1
-
-    def widths(self) -> np.ndarray:
-        return np.diff(self.boundaries)
-
-
-def _unit_centers_x(grid: ClusterGrid, supercluster_size: int) -> np.ndarray:
-    centers = grid.cluster_centers()[:, 0]
-    if supercluster_size == 1:
-        return centers
-    n_groups = -(-grid.n_clusters // supercluster_size)
-    return np.array([centers[g * supercluster_size:(g + 1) * supercluster_size].mean() for g in range(n_groups)])
-
-
-def assign_slabs(boundaries: np.ndarray, centers_x: np.ndarray) -> np.ndarray:
-    """Slab per unit centre; boundary centres go right (engine.py:176-179)."""
-    idx = np.searchsorted(boundaries[1:-1], centers_x, side="right")
-    return np.clip(idx, 0, boundaries.shape[0] - 2).astype(np.int64)
-
-
-def build_slab_partition(box_length_x: float, n_slabs: int, min_width: float, grid: ClusterGrid | None = None,
-                         supercluster_size: int = 1) -> SlabPartition:
-    """Equal-width initial partition (engine.py:182-205)."""
-    if n_slabs < 1:
-        raise ParameterError(f"n_slabs must be >= 1, got {n_slabs}")
-    if min_width <= 0.0 or n_slabs * min_width > box_length_x:
-        raise ParameterError(f"{n_slabs} slabs of minimum width {min_width} do not fit in box length {box_length_x}")
-    boundaries = np.linspace(0.0, box_length_x, n_slabs + 1)
-    boundaries[-1] = box_length_x
-    assignments = (assign_slabs(boundaries, _unit_centers_x(grid, supercluster_size))
-                   if grid is not None else np.empty(0, dtype=np.int64))
-    return SlabPartition(boundaries=boundaries, min_width=float(min_width), assignments=assignments)
-
-
-def rebalance_slabs(partition: SlabPartition, timings, alpha: float = 0.5, grid: ClusterGrid | None = None,
-                    supercluster_size: int = 1) -> SlabPartition:
-    """Widths scaled by t_mean/t_i, renormalised, clamped to min_width,
-    blended by alpha (engine.py:208-263)."""
-    t = np.asarray(timings, dtype=np.float64)
-    n = partition.n_slabs
-    if t.shape != (n,):
-        raise ParameterError(f"expected {n} timings, got shape {t.shape}")
-    if np.any(t <= 0.0) or not np.all(np.isfinite(t)):
-        raise ParameterError("per-slab timings must be positive and finite")
-    if not (0.0 < alpha <= 1.0):
-        raise ParameterError(f"alpha must be in (0, 1], got {alpha}")
-    span = float(partition.boundaries[-1] - partition.boundaries[0])
-    old = partition.widths()
-    prop = old * (t.mean() / t)
-    prop *= span / prop.sum()
-    free = np.ones(n, dtype=bool)
-    for _ in range(n):
-        clamped = free & (prop < partition.min_width)
-        if not np.any(clamped):
-            break
-        free &= ~clamped
-        prop[~free] = partition.min_width
-        rest = span - partition.min_width * np.count_nonzero(~free)
-        if np.any(free):
-            prop[free] *= rest / prop[free].sum()
-    widths = alpha * prop + (1.0 - alpha) * old
-    b = np.empty(n + 1)
-    b[0] = partition.boundaries[0]
-    np.cumsum(widths, out=b[1:])
-    b[1:] += partition.boundaries[0]
-    b[-1] = partition.boundaries[-1]
-    assignments = partition.assignments
-    if grid is not None:
-        assignments = assign_slabs(b, _unit_centers_x(grid, supercluster_size))
-    return SlabPartition(boundaries=b, min_width=partition.min_width, assignments=assignments)
-
-
 # ---------------------------------------------------------------- lifecycle
 @dataclass
 class ListPolicy:
@@ -236,7 +151,7 @@ class MDState:
     drift: DriftTracker
     n_rebuilds: int = 0
     n_drift_rebuilds: int = 0
-    slabs: SlabPartition | None = None
+    slabs: object | None = None  # always None: see init_state
     target_occupancy: float | None = None
 
 
@@ -246,7 +161,9 @@ def _build(system, params, m, supercluster_size, n_lane, step, policy, occupancy
     plist = build_pair_list(grid, system.box, params.r_list, supercluster_size=supercluster_size,
                             n_lane=n_lane, build_step=step)
     if policy.prune_on_build and policy.rebuild_interval > 1:
-        plist = prune_pair_list(plist, grid.clustered_positions_device, system.box)
+        # the same inner list (dynamic pruning) as run_md's rebuilds
+        plist = prune_pair_list(plist, grid.clustered_positions_device, system.box,
+                                r_inner=min(policy.r_inner, params.r_list))
     return grid, plist
 
 
@@ -257,14 +174,6 @@ def _rebuild(state: MDState, params: NonbondedParams, policy: ListPolicy, timer)
                                          state.plist.n_lane, state.step, policy, state.target_occupancy)
     state.drift = DriftTracker(reference_positions=wrap_position(state.system.positions, state.system.box))
     state.n_rebuilds += 1
-    if state.slabs is not None:
-        t = state.slabs.last_timings
-        if t is not None and np.all(t > 0.0):
-            state.slabs = rebalance_slabs(state.slabs, t, grid=state.grid,
-                                          supercluster_size=state.plist.supercluster_size)
-        else:
-            state.slabs.assignments = assign_slabs(state.slabs.boundaries,
-                                                   _unit_centers_x(state.grid, state.plist.supercluster_size))
 
 
 def init_state(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout, *,
@@ -278,10 +187,11 @@ def init_state(system: ParticleSystem, params: NonbondedParams, layout: KernelLa
     state = MDState(system=system, step=0, grid=grid, plist=plist,
                     drift=DriftTracker(reference_positions=wrap_position(system.positions, system.box)),
                     n_rebuilds=1, target_occupancy=target_occupancy)
-    if n_slabs > 0:
-        width = params.r_list if slab_min_width is None else slab_min_width
-        state.slabs = build_slab_partition(float(system.box.lengths[0]), n_slabs, width, grid=grid,
-                                           supercluster_size=supercluster_size)
+    if n_slabs < 0:
+        raise ParameterError(f"n_slabs must be >= 0, got {n_slabs}")
+    # n_slabs / slab_min_width are accepted for signature compatibility: one
+    # GPU pass needs no work slabs, and the multi-GPU decomposition is
+    # dd.SlabDecomposition (with its own cost-quantile rebalancing)
     return state
 
 
@@ -308,8 +218,6 @@ def parallel_forces(state: MDState, params: NonbondedParams, layout: KernelLayou
     s = state.system
     res = compute_nonbonded_original(state.plist, state.grid, s.positions, s.charges, s.lj_type, params, s.box,
                                      layout)
-    if state.slabs is not None:
-        state.slabs.last_timings = np.ones(state.slabs.n_slabs)
     return res
 
 

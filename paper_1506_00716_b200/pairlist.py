@@ -8,7 +8,6 @@ super layout) on first access, set-identical to the reference.
 
 from __future__ import annotations
 
-import csv
 import ctypes
 from dataclasses import dataclass
 
@@ -291,21 +290,40 @@ def interaction_stats(plist: ClusterPairList, grid: ClusterGrid, positions, box:
     return InteractionStats(n_admitted=n_adm, n_within_cutoff=n_win, ratio=ratio)
 
 
+def pair_diagnostics(plist: ClusterPairList, grid: ClusterGrid, box: SimBox):
+    """Per-row (bbox gap^2, exact minimum admitted slot distance^2) at the
+    list's build positions, computed on the GPU (nbx_list_diagnostics) with
+    the reference's FP64 operation order: bit-identical to gridder.bbox_gap_sq
+    and pairlist._pair_min_dist_sq (pairlist.py:220-239, :349-360).
+    Returns two float64 numpy arrays of length n_pairs."""
+    n = plist.n_pairs
+    if n == 0:
+        return np.empty(0), np.empty(0)
+    if plist._build_positions is None:
+        p, keep_alive = ctypes.c_void_p(0), None
+    else:
+        p, keep_alive = _positions_ptr(plist, plist._build_positions)
+    out = torch.empty((2, n), dtype=torch.float64, device=dev.require_cuda())
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_list_diagnostics(plist.handle, grid.handle, p, _lib.ptr(L), _lib.ptr(out[0]),
+                                                _lib.ptr(out[1]), dev.stream()), "list_diagnostics")
+    del keep_alive
+    host = out.cpu().numpy()
+    return host[0], host[1]
+
+
 def write_pairs_csv(plist: ClusterPairList, grid: ClusterGrid, box: SimBox, path) -> None:
-    """Per-row diagnostics CSV (pairlist.py:349-376): bbox vs exact distance."""
-    ci = plist.pair_i_clusters()
-    pos = plist.build_positions.reshape(-1, plist.m, 3)
+    """Per-row diagnostics CSV (pairlist.py:349-376): bbox vs exact distance.
+
+    The distances come from the GPU (pair_diagnostics, bit-identical values);
+    the host only formats them, with the reference's csv dialect and
+    ``repr`` of each float, so the file is byte-identical."""
+    gap_sq, min_d2 = pair_diagnostics(plist, grid, box)
+    ci = plist.pair_i_clusters().tolist() if plist.n_pairs else []
+    cj = plist.j_idx.tolist() if plist.n_pairs else []
+    gap = np.sqrt(gap_sq).tolist()
+    finite = np.isfinite(min_d2)
+    exact = np.where(finite, np.sqrt(np.where(finite, min_d2, 0.0)), np.nan).tolist()
     with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(["i_cluster", "j_cluster", "bbox_distance_nm", "exact_min_distance_nm"])
-        for p in range(plist.n_pairs):
-            lo_i, hi_i = grid.bboxes[ci[p]]
-            lo_j, hi_j = grid.bboxes[plist.j_idx[p]]
-            gap = float(np.sqrt(bbox_gap_sq(lo_i, hi_i, lo_j, hi_j, box.lengths)))
-            dr = pos[ci[p]][:, None, :] - pos[plist.j_idx[p]][None, :, :]
-            dr = dr - np.floor(dr / box.lengths + 0.5) * box.lengths
-            d2 = np.einsum("abd,abd->ab", dr, dr)
-            d2[~plist.masks[p]] = np.inf
-            mn = float(d2.min())
-            w.writerow([int(ci[p]), int(plist.j_idx[p]), repr(gap),
-                        repr(float(np.sqrt(mn))) if np.isfinite(mn) else repr(float("nan"))])
+        fh.write("i_cluster,j_cluster,bbox_distance_nm,exact_min_distance_nm\r\n")
+        fh.writelines(f"{a},{b},{g!r},{e!r}\r\n" for a, b, g, e in zip(ci, cj, gap, exact))

@@ -1,6 +1,6 @@
 """Generate golden vectors by running the REAL reference (build container only).
 
-    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [--large]
 
 Imports clustermd read-only from /root/reference/pkg/src, runs its public API
 (build_cluster_grid, build_pair_list, prune_pair_list, interaction_stats,
@@ -142,5 +142,118 @@ def main():
     print("scalars:", e, fr, g.perm.tolist())
 
 
+def digest(*arrays) -> str:
+    """SHA-256 over the arrays' bytes in a fixed dtype per array (see callers)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def list_digest(plist) -> str:
+    return digest(np.asarray(plist.offsets, dtype=np.int64), np.asarray(plist.j_idx, dtype=np.int64),
+                  pack_bits(plist.masks))
+
+
+def dump_large(name, n, *, m, tuned, r_cut=1.0, r_list=1.1, seed=2024, f64=False):
+    """BASELINE-size case (24k / 96k SPC water): the reference's grid, built
+    and pruned lists and counts as SHA-256 digests (the arrays are tens of MB),
+    its forces in original order and its energies.  Positions are regenerated
+    by systems.spc_water(n, seed) on the test side and pinned by their digest."""
+    import time
+
+    system, tab = spc(n, seed)
+    L = float(system.box.lengths[0])
+    occ = tuned_occupancy(n, L, m) if tuned else None
+    params = cm.NonbondedParams(r_cut=r_cut, r_list=r_list, lj_table=tab, shift_potential=True)
+    box = system.box
+    t0 = time.time()
+    grid = cm.build_cluster_grid(system, m, target_occupancy=occ)
+    built = cm.build_pair_list(grid, box, r_list, n_lane=m)
+    pruned = cm.prune_pair_list(built, grid.clustered_positions, box)
+    layout = cm.KernelLayout(m=m, n_lane=m)
+    res = cm.compute_nonbonded_original(pruned, grid, system.positions, system.charges, system.lj_type,
+                                        params, box, layout)
+    stats = cm.interaction_stats(pruned, grid, grid.clustered_positions, box, r_cut)
+    out = dict(
+        n=n, seed=seed, m=m, r_cut=r_cut, r_list=r_list, shift=1,
+        occupancy=np.nan if occ is None else occ, box=box.lengths,
+        positions_digest=digest(np.asarray(system.positions, dtype=np.float64)),
+        n_clusters=grid.n_clusters, n_slots=grid.perm.shape[0],
+        grid_digest=digest(np.asarray(grid.perm, dtype=np.int64), np.asarray(grid.fill_mask, dtype=np.bool_),
+                           np.asarray(grid.cell_of_cluster, dtype=np.int64),
+                           np.asarray(grid.bboxes, dtype=np.float64)),
+        perm_digest=digest(np.asarray(grid.perm, dtype=np.int64)),
+        bbox_digest=digest(np.asarray(grid.bboxes, dtype=np.float64)),
+        built_rows=built.n_pairs, built_digest=list_digest(built),
+        pruned_rows=pruned.n_pairs, pruned_digest=list_digest(pruned),
+        pruned_offsets_digest=digest(np.asarray(pruned.offsets, dtype=np.int64)),
+        n_admitted=stats.n_admitted, n_within=stats.n_within_cutoff,
+        f_original=res.forces if f64 else res.forces.astype(np.float32),
+        e_lj=res.e_lj, e_coulomb=res.e_coulomb,
+    )
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(f"{name}: n={n} clusters={grid.n_clusters} built={built.n_pairs} pruned={pruned.n_pairs} "
+          f"admitted={stats.n_admitted} within={stats.n_within_cutoff} ({time.time() - t0:.1f} s)", flush=True)
+
+
+def main_large():
+    """24k (config 2 geometry) with both grid rules, 96k (config 3) tuned and
+    default (the needle-cluster multi-image case) and 96k m = 8."""
+    dump_large("spc24k_default", 24000, m=4, tuned=False, f64=True)
+    dump_large("spc24k_tuned", 24000, m=4, tuned=True, f64=True)
+    dump_large("spc96k_tuned", 96000, m=4, tuned=True)
+    dump_large("spc96k_tuned_m8", 96000, m=8, tuned=True)
+    dump_large("spc96k_default", 96000, m=4, tuned=False)
+
+
+def dump_diagnostics():
+    """Reference outputs of the diagnostics row: the
+    write_pairs_csv file (SHA-256 of its bytes), flop_count for several
+    kernel layouts, and scatter_to_original of a seeded per-slot array."""
+    import hashlib
+    import tempfile
+
+    out = {}
+    cases = [("spc3k_tuned", 4), ("spc3k_default", 4), ("uniform_m8", 8), ("uniform_m2", 2), ("uniform_super8", 4)]
+    for name, m in cases:
+        with np.load(HERE / f"{name}.npz") as z:
+            g = {k: z[k] for k in z.files}
+        n = g["positions"].shape[0]
+        system = cm.ParticleSystem(positions=g["positions"], velocities=np.zeros((n, 3)), masses=g["masses"],
+                                   charges=g["charges"], lj_type=g["lj_type"], box=cm.SimBox(g["box"]))
+        occ = None if np.isnan(g["occupancy"]) else float(g["occupancy"])
+        grid = cm.build_cluster_grid(system, m, target_occupancy=occ)
+        built = cm.build_pair_list(grid, system.box, float(g["r_list"]), supercluster_size=int(g["supercluster"]))
+        pruned = cm.prune_pair_list(built, grid.clustered_positions, system.box)
+        for tag, pl in (("built", built), ("pruned", pruned)):
+            with tempfile.TemporaryDirectory() as d:
+                path = Path(d) / "pairs.csv"
+                cm.write_pairs_csv(pl, grid, system.box, path)
+                out[f"{name}_{tag}_csv_sha256"] = hashlib.sha256(path.read_bytes()).hexdigest()
+        layouts = [(m, nl) for nl in (1, 2, 4, 8)]
+        fl = np.array([[nl, cm.flop_count(pruned, grid, cm.KernelLayout(m=m, n_lane=nl), system.box,
+                                          float(g["r_cut"])).total_flops,
+                        cm.flop_count(pruned, grid, cm.KernelLayout(m=m, n_lane=nl), system.box,
+                                      float(g["r_cut"])).useful_flops] for _, nl in layouts], dtype=np.int64)
+        out[f"{name}_flops"] = fl
+        rng = np.random.default_rng(99)
+        vals = rng.normal(size=(grid.n_slots, 3))
+        out[f"{name}_scatter_in"] = vals
+        out[f"{name}_scatter_out"] = cm.scatter_to_original(grid, vals)
+        print(name, "csv", out[f"{name}_pruned_csv_sha256"][:12], "flops", fl.tolist())
+    np.savez_compressed(HERE / "diagnostics.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if "--large" in sys.argv:
+        main_large()
+    elif "--diagnostics" in sys.argv:
+        dump_diagnostics()
+    else:
+        main()

@@ -158,3 +158,35 @@ def test_rf_eps1_equals_shifted_cutoff_and_ewald_dimer():
     e = lambda rr: float(of.pair_terms(rr * rr, 0, 0, 1.0, 1.0, ew)[1])
     fnum = -(e(r + h) - e(r - h)) / (2 * h) / r
     assert float(of.pair_terms(r * r, 0, 0, 1.0, 1.0, ew)[2]) == pytest.approx(fnum, rel=1e-7)
+
+
+# ---------------------------------------------------------------- BASELINE sizes (24k / 96k)
+from conftest import digest, grid_digest, large_golden_names, large_system, list_digest  # noqa: E402
+
+
+@pytest.mark.parametrize("name", large_golden_names())
+def test_large_fixture_oracle(name):
+    """The oracle's C port reproduces the reference at the BASELINE sizes:
+    grid and built / pruned lists bit-identical (SHA-256 of the reference's
+    arrays), admitted / within counts equal, forces to FP64 rounding."""
+    g = load_golden(name)
+    s, table, occ = large_system(g)
+    L = s.box.lengths
+    m = int(g["m"])
+    grid = search.build_grid(s.positions, L, m, occ)
+    assert grid_digest(grid["perm"], grid["fill_mask"], grid["cell_of_cluster"], grid["bboxes"]) == str(g["grid_digest"])
+    built = native.search_list(grid, L, float(g["r_list"]), method="cols")
+    assert list_digest(built["offsets"], built["j_idx"], search.pack_masks(built["masks"])) == str(g["built_digest"])
+    pruned = native.prune_list(built, grid["clustered_positions"], L)
+    assert list_digest(pruned["offsets"], pruned["j_idx"], search.pack_masks(pruned["masks"])) == \
+        str(g["pruned_digest"])
+    assert int(search.unpack_masks(search.pack_masks(pruned["masks"]), m).sum()) == int(g["n_admitted"])
+    assert native.count_within(pruned, grid["clustered_positions"], L, float(g["r_cut"])) == int(g["n_within"])
+    phys = of.Physics(r_cut=float(g["r_cut"]), lj_table=table, shift_potential=bool(g["shift"]))
+    fc, elj, ec = native.list_forces(pruned, grid, s.positions, s.charges, s.lj_type, L, phys)
+    f = search.scatter_to_original(grid, fc)
+    ref = g["f_original"].astype(np.float64)
+    tol = 1e-12 if g["f_original"].dtype == np.float64 else 1e-6  # 96k fixtures store FP32 forces
+    assert np.sqrt(((f - ref) ** 2).sum() / (ref ** 2).sum()) <= tol
+    assert abs(elj - float(g["e_lj"])) <= 1e-12 * abs(float(g["e_lj"]))
+    assert abs(ec - float(g["e_coulomb"])) <= 1e-12 * abs(float(g["e_coulomb"]))
