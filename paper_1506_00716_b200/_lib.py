@@ -7,13 +7,16 @@ device is visible, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 from .model import ParameterError, SingularityError
 
-LIB_PATH = Path(__file__).resolve().parent / "libnbx.so"
+# NBX_LIB: an alternative build of the same library (A/B kernel variants,
+# tools/build_variant.sh); default the in-tree libnbx.so
+LIB_PATH = Path(os.environ.get("NBX_LIB") or (Path(__file__).resolve().parent / "libnbx.so"))
 
 NBX_OK, NBX_ERR_PARAM, NBX_ERR_SINGULAR, NBX_ERR_CUDA = 0, 1, 2, 3
 ELEC = {"cutoff": 0, "reaction_field": 1, "ewald": 2}
