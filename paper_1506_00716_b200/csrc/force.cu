@@ -936,37 +936,19 @@ k_force_h(const ForceArgs A) {
   const bool use_inner = A.ent_fmask && __uint_as_float(A.scalars[A.inner_slot]) <= A.inner_dmax;
   const uint64_t* emask = use_inner ? A.ent_fmask : A.ent_mask;
 
-  // work items (groups, LPT order) are claimed one ahead: the next claim and
-  // its descriptor loads are issued while the current group runs, so their
-  // latency (an atomic, then two dependent loads) leaves the critical path
-  struct Desc {
-    int64_t wi;
-    int32_t first, nmem, e_beg, e_end;
-  };
-  auto load_desc = [&](int64_t wi) {
-    Desc d{wi, 0, 0, 0, 0};
-    if (wi < A.n_work) {
-      const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
-      d.first = A.grp_first[g];
-      d.nmem = A.grp_nmem[g];
-      // inner list: entries past ent_fend have no member within r_inner; they
-      // are not evaluated and k_reduce skips their (unwritten) partials (split
-      // transpose: per j-cluster the entries with an inner member come first)
-      d.e_beg = A.ent_off[g];
-      d.e_end = use_inner ? A.ent_fend[g] : A.ent_off[g + 1];
-    }
-    return d;
-  };
-  unsigned int claim = 0;
-  if (lane == 0) claim = atomicAdd(A.scalars + 4, 1u);
-  Desc cur = load_desc((int64_t)__shfl_sync(0xffffffffu, claim, 0));
   for (;;) {
-    if (cur.wi >= A.n_work) break;
-    if (lane == 0) claim = atomicAdd(A.scalars + 4, 1u);
-    const int64_t wi = cur.wi;
-    const int32_t first = cur.first;
-    const int nmem = cur.nmem;
-    const int32_t e_beg = cur.e_beg, e_end = cur.e_end;
+    int64_t wi = 0;
+    if (lane == 0) wi = (int64_t)atomicAdd(A.scalars + 4, 1u);
+    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if (wi >= A.n_work) break;
+    const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
+    const int32_t first = A.grp_first[g];
+    const int nmem = A.grp_nmem[g];
+    // inner list: entries past ent_fend have no member within r_inner; they
+    // are not evaluated and k_reduce skips their (unwritten) partials (split
+    // transpose: per j-cluster the entries with an inner member come first)
+    const int32_t e_beg = A.ent_off[g], e_all = A.ent_off[g + 1];
+    const int32_t e_end = use_inner ? A.ent_fend[g] : e_all;
     const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
 
     // chunk staging: entry fields of chunk c (lanes < CH), j-atoms of chunk
@@ -978,7 +960,7 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
         for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], emask + (int64_t)e * W + q, 8);
         cp_async(&S.cj[slot][lane], A.ent_j + e, 4);
-        cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
+        if (A.ent_tpos) cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
       }
     };
     auto stage_jatoms = [&](int xslot, int eslot) {
@@ -988,7 +970,6 @@ k_force_h(const ForceArgs A) {
         const int ent = rem / JP, b = 2 * (rem - ent * JP) + q;
         cp_async(&S.xj[xslot][f], A.xyzq + (int64_t)S.cj[eslot][ent] * M + b, 16);
       }
-      // types [entry][M]: one 16-byte copy per 4 atoms (lane -> entry, quarter)
       const int te = lane / (M / 4), tq = lane % (M / 4);
       cp_async(&S.tj[xslot][te * M + tq * 4], A.type + (int64_t)S.cj[eslot][te] * M + tq * 4, 16);
     };
@@ -1046,6 +1027,7 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
     for (int h = 0; h < 4; ++h) fi[h][0] = fi[h][1] = fi[h][2] = make_float2(0.f, 0.f);
     double elj_acc = 0.0, ec_acc = 0.0;
+    float4* pj = A.part_j + (int64_t)(e_beg + r) * M + ba;
     const int sha_ = 8 * ih * (W == 1) + 32 * ih * (W == 2) + 2 * jp;  // mask shift of the lane's pairs
 
     int es = 0;
@@ -1071,7 +1053,7 @@ k_force_h(const ForceArgs A) {
       es = es == 2 ? 0 : es + 1;
       const int32_t c_end = min(ec0 + CH, e_end);
 #pragma unroll 1
-    for (int32_t e0 = ec0, ci = 0; e0 < c_end; e0 += R, ci += R) {
+    for (int32_t e0 = ec0, ci = 0; e0 < c_end; e0 += R, ci += R, pj += R * M) {
       const bool valid = e0 + r < e_end;
       const int ce = ci + r;  // entry within the chunk
       const float4 d = c_ed[ce];
@@ -1149,12 +1131,16 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) out[c] = fj[0][c] + __shfl_xor_sync(0xffffffffu, fj[1][c], 16);
       if (valid) {
-        // partials land in j-cluster order (t_pos, always set for this
-        // kernel), so k_reduce streams them (packed xyz, 12 B per partial)
-        float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)c_tp[ce] * M + ba) * 3;
-        dst[0] = out[0];
-        dst[1] = out[1];
-        dst[2] = out[2];
+        // partials land in j-cluster order (t_pos), so k_reduce streams them
+        // (packed xyz, 12 B per partial: a quarter less traffic than float4)
+        if (A.ent_tpos) {
+          float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)c_tp[ce] * M + ba) * 3;
+          dst[0] = out[0];
+          dst[1] = out[1];
+          dst[2] = out[2];
+        } else {
+          *pj = make_float4(out[0], out[1], out[2], 0.f);
+        }
       }
       if (ENERGY) {
         elj_acc += (double)elj;
@@ -1165,7 +1151,6 @@ k_force_h(const ForceArgs A) {
 
     cp_async_wait_all();
     __syncwarp();
-    const Desc nxt = load_desc((int64_t)__shfl_sync(0xffffffffu, claim, 0));
 
     // i-forces: lane holds -F of atoms lane_atom(hl, s, ih) at t = 2 hl + s;
     // sum over the 16 lanes of each half in a fixed order
@@ -1214,7 +1199,6 @@ k_force_h(const ForceArgs A) {
       }
     }
     __syncwarp();
-    cur = nxt;
   }
 }
 
