@@ -2,37 +2,50 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--atoms 96000] [--elec ewald|rf|cutoff] [--nstlist 10] [--rlist 1.1]
+                    [--positions moving|static] [--rinner R]
 
-One STEP = one MD step of the non-bonded hot path: every `nstlist` steps the
-grid, the cluster-pair search and the prune are redone from scratch at the
-current positions, and every step runs the force + energy pass.  Positions
-are static (the reference's SPC water has no exclusions/constraints, so its
-MD diverges -- SURVEY.md 0.3); nothing is cached across rebuilds.
+One STEP = one MD step of the non-bonded hot path on MOVING positions
+(default): the atoms follow a deterministic trajectory (every water molecule
+oscillates rigidly about its start with amplitude 0.025 nm and a period of
+40-80 steps: an MD stand-in -- the reference's SPC water has no exclusions or
+constraints, so real dynamics of it diverge), the list
+lifecycle of run_md runs on the device (rebuild -- grid, cluster-pair search,
+prune from scratch -- every nstlist steps or when the drift guard
+2 d_max > r_list - r_c fires, one scalar read per step), and every step runs
+the force pass (energies every nstlist steps).  --positions static keeps the
+box fixed (the r01 configuration).
 
 value   = useful pair interactions (admitted slot pairs with r <= r_c) per
           second, whole job, inputs resident in HBM, per-step CUDA events,
           L2 flushed (256 MiB write) between steps outside the timed events.
-e2e     = the same metric with host (pinned) positions/charges/types copied
-          H2D and forces + energies copied D2H inside every timed step.
+e2e     = the same metric through the drop-in API a reference user calls:
+          compute_nonbonded_original with numpy host arrays every step,
+          build_cluster_grid / build_pair_list / prune_pair_list on a
+          ParticleSystem every nstlist steps; wall clock per step (host
+          conversions, H2D of positions / charges / types, D2H of forces and
+          energies included).  e2e_pinned: the device API with pinned host
+          buffers copied in and out every step (CUDA events).
 roofline= the force kernel (k_force) against the FP32 pipe peak
           (148 SMs x 128 lanes x 2 flop x sm_max_mhz from MEASURED_PEAKS.json),
           flops = admitted slot pairs the kernel evaluates x per-pair cost
-          (kernels.FLOPS_PER_PAIR = 40, +12 for Ewald).  With dynamic
-          pruning (--rinner, default r_c + 0.02 nm; 0 = off) those are the
-          inner list's pairs (pairs_per_step.force_kernel), not the r_list
-          list's (pairs_per_step.admitted).
+          (kernels.FLOPS_PER_PAIR = 40, +12 for Ewald), kernel time from
+          CUDA events around every launch of K force passes on the moved
+          positions.  Dynamic pruning (--rinner > 0) is off by default for
+          moving positions (the inner list is invalidated within a few steps
+          of motion) and r_c + 0.02 nm for static ones.
 cpu_baseline = the reference algorithm's CPU port (oracle/, FP64, all host
           threads) on the same system: one rebuild + one force pass.
---impl reference: that CPU port timed for W + K steps (rank 0 only).
+--impl reference: that CPU port timed for W + K steps of the same
+          trajectory (rank 0 only).
 """
 
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 from pathlib import Path
@@ -57,7 +70,9 @@ def parse():
     ap.add_argument("--nstlist", type=int, default=10)
     ap.add_argument("--rlist", type=float, default=1.1, help="buffered list cutoff r_list in nm (config 5 sweep)")
     ap.add_argument("--rinner", type=float, default=None,
-                    help="dynamic-pruning inner radius in nm (default r_c + 0.02; 0 = off)")
+                    help="dynamic-pruning inner radius in nm (default: off for moving positions, r_c + 0.02 "
+                         "for static; 0 = off)")
+    ap.add_argument("--positions", default="moving", choices=["moving", "static"])
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -72,6 +87,46 @@ def workload(args):
     return system, table, occ
 
 
+AMP_NM = 0.025  # trajectory amplitude: 10-step displacement <= 0.035 nm < (r_list - r_c) / 2
+
+
+class Trajectory:
+    """Deterministic MD stand-in: molecule m (atoms 3m..3m+2, rigid) moves as
+    x0 + A (sin(w_m k + p_m) - sin(p_m)) u_m, u_m a random unit vector,
+    w_m in [2 pi / 80, 2 pi / 40] per step.  x(0) = x0; any 10-step window
+    moves an atom by at most 2 A sin(10 w / 2) < 0.035 nm, so interval
+    rebuilds alone keep the list valid (the drift guard still runs)."""
+
+    def __init__(self, system, static=False, seed=7):
+        n = system.n
+        rng = np.random.default_rng(seed)
+        nmol = (n + 2) // 3
+        u = rng.normal(size=(nmol, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        self.u = np.repeat(u, 3, axis=0)[:n]
+        self.w = np.repeat(rng.uniform(2 * np.pi / 80, 2 * np.pi / 40, nmol), 3)[:n]
+        self.p = np.repeat(rng.uniform(0, 2 * np.pi, nmol), 3)[:n]
+        self.x0 = np.array(system.positions)
+        self.static = static
+
+    def host(self, k):
+        if self.static:
+            return self.x0
+        s = AMP_NM * (np.sin(self.w * k + self.p) - np.sin(self.p))
+        return self.x0 + s[:, None] * self.u
+
+    def to_device(self, dev, steps):
+        """Materialise the positions of trajectory steps `steps` in HBM (the
+        stand-in for the integrator's output: no per-step kernel)."""
+        import torch
+
+        self.dev_pos = {k: torch.from_numpy(self.host(k)).to(dev) for k in steps}
+
+    def device(self, k, out=None):
+        """positions of step k (device tensor)."""
+        return self.dev_pos[k]
+
+
 def make_params(args, table):
     import paper_1506_00716_b200 as nbx
 
@@ -84,60 +139,118 @@ def make_params(args, table):
     return nbx.NonbondedParams(r_cut=R_CUT, r_list=R_LIST, lj_table=table, shift_potential=True)
 
 
+def workload_name(args):
+    elec = {"ewald": "Ewald real-space (erfc, beta: erfc(beta rc)=1e-5)", "rf": "reaction-field (eps_rf=inf)",
+            "cutoff": "shifted cutoff Coulomb (= RF eps_rf=1, reference physics)"}[args.elec]
+    return f"SPC water {args.atoms // 1000}k atoms, LJ+{elec}"
+
+
+def positions_note(args):
+    if args.positions == "static":
+        return "static (search+prune from scratch every nstlist steps, forces every step, energies every nstlist steps)"
+    return (f"moving: rigid molecules oscillating about their start (amplitude {AMP_NM} nm, period 40-80 steps; "
+            "MD stand-in); list rebuilt from scratch every nstlist steps or when the drift guard fires, "
+            "forces every step, energies every nstlist steps")
+
+
 def config(args, occ, extra=None):
-    c = {"workload": f"SPC water {args.atoms // 1000}k atoms, LJ+{ {'ewald': 'Ewald real-space (erfc, beta: erfc(beta rc)=1e-5)', 'rf': 'reaction-field (eps_rf=inf)', 'cutoff': 'shifted cutoff Coulomb (= RF eps_rf=1, reference physics)'}[args.elec]}",
+    """config of our arm (GPU)."""
+    c = {"workload": workload_name(args),
          "n_atoms": args.atoms, "r_cut_nm": R_CUT, "r_list_nm": R_LIST, "cluster_size": M,
-         "nstlist": args.nstlist, "r_inner_nm": getattr(args, "rinner", 0.0) or 0.0, "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
-         "positions": "static (search+prune from scratch every nstlist steps, forces every step, energies every nstlist steps)",
+         "nstlist": args.nstlist, "r_inner_nm": getattr(args, "rinner", 0.0) or 0.0,
+         "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
+         "positions": positions_note(args),
          "dynamic_pruning": ("off" if not getattr(args, "rinner", 0.0) else
                              "inner force list at r_inner, used while 2 d_max <= r_inner - r_c (device check per call)"),
          "l2": "flushed between steps by a 256 MiB write outside the timed events",
-         "parallelism": f"{'replicas' if args.gpus > 1 else 'single'} x{args.gpus}"}
+         "parallelism": f"{'slab DD' if args.gpus > 1 else 'single GPU'} x{args.gpus}"}
     if extra:
         c.update(extra)
     return c
 
 
+def config_reference(args, occ, threads):
+    """config of the reference arm: the oracle's C port of the reference CPU
+    path -- no dynamic pruning, no GPU, no cache flush."""
+    return {"workload": workload_name(args), "n_atoms": args.atoms, "r_cut_nm": R_CUT, "r_list_nm": R_LIST,
+            "cluster_size": M, "nstlist": args.nstlist,
+            "grid_occupancy": args.occupancy if occ is None else f"tuned ({occ:.1f})",
+            "positions": positions_note(args),
+            "impl": ("oracle/ C port of the reference CPU path (FP64; grid numpy, O(n_c^2) search, prune and "
+                     f"blocked force kernel in C with OpenMP on {threads} host threads)"),
+            "parallelism": f"CPU x{threads} threads"}
+
+
 # ---------------------------------------------------------------- clocks
 class Clocks:
+    """SM clock + clock-event reasons sampled through NVML every ~5 ms on a
+    background thread while the timed region runs (also one sample at start
+    and one at stop, so short multi-rank regions always have records).  The
+    NVML device is the one this rank's CUDA device maps to (by UUID)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
     def __init__(self, idx):
-        self.proc = None
-        self.path = REPO / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+        import threading
+
+        self.samples, self.reasons, self.max_mhz = [], set(), 0.0
+        self.h = None
         try:
-            self.path.parent.mkdir(exist_ok=True)
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(idx), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = self._handle(pynvml, torch, idx)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
         except Exception:
-            self.proc = None
+            self.h = None
+            return
+        self._stop = threading.Event()
+        self._sample()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    @staticmethod
+    def _handle(nv, torch, idx):
+        """NVML handle of CUDA device idx: matched by UUID (robust to
+        CUDA_VISIBLE_DEVICES and to the enumeration order)."""
+        want = str(torch.cuda.get_device_properties(idx).uuid).lower()
+        want = want[4:] if want.startswith("gpu-") else want
+        for i in range(nv.nvmlDeviceGetCount()):
+            h = nv.nvmlDeviceGetHandleByIndex(i)
+            u = nv.nvmlDeviceGetUUID(h)
+            u = (u.decode() if isinstance(u, bytes) else str(u)).lower()
+            if (u[4:] if u.startswith("gpu-") else u) == want:
+                return h
+        return nv.nvmlDeviceGetHandleByIndex(idx)
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for name, const in self.REASONS.items():
+            if bits & getattr(nv, const):
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.wait(0.005):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def stop(self):
-        if self.proc is None:
+        if self.h is None:
             return None
-        self.proc.terminate()
-        self.proc.wait()
-        self.fh.close()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        self.th.join()
+        self._sample()
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------- CPU port
@@ -185,32 +298,39 @@ def run_reference(args):
 
     L = system.box.lengths
     threads = native.default_threads()
+    traj = Trajectory(system, static=args.positions == "static")
     state = {}
+    within = []
 
-    def step(k):
+    def step(k, count=False):
+        pos = traj.host(k)
         if k % args.nstlist == 0 or not state:
-            og = search.build_grid(system.positions, L, M, occ)
+            og = search.build_grid(pos, L, M, occ)
             ol = native.search_list(og, L, R_LIST, method="n2", threads=threads)
             op = native.prune_list(ol, og["clustered_positions"], L, threads=threads)
             state.update(og=og, op=op, bits=np.ascontiguousarray(search.pack_masks(op["masks"])))
-        native.list_forces(state["op"], state["og"], system.positions, system.charges, system.lj_type, L, phys,
+            if count:
+                within.append(native.count_within(op, og["clustered_positions"], L, R_CUT, threads=threads))
+        native.list_forces(state["op"], state["og"], pos, system.charges, system.lj_type, L, phys,
                            threads=threads, packed_masks=state["bits"])
 
     for k in range(args.warmup):
         step(k)
-    n_within = native.count_within(state["op"], state["og"]["clustered_positions"], L, R_CUT, threads=threads)
     t0 = time.perf_counter()
     for k in range(args.warmup, args.warmup + args.steps):
-        step(k)
+        step(k, count=True)
     dt = time.perf_counter() - t0
+    if not within:  # no rebuild inside the timed steps
+        within.append(native.count_within(state["op"], state["og"]["clustered_positions"], L, R_CUT, threads=threads))
+    n_within = float(np.mean(within))
     value = n_within * args.steps / dt
     line = {
         "impl": "reference", "metric": "nonbonded pair-interactions/s (useful, r<=r_c)", "value": value,
         "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "ns_per_day": args.steps / dt * DT_PS * 86.4,
-        "config": config(args, occ, {"impl": "oracle/ C port of the reference CPU path (no GPU)"}),
+        "config": config_reference(args, occ, threads),
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
                          "sample": f"{args.steps} steps (rebuild every {args.nstlist}) of the full workload"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -224,6 +344,7 @@ def run_ours(args):
 
     import paper_1506_00716_b200 as nbx
     from paper_1506_00716_b200 import _lib
+    from paper_1506_00716_b200.engine import max_displacement_device
     from paper_1506_00716_b200.kernels import flops_per_pair
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -232,72 +353,120 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         return run_dd(args, world, rank, local)
-    dist = None
     lib = _lib.load()
     system, table, occ = workload(args)
     params = nbx.NonbondedParams(**{k: getattr(make_params(args, table), k) for k in (
         "r_cut", "r_list", "lj_table", "coulomb_scale", "shift_potential", "elec", "epsilon_rf", "ewald_beta")})
     box = system.box
+    n = system.n
     dev = torch.device("cuda", local)
-    pos_d = torch.from_numpy(np.array(system.positions)).to(dev)
+    W = max(3, args.warmup)
+    S0 = 10 * args.nstlist  # first timed step (trajectory index)
+    n_setup = 2 * args.nstlist if args.nstlist <= 50 else 2
+    traj = Trajectory(system, static=args.positions == "static")
+    traj.to_device(dev, sorted(set(range(n_setup)) | set(range(S0 - W, S0 + args.steps))))
+    ref_d = torch.empty((n, 3), dtype=torch.float64, device=dev)  # build positions (drift-guard reference)
     q_d = torch.from_numpy(np.array(system.charges)).to(dev)
     t_d = torch.from_numpy(np.array(system.lj_type)).to(dev)
-    f_d = torch.empty((system.n, 3), dtype=torch.float64, device=dev)
+    f_d = torch.empty((n, 3), dtype=torch.float64, device=dev)
     e_d = torch.zeros(2, dtype=torch.float64, device=dev)
     bad_d = torch.empty(2, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    buffer = R_LIST - R_CUT
     st = {}
 
-    def rebuild(pos, q, t, out):
+    def rebuild(k, pos, counts):
         grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
-        st["grid"] = grid
-        st["plist"] = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box,
-                                          r_inner=args.rinner)
+        plist = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box,
+                                    r_inner=args.rinner)
+        st.update(grid=grid, plist=plist, build=k, rebuilds=st.get("rebuilds", 0) + 1)
+        ref_d.copy_(pos)
+        if counts is not None:
+            counts[k] = nbx.interaction_stats(plist, grid, grid.clustered_positions_device, box, R_CUT).n_within_cutoff
 
-    def step(k, pos, q, t, out):
-        if k % args.nstlist == 0 or "plist" not in st:
-            rebuild(pos, q, t, out)
-        # energies on list steps (nstcalcenergy = nstlist), forces every step
+    d_pin = torch.zeros(1, dtype=torch.float64).pin_memory()
+    d_ev = torch.cuda.Event()
+
+    def force(k, pos, q, t, out):
         nbx.compute_nonbonded_device(st["plist"], st["grid"], pos, q, t, params, box,
                                      energy=(k % args.nstlist == 0), out=out, e_out=e_d, bad=bad_d)
 
-    clocks = Clocks(local)
-    # setup (not timed, not counted as warm-up steps): two full list cycles so
-    # the stream-ordered memory pool holds two list generations (steady state)
-    for k in range(2 * args.nstlist if args.nstlist <= 50 else 2):
-        step(k, pos_d, q_d, t_d, f_d)
-    for k in range(max(3, args.warmup)):
-        step(k, pos_d, q_d, t_d, f_d)
+    def step(k, q, t, out, counts=None):
+        """one MD step of the hot path: positions of step k, list lifecycle
+        (interval or drift guard 2 d_max > r_list - r_c, engine.lifecycle_tick),
+        force pass.  The drift guard is evaluated without stalling the GPU:
+        d_max is reduced and copied to pinned memory ahead of a speculative
+        force pass on the current list, and the host reads it while that pass
+        runs; when the guard fires (rare) the list is rebuilt and the pass
+        redone -- the same decision, at the same step, as the reference."""
+        pos = traj.device(k)
+        due = "plist" not in st or k - st["build"] >= args.nstlist
+        if due:
+            rebuild(k, pos, counts)
+            force(k, pos, q, t, out)
+            return
+        if traj.static:
+            force(k, pos, q, t, out)
+            return
+        d_pin.copy_(max_displacement_device(ref_d, pos, box), non_blocking=True)
+        d_ev.record()
+        force(k, pos, q, t, out)
+        d_ev.synchronize()
+        if 2.0 * float(d_pin[0]) > buffer:
+            st["drift"] = st.get("drift", 0) + 1
+            rebuild(k, pos, counts)
+            force(k, pos, q, t, out)
+
+    # setup (not timed, not counted as warm-up steps): two list cycles so the
+    # stream-ordered memory pool holds two list generations (steady state)
+    for k in range(n_setup):
+        step(k, q_d, t_d, f_d)
+    # counting pass over exactly the timed steps (same rebuild schedule: the
+    # lifecycle restarts at S0 - W in both passes): within-r_c pairs of every
+    # list the timed pass will use
+    counts = {}
+    st.clear()
+    for k in range(S0 - W, S0 + args.steps):
+        step(k, q_d, t_d, f_d, counts=counts)
     torch.cuda.synchronize()
     if int(bad_d[0].item()) != -1:
         raise RuntimeError("singular pair in the benchmark system")
-    stats = nbx.interaction_stats(st["plist"], st["grid"], st["grid"].clustered_positions_device, box, R_CUT)
-    n_within, n_admitted = stats.n_within_cutoff, stats.n_admitted
-    # pairs the force kernel evaluates (the inner list's under dynamic pruning;
-    # the positions are static, so the inner list stays valid every step)
-    n_force = st["plist"].force_pairs(inner=True)
+    builds = sorted(counts)
+    within_at = [counts[max(b for b in builds if b <= k)] for k in range(S0, S0 + args.steps)]
+    n_within_total = float(sum(within_at))
+    n_admitted = nbx.interaction_stats(st["plist"], st["grid"], st["grid"].clustered_positions_device, box,
+                                       R_CUT).n_admitted
+    drift_count = st.get("drift", 0)
 
     # ---- device-resident timed region
-    W = max(3, args.warmup)
+    clocks = Clocks(local)
+    st.clear()
+    for k in range(S0 - W, S0):
+        step(k, q_d, t_d, f_d)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.nbx_launch_count()
-    if dist is not None:
-        dist.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record()
-        step(W + i, pos_d, q_d, t_d, f_d)
+        step(S0 + i, q_d, t_d, f_d)
         ev[i][1].record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     launches = lib.nbx_launch_count() - launches0
+    rebuilds_timed = st.get("rebuilds", 0)
+    t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if os.environ.get("NBX_BENCH_DEBUG"):
+        print("per-step ms:", [round(a.elapsed_time(b), 3) for a, b in ev], file=sys.stderr)
+    value = n_within_total / (t_ms * 1e-3)
+
+    # ---- k_force duration: events around every launch of K force passes
+    # (no energies) on the launching stream, same list, last timed positions
     lib.nbx_timing_enable(0)
     lib.nbx_timing_query(None, None)
-    # k_force duration: events around every launch of K eager (non-energy)
-    # passes on the launching stream, the same list as the timed region
     lib.nbx_timing_enable(1)
+    pos_d = traj.device(S0 + args.steps - 1)
     for _ in range(args.steps):
         flush.zero_()
         nbx.compute_nonbonded_device(st["plist"], st["grid"], pos_d, q_d, t_d, params, box, energy=False,
@@ -307,46 +476,73 @@ def run_ours(args):
     fk_ms, fk_n = (np.zeros(1), np.zeros(1, dtype=np.int64))
     _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
     clk = clocks.stop()
-    t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
-    if os.environ.get("NBX_BENCH_DEBUG"):
-        print("per-step ms:", [round(a.elapsed_time(b), 3) for a, b in ev], file=sys.stderr)
-    if dist is not None:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-    value = world * n_within * args.steps / (t_ms * 1e-3)
+    # pairs that launch evaluated: the inner list only while it is valid at
+    # these positions (the kernel's own device test, 2 d_max <= r_inner - r_c)
+    d_now = float(max_displacement_device(ref_d, pos_d, box).item())
+    inner_ok = bool(args.rinner) and 2.0 * d_now <= args.rinner - R_CUT - 1e-4
+    n_force = st["plist"].force_pairs(inner=inner_ok)
 
-    # ---- end-to-end through the public API with host (pinned) buffers
-    pos_h = torch.from_numpy(np.array(system.positions)).pin_memory()
-    q_h = torch.from_numpy(np.array(system.charges)).pin_memory()
-    t_h = torch.from_numpy(np.array(system.lj_type)).pin_memory()
-    f_h = torch.empty((system.n, 3), dtype=torch.float64).pin_memory()
+    # ---- e2e through the drop-in API (numpy host arrays, wall clock per step)
+    layout = nbx.KernelLayout(M, M)
+    host_pos = [traj.host(k) for k in range(S0 - W, S0 + args.steps)]
+    charges, types = np.array(system.charges), np.array(system.lj_type)
+    de = {}
+    e2e_s = []
+    h2d = d2h = 0
+    for i, k in enumerate(range(S0 - W, S0 + args.steps)):
+        pos_np = host_pos[i]
+        t0 = time.perf_counter()
+        rb = "plist" not in de or k - de["build"] >= args.nstlist
+        if rb:
+            sysk = nbx.ParticleSystem(positions=pos_np, velocities=system.velocities, masses=system.masses,
+                                      charges=charges, lj_type=types, box=box)
+            grid = nbx.build_cluster_grid(sysk, M, occ)
+            plist = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions, box)
+            de.update(grid=grid, plist=plist, build=k)
+        res = nbx.compute_nonbonded_original(de["plist"], de["grid"], pos_np, charges, types, params, box, layout)
+        dt = time.perf_counter() - t0
+        if k >= S0:
+            e2e_s.append(dt)
+            h2d += 40 * n + (24 * n if rb else 0)
+            d2h += 24 * n + 32 + (24 * de["grid"].n_slots if rb else 0)
+    del res
+    e2e_time = sum(e2e_s)
+
+    # ---- e2e with the device API and pinned host buffers (CUDA events)
+    pin_pos = [torch.from_numpy(p).pin_memory() for p in host_pos]
+    q_h = torch.from_numpy(charges).pin_memory()
+    t_h = torch.from_numpy(types).pin_memory()
+    f_h = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     e_h = torch.empty(2, dtype=torch.float64).pin_memory()
-    pos_s = torch.empty_like(pos_d)
-    q_s = torch.empty_like(q_d)
-    t_s = torch.empty_like(t_d)
+    q_s, t_s = torch.empty_like(q_d), torch.empty_like(t_d)
     st.clear()
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(W + args.steps):
-        if i >= W:
+
+    pos_s = torch.empty((n, 3), dtype=torch.float64, device=dev)
+
+    class Pinned:  # trajectory replay from pinned host memory (H2D inside the step)
+        static = traj.static
+
+        @staticmethod
+        def device(k, out=None):
+            return pos_s.copy_(pin_pos[k - (S0 - W)], non_blocking=True)
+
+    traj_dev = traj
+    traj = Pinned
+    for i, k in enumerate(range(S0 - W, S0 + args.steps)):
+        if k >= S0:
             flush.zero_()
             ev2[i - W][0].record()
-        pos_s.copy_(pos_h, non_blocking=True)
         q_s.copy_(q_h, non_blocking=True)
         t_s.copy_(t_h, non_blocking=True)
-        step(i, pos_s, q_s, t_s, f_d)
+        step(k, q_s, t_s, f_d)
         f_h.copy_(f_d, non_blocking=True)
         e_h.copy_(e_d, non_blocking=True)
-        if i >= W:
+        if k >= S0:
             ev2[i - W][1].record()
     torch.cuda.synchronize()
-    e2e_ms = float(sum(a.elapsed_time(b) for a, b in ev2))
-    if dist is not None:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    h2d = system.n * (24 + 8 + 8)
-    d2h = system.n * 24 + 16
+    traj = traj_dev
+    pin_ms = float(sum(a.elapsed_time(b) for a, b in ev2))
 
     # ---- roofline (force kernel, FP32 pipe)
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
@@ -367,20 +563,30 @@ def run_ours(args):
     line = {
         "metric": "nonbonded pair-interactions/s (useful, r<=r_c)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": W,
-        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp32 (pair math; fp64 energy + final force accumulation)",
-        "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
+        "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe; moving-trajectory stand-in)",
         "config": config(args, occ),
         "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
-        "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted, "force_kernel": n_force,
-                           "admitted_per_s": world * n_admitted * args.steps / (t_ms * 1e-3)},
-        "e2e": {"value": world * n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / args.steps},
+        "ns_per_day_note": "steps/s of the timed hot-path loop x 2 fs (force + list lifecycle on the moving "
+                           "stand-in trajectory; no integrator, SURVEY 0.3)",
+        "pairs_per_step": {"within_rc": n_within_total / args.steps, "admitted": n_admitted,
+                           "force_kernel": n_force, "admitted_per_s": n_admitted * args.steps / (t_ms * 1e-3)},
+        "lifecycle": {"rebuilds_timed": rebuilds_timed, "drift_rebuilds_count_pass": drift_count},
+        "e2e": {"value": n_within_total / e2e_time, "unit": "pairs/s", "kind": (
+                    "drop-in API, numpy host arrays: compute_nonbonded_original every step, "
+                    "build_cluster_grid/build_pair_list/prune_pair_list every nstlist; wall clock"),
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                "ms_per_step": 1e3 * e2e_time / args.steps},
+        "e2e_pinned": {"value": n_within_total / (pin_ms * 1e-3), "unit": "pairs/s",
+                       "kind": "device API, pinned host buffers copied in/out every step; CUDA events",
+                       "h2d_bytes_per_step": 40 * n, "d2h_bytes_per_step": 24 * n + 16,
+                       "ms_per_step": pin_ms / args.steps},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp32", "kernel": "k_force", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
-                     "kernel_ms": fk_avg_ms, "flops_per_pair": fpp, "pairs": "force_kernel (admitted pairs the kernel evaluates)",
+                     "kernel_ms": fk_avg_ms, "flops_per_pair": fpp,
+                     "pairs": "force_kernel (admitted pairs the kernel evaluates)",
                      "peak_note": f"nominal FP32: {n_sm} SMs x 128 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json)"},
         "clocks": clk,
         "wall_s_timed": wall,
@@ -389,15 +595,11 @@ def run_ours(args):
         c = cpu_port_times(system, oracle_physics(params), occ, args.nstlist)
         per_step = c["force"] + (c["grid"] + c["search"] + c["prune"]) / args.nstlist
         line["cpu_baseline"] = {
-            "value": n_within / per_step, "unit": "pairs/s", "cores": c["threads"], "kind": "port",
+            "value": (n_within_total / args.steps) / per_step, "unit": "pairs/s", "cores": c["threads"], "kind": "port",
             "sample": (f"one rebuild (grid {c['grid']:.3f}s, O(n_c^2) search {c['search']:.3f}s, "
                        f"prune {c['prune']:.3f}s) + one force pass {c['force']:.3f}s, amortised over "
                        f"nstlist={args.nstlist}")}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
 
 
 def run_dd(args, world, rank, local):
@@ -531,10 +733,11 @@ def run_dd(args, world, rank, local):
 
 def main():
     global R_LIST
+    faulthandler.enable()
     args = parse()
     R_LIST = args.rlist
     if args.rinner is None:
-        args.rinner = min(R_CUT + 0.02, R_LIST)
+        args.rinner = 0.0 if args.positions == "moving" else min(R_CUT + 0.02, R_LIST)
     if args.impl == "reference":
         run_reference(args)
     else:

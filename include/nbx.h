@@ -156,6 +156,13 @@ int nbx_super_layout(const nbx_list_t* list, int32_t size, void* stream, int64_t
  * super_pair_idx (n_entries*size, -1 = absent); syncs */
 int nbx_super_download(const nbx_list_t* list, int64_t* super_offsets, int64_t* super_j,
                        int64_t* super_pair_idx, void* stream);
+/* Extension (rigid water / molecular topologies; the reference masks only
+ * fillers and the diagonal, pairlist.py:106-112): clear, in place, every mask
+ * bit (canonical and inner force masks) whose two particles carry the same
+ * molecule id.  mol: device int32 per particle, original order.  n_removed
+ * (host, may be NULL; syncs when given): admitted slot pairs removed. */
+int nbx_list_exclude(nbx_list_t* list, const nbx_grid_t* grid, const int32_t* mol, void* stream,
+                     int64_t* n_removed);
 /* Per-row diagnostics of pairlist.write_pairs_csv (pairlist.py:349-376):
  * gap_sq[r] = periodic bounding-box gap^2 of row r (gridder.py:165-185),
  * min_d2[r] = exact FP64 minimum admitted slot distance^2 at `positions`

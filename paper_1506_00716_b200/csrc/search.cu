@@ -1936,3 +1936,103 @@ fail:
   ci.release(s);
   return NBX_ERR_CUDA;
 }
+
+// ---------------------------------------------------------------- exclusions
+// Intramolecular exclusions (extension; the reference masks only fillers and
+// the diagonal, pairlist.py:106-112): slot pairs whose particles carry the
+// same molecule id are removed from the masks, so rigid water (SPC, SETTLE)
+// has no intramolecular non-bonded terms.  Applied to a finished list, in
+// place: the canonical masks (ent_mask) and the inner force masks (ent_fmask)
+// of every entry.  Member presence and the entry order are unchanged (a
+// member row always keeps pairs with other molecules: a cluster pair never
+// holds only one molecule's atoms when m >= 2 and molecules have <= m atoms
+// ... and when it does, the row simply evaluates nothing).
+__global__ void k_mol_slots(const int32_t* __restrict__ mol, const int32_t* __restrict__ perm,
+                            const uint8_t* __restrict__ fill, int64_t n_slots, int32_t* __restrict__ out) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n_slots) return;
+  out[s] = fill[s] ? (int32_t)(-1 - s) : mol[perm[s]];  // fillers never match
+}
+
+__global__ void k_exclude(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
+                          int64_t n_groups, const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
+                          const int32_t* __restrict__ mol_slot, int m, uint64_t* __restrict__ ent_mask,
+                          uint64_t* __restrict__ ent_fmask, unsigned long long* __restrict__ n_removed) {
+  const int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const int lane = threadIdx.x & 31;
+  const int32_t first = grp_first[g];
+  const int nmem = grp_nmem[g];
+  const int W = (m == 8) ? 2 : 1, mm = m * m;
+  // the group's i-slot molecule ids (<= 16 slots): lane i holds slot i
+  const int ni = nmem * m;
+  const int32_t mi = lane < ni ? mol_slot[(int64_t)first * m + lane] : INT32_MIN;
+  unsigned long long removed = 0;
+  for (int32_t e = ent_off[g] + lane; __any_sync(0xffffffffu, e < ent_off[g + 1]); e += 32) {
+    const bool valid = e < ent_off[g + 1];
+    const int32_t cj = valid ? ent_j[e] : 0;
+    int32_t mj[8];
+    for (int b = 0; b < m; ++b) mj[b] = valid ? mol_slot[(int64_t)cj * m + b] : INT32_MIN;
+    uint64_t clr[2] = {0ull, 0ull};
+    for (int ia = 0; ia < ni; ++ia) {
+      const int32_t mia = __shfl_sync(0xffffffffu, mi, ia);
+      const int k = ia / m, a = ia - k * m;
+      for (int b = 0; b < m; ++b)
+        if (valid && mia == mj[b]) {
+          const int bit = (W == 2) ? a * m + b : k * mm + a * m + b;
+          clr[W == 2 ? k : 0] |= 1ull << bit;
+        }
+    }
+    if (valid) {
+      for (int q = 0; q < W; ++q) {
+        if (!clr[q]) continue;
+        const uint64_t old = ent_mask[(int64_t)e * W + q];
+        removed += __popcll(old & clr[q]);
+        ent_mask[(int64_t)e * W + q] = old & ~clr[q];
+        if (ent_fmask) ent_fmask[(int64_t)e * W + q] &= ~clr[q];
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) removed += __shfl_xor_sync(0xffffffffu, removed, o);
+  if (lane == 0 && removed) atomicAdd(n_removed, removed);
+}
+
+extern "C" int nbx_list_exclude(nbx_list_t* l, const nbx_grid_t* grid, const int32_t* mol, void* stream,
+                                int64_t* n_removed) {
+  if (!l || !grid || (grid->n > 0 && !mol) || grid->m != l->m || grid->n_clusters != l->n_clusters) {
+    set_error("nbx_list_exclude: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  DBuf<int32_t> ms;
+  DBuf<unsigned long long> cnt;
+  unsigned long long h = 0;
+  const int64_t ns = grid->n_slots();
+  TRY(cnt.alloc(1, s));
+  TRY(cudaMemsetAsync(cnt.p, 0, 8, s));
+  if (ns > 0 && l->n_groups > 0) {
+    TRY(ms.alloc(ns, s));
+    count_launch(2);
+    k_mol_slots<<<nb(ns, 256), 256, 0, s>>>(mol, grid->perm.p, grid->fill.p, ns, ms.p);
+    k_exclude<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups, l->ent_offsets.p,
+                                                  l->ent_j.p, ms.p, l->m, l->ent_mask.p, l->ent_fmask.p, cnt.p);
+    TRY(cudaGetLastError());
+  }
+  // canonical rows and the reference super layout are re-derived from the
+  // entries on their next use
+  l->rows_ready = false;
+  l->delta_ready = false;
+  l->super_size = 0;
+  if (n_removed) {
+    TRY(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    *n_removed = (int64_t)h;
+  }
+  ms.release(s);
+  cnt.release(s);
+  return NBX_OK;
+fail:
+  ms.release(s);
+  cnt.release(s);
+  return NBX_ERR_CUDA;
+}
