@@ -205,6 +205,15 @@ int nbx_max_displacement(const double* ref, const double* cur, int64_t n, const 
  * original order. */
 int nbx_vv_update(double* x, double* v, const double* f, const double* mass, int64_t n, double dt,
                   int32_t move, const double box[3], void* stream);
+/* Extension (rigid 3-site water; the reference has no
+ * constraints): molecules are atoms (3k, 3k+1, 3k+2) = (O, H, H) with bond
+ * lengths d_oh, d_oh, d_hh.  mode 0 (after the drift of a velocity-Verlet
+ * step): SETTLE x (device (3 n_mol, 3) f64, drifted, wrapped) given the
+ * constrained positions x_old of the previous step, and v += displacement / dt;
+ * mode 1 (after the second half kick): RATTLE velocity stage, v projected so
+ * that no bond length changes (x_old unused). */
+int nbx_settle(const double* x_old, double* x, double* v, int64_t n_mol, double m_o, double m_h, double d_oh,
+               double d_hh, double dt, int32_t mode, const double box[3], void* stream);
 
 /* ---------------------------------------------------------------- domain decomposition
  * Halo exchange of the 1-D slab decomposition (paper_1506_00716_b200/dd.py,

@@ -138,9 +138,13 @@ def list_forces(lst: dict, grid: dict, positions, charges, lj_type, lengths, phy
     return f, float(np.sum(e_lj)), float(np.sum(e_c))
 
 
-def brute_force(positions, charges, lj_type, lengths, phys: Physics):
-    """oracle.py:28-67: all pairs within r_c, original order, O(n^2)."""
+def brute_force(positions, charges, lj_type, lengths, phys: Physics, molecules=None, abs_sums=False):
+    """oracle.py:28-67: all pairs within r_c, original order, O(n^2).
+    ``molecules`` (extension, rigid water): pairs within one molecule are
+    excluded.  ``abs_sums``: also return (sum |E_lj pair|, sum |E_c pair|),
+    the scale of the cancelling sums."""
     pos = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+    mol = None if molecules is None else np.asarray(molecules)
     n = pos.shape[0]
     charges = np.asarray(charges, dtype=np.float64)
     lj_type = np.asarray(lj_type, dtype=np.int64)
@@ -148,10 +152,14 @@ def brute_force(positions, charges, lj_type, lengths, phys: Physics):
     e_lj = 0.0
     e_c = 0.0
     rc2 = phys.r_cut * phys.r_cut
+    a_lj = a_c = 0.0
     for i in range(n - 1):
         dr = min_image(pos[i] - pos[i + 1:], lengths)
         r2 = np.einsum("kd,kd->k", dr, dr)
-        idx = np.nonzero(r2 <= rc2)[0]
+        keep = r2 <= rc2
+        if mol is not None:
+            keep &= mol[i + 1:] != mol[i]
+        idx = np.nonzero(keep)[0]
         if idx.shape[0] == 0:
             continue
         if np.any(r2[idx] == 0.0):
@@ -160,9 +168,13 @@ def brute_force(positions, charges, lj_type, lengths, phys: Physics):
                               charges[i + 1 + idx], phys)
         e_lj += float(np.sum(a))
         e_c += float(np.sum(c))
+        a_lj += float(np.sum(np.abs(a)))
+        a_c += float(np.sum(np.abs(c)))
         fv = fr[:, None] * dr[idx]
         f[i] += fv.sum(axis=0)
         f[i + 1 + idx] -= fv
+    if abs_sums:
+        return f, e_lj, e_c, (a_lj, a_c)
     return f, e_lj, e_c
 
 

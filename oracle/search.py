@@ -254,3 +254,20 @@ def admitted_pair_set(lst: dict, grid: dict) -> set:
     oi = grid["perm"][ci[p] * m + a]
     oj = grid["perm"][lst["j_idx"][p] * m + b]
     return set(zip(np.minimum(oi, oj).tolist(), np.maximum(oi, oj).tolist()))
+
+
+def exclude_molecules(lst: dict, grid: dict, molecules) -> dict:
+    """Extension (rigid water): the list with every admitted slot pair whose
+    particles share a molecule id removed from the masks (rows unchanged).
+    Restates csrc/search.cu k_exclude; fillers never match."""
+    m = lst["m"]
+    perm, fill = grid["perm"], grid["fill_mask"]
+    mol = np.asarray(molecules, dtype=np.int64)[perm]
+    mol = np.where(fill, -1 - np.arange(perm.shape[0]), mol)
+    ci = row_ci(lst)
+    mi = mol.reshape(-1, m)[ci]                 # (rows, m)
+    mj = mol.reshape(-1, m)[lst["j_idx"]]
+    same = mi[:, :, None] == mj[:, None, :]
+    out = dict(lst)
+    out["masks"] = lst["masks"] & ~same
+    return out

@@ -140,6 +140,49 @@ class ListPolicy:
                                  f"{self.prune_interval}")
 
 
+@dataclass(frozen=True)
+class RigidWater:
+    """Rigid 3-site water (extension: the reference has neither
+    exclusions nor constraints, so its SPC water cannot be integrated, SURVEY
+    0.3).  Molecules are atoms (3k, 3k+1, 3k+2) = (O, H, H) -- the order of
+    systems.spc_water -- held rigid by SETTLE (positions) and RATTLE's
+    velocity stage (nbx_settle), with every intramolecular pair excluded
+    from the non-bonded list (pairlist.exclude_molecules).  Defaults: SPC
+    geometry (O-H 0.1 nm, H-O-H 109.47 deg)."""
+
+    d_oh: float = 0.1
+    d_hh: float = 2.0 * 0.1 * float(np.sin(np.deg2rad(109.47) / 2.0))
+
+    def molecules(self, n: int) -> np.ndarray:
+        return np.arange(n, dtype=np.int64) // 3
+
+    def check(self, system: ParticleSystem) -> tuple[float, float]:
+        """(m_O, m_H) after validating the layout of ``system``."""
+        n = system.n
+        if n % 3:
+            raise ParameterError(f"rigid water needs 3 atoms per molecule, got n={n}")
+        if not (0.0 < 0.5 * self.d_hh < self.d_oh):
+            raise ParameterError(f"invalid water geometry d_oh={self.d_oh}, d_hh={self.d_hh}")
+        mm = system.masses.reshape(-1, 3)
+        if n and not (np.all(mm[:, 0] == mm[0, 0]) and np.all(mm[:, 1:] == mm[0, 1])):
+            raise ParameterError("rigid water needs identical (O, H, H) masses in every molecule")
+        return (float(mm[0, 0]), float(mm[0, 1])) if n else (1.0, 1.0)
+
+    def dof(self, n: int) -> int:
+        return max(6 * (n // 3) - 3, 1)
+
+
+def settle_device(x_old, x, v, water: RigidWater, m_o: float, m_h: float, dt: float, box: SimBox,
+                  velocities_only: bool = False) -> None:
+    """SETTLE of the drifted positions x (with v += displacement / dt), or --
+    velocities_only -- RATTLE's velocity projection (device, in place)."""
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_settle(_lib.ptr(x_old) if x_old is not None else None, _lib.ptr(x), _lib.ptr(v),
+                                      int(x.shape[0]) // 3, float(m_o), float(m_h), float(water.d_oh),
+                                      float(water.d_hh), float(dt), 1 if velocities_only else 0, _lib.ptr(L),
+                                      dev.stream()), "settle")
+
+
 @dataclass
 class MDState:
     """engine.py:280-291 (+ optional grid occupancy for the compact-cluster grid)."""
@@ -155,11 +198,11 @@ class MDState:
     target_occupancy: float | None = None
 
 
-def _build(system, params, m, supercluster_size, n_lane, step, policy, occupancy):
+def _build(system, params, m, supercluster_size, n_lane, step, policy, occupancy, molecules=None):
     """engine.py:301-314: grid, list, and the prune of a reused list."""
     grid = build_cluster_grid(system, m, occupancy)
     plist = build_pair_list(grid, system.box, params.r_list, supercluster_size=supercluster_size,
-                            n_lane=n_lane, build_step=step)
+                            n_lane=n_lane, build_step=step, molecules=molecules)
     if policy.prune_on_build and policy.rebuild_interval > 1:
         # the same inner list (dynamic pruning) as run_md's rebuilds
         plist = prune_pair_list(plist, grid.clustered_positions_device, system.box,
@@ -178,12 +221,14 @@ def _rebuild(state: MDState, params: NonbondedParams, policy: ListPolicy, timer)
 
 def init_state(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout, *,
                supercluster_size: int = 1, policy: ListPolicy | None = None, n_slabs: int = 0,
-               slab_min_width: float | None = None, timer=None, target_occupancy: float | None = None) -> MDState:
+               slab_min_width: float | None = None, timer=None, target_occupancy: float | None = None,
+               molecules=None) -> MDState:
     """Initial grid, list (pruned when reused) and optional slabs (engine.py:337-384)."""
     if params.r_list < params.r_cut:
         raise ParameterError(f"r_list={params.r_list} must be >= r_cut={params.r_cut}")
     policy = policy or ListPolicy()
-    grid, plist = _build(system, params, layout.m, supercluster_size, layout.n_lane, 0, policy, target_occupancy)
+    grid, plist = _build(system, params, layout.m, supercluster_size, layout.n_lane, 0, policy, target_occupancy,
+                         molecules)
     state = MDState(system=system, step=0, grid=grid, plist=plist,
                     drift=DriftTracker(reference_positions=wrap_position(system.positions, system.box)),
                     n_rebuilds=1, target_occupancy=target_occupancy)
@@ -303,7 +348,7 @@ class RunResult:
 def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout, dt: float, n_steps: int, *,
            supercluster_size: int = 1, policy: ListPolicy | None = None, workers: int = 1, n_slabs: int = 0,
            slab_min_width: float | None = None, report_interval: int = 100, timer: TimingReport | None = None,
-           target_occupancy: float | None = None) -> RunResult:
+           target_occupancy: float | None = None, constraints: RigidWater | None = None) -> RunResult:
     """NVE velocity-Verlet run with the state resident on the GPU
     (engine.py:610-706 semantics).
 
@@ -316,7 +361,12 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     nstcalcenergy) and the second half kick.  Reports read back the
     energies and the kinetic energy; a singular pair raises at the next
     report (SingularityError, original indices) as the reference does at
-    the failing step."""
+    the failing step.
+
+    ``constraints`` (extension): a RigidWater spec makes the run rigid-water
+    MD -- intramolecular pairs excluded from every list, SETTLE after the
+    drift, RATTLE's velocity stage after the second kick, temperature over
+    6 n_mol - 3 degrees of freedom."""
     if dt <= 0.0:
         raise ParameterError(f"dt must be positive, got {dt}")
     if n_steps < 0:
@@ -333,11 +383,19 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     d = dev.require_cuda()
     box = system.box
     buffer = params.r_list - params.r_cut
+    mol = None
+    if constraints is not None:
+        m_o, m_h = constraints.check(system)
+        mol = dev.to_device(constraints.molecules(system.n), torch.int64)
     with timer.section("setup"):
         state = init_state(system, params, layout, supercluster_size=supercluster_size, policy=policy,
-                           n_slabs=n_slabs, slab_min_width=slab_min_width, target_occupancy=target_occupancy)
+                           n_slabs=n_slabs, slab_min_width=slab_min_width, target_occupancy=target_occupancy,
+                           molecules=mol)
         x = dev.to_device(system.positions, torch.float64).clone()
         v = dev.to_device(system.velocities, torch.float64).clone()
+        x_old = torch.empty_like(x) if constraints is not None else None
+        if constraints is not None:  # start from velocities that keep the bonds rigid
+            settle_device(None, x, v, constraints, m_o, m_h, dt, box, velocities_only=True)
         m = dev.to_device(system.masses, torch.float64)
         q = dev.to_device(system.charges, torch.float64)
         ty = dev.to_device(system.lj_type, torch.int64)
@@ -346,6 +404,8 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
         e = torch.zeros(2, dtype=torch.float64, device=d)
         bad = torch.empty(2, dtype=torch.int64, device=d)
         d_max = 0.0
+        d_pin = torch.zeros(1, dtype=torch.float64).pin_memory()
+        d_ev = torch.cuda.Event()
 
         def force_pass(energy: bool):
             age = state.step - state.plist.build_step
@@ -358,6 +418,8 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     steps, e_kin, e_pot, temps, drifts = [], [], [], [], []
     log = ["# clustermd run log", "# step e_kinetic e_potential e_total temperature_K max_drift_nm"]
     dof = 3 * system.n - 3 if system.n > 1 else 3
+    if constraints is not None:
+        dof = constraints.dof(system.n)
 
     def record():
         bad_h = bad.cpu().numpy()
@@ -376,15 +438,33 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     for _ in range(n_steps):
         with timer.section("step"):
             with timer.section("integrate"):
+                if constraints is not None:
+                    x_old.copy_(x)
                 vv_half_kick_device(x, v, f, m, dt, box, move=True)
+                if constraints is not None:
+                    settle_device(x_old, x, v, constraints, m_o, m_h, dt, box)
                 state.step += 1
+            report = state.step % report_interval == 0 or state.step == n_steps
             with timer.section("lifecycle"):
                 interval_due = state.step - state.plist.build_step >= policy.rebuild_interval
                 guard_due = False
+                speculative = False
                 if not interval_due:
-                    d_max = max(d_max, float(max_displacement_device(ref, x, box).item()))
+                    # drift guard without stalling the GPU: d_max goes to
+                    # pinned memory ahead of a speculative force pass on the
+                    # current list; the host reads it while that pass runs and,
+                    # when the guard fires (rare), rebuilds and redoes the pass
+                    # -- the reference's decision at the same step
+                    d_pin.copy_(max_displacement_device(ref, x, box), non_blocking=True)
+                    d_ev.record()
+                    with timer.section("forces"):
+                        force_pass(report)
+                    speculative = True
+                    d_ev.synchronize()
+                    d_max = max(d_max, float(d_pin[0]))
                     guard_due = 2.0 * d_max > buffer
                 if interval_due or guard_due:
+                    speculative = False
                     if guard_due:
                         state.n_drift_rebuilds += 1
                     with timer.section("rebuild"):
@@ -392,18 +472,21 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                                                         state.target_occupancy, positions=x)
                         state.plist = build_pair_list(state.grid, box, params.r_list,
                                                       supercluster_size=state.plist.supercluster_size,
-                                                      n_lane=state.plist.n_lane, build_step=state.step)
+                                                      n_lane=state.plist.n_lane, build_step=state.step,
+                                                      molecules=mol)
                         if policy.prune_on_build and policy.rebuild_interval > 1:
                             state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box,
                                                           r_inner=min(policy.r_inner, params.r_list))
                     ref.copy_(x)
                     d_max = 0.0
                     state.n_rebuilds += 1
-            report = state.step % report_interval == 0 or state.step == n_steps
-            with timer.section("forces"):
-                force_pass(report)
+            if not speculative:
+                with timer.section("forces"):
+                    force_pass(report)
             with timer.section("integrate"):
                 vv_half_kick_device(x, v, f, m, dt, box, move=False)
+                if constraints is not None:
+                    settle_device(None, x, v, constraints, m_o, m_h, dt, box, velocities_only=True)
             if report:
                 with timer.section("report"):
                     record()

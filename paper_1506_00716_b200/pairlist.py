@@ -158,12 +158,14 @@ class InteractionStats:
 
 
 def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, supercluster_size: int = 1,
-                    n_lane: int = 1, build_step: int = 0, halo=None) -> ClusterPairList:
+                    n_lane: int = 1, build_step: int = 0, halo=None, molecules=None) -> ClusterPairList:
     """All cluster pairs with AABB gap <= r_list, j >= i (pairlist.py:147-217).
 
     ``halo`` (extension, domain decomposition): CUDA uint8 tensor per
     particle marking particles owned by another rank; halo-halo slot pairs
-    are masked out."""
+    are masked out.  ``molecules`` (extension, rigid water): per-particle
+    molecule ids; slot pairs within one molecule are masked out
+    (exclude_molecules)."""
     if r_list <= 0.0:
         raise ParameterError(f"r_list must be positive, got {r_list}")
     if np.any(box.lengths < 2.0 * r_list):
@@ -176,12 +178,34 @@ def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, superclust
     L = _lib.box3(box.lengths)
     _lib.check(_lib.load().nbx_pairlist_build_ex(grid.handle, _lib.ptr(L), float(r_list), _lib.ptr(halo),
                                                  dev.stream(), ctypes.byref(h)), "pairlist_build")
-    return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+    plist = ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+    if molecules is not None:
+        exclude_molecules(plist, molecules)
+    return plist
+
+
+def exclude_molecules(plist: ClusterPairList, molecules, count: bool = False):
+    """Extension (SPC / rigid water; the reference masks only fillers and the
+    diagonal, pairlist.py:106-112): remove, in place, every admitted slot pair
+    whose two particles share a molecule id (``molecules``: one int per
+    particle, original order; numpy or CUDA tensor).  Applied before the
+    prune, excluded pairs also no longer keep a row alive.  Returns the number
+    of removed slot pairs when ``count`` (one host sync), else None."""
+    g = plist.grid
+    mol = dev.to_device(molecules, torch.int64).to(torch.int32).contiguous()
+    if mol.shape != (g.n,):
+        raise ParameterError(f"molecules must have shape ({g.n},), got {tuple(mol.shape)}")
+    out = ctypes.c_int64(0)
+    _lib.check(_lib.load().nbx_list_exclude(plist.handle, g.handle, _lib.ptr(mol), dev.stream(),
+                                            ctypes.byref(out) if count else None), "list_exclude")
+    plist._host = None
+    plist._super = None
+    return int(out.value) if count else None
 
 
 def build_pruned_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, positions=None, *,
                            supercluster_size: int = 1, n_lane: int = 1, build_step: int = 0,
-                           halo=None) -> ClusterPairList:
+                           halo=None, molecules=None) -> ClusterPairList:
     """``prune_pair_list(build_pair_list(grid, box, r_list, ...), positions, box)``
     in one GPU search (extension): each bounding-box hit is checked against
     the exact prune criterion before it is stored, so the unpruned list is
@@ -210,7 +234,10 @@ def build_pruned_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, positi
     _lib.check(_lib.load().nbx_pairlist_build_pruned(grid.handle, _lib.ptr(L), float(r_list), p, _lib.ptr(halo),
                                                      dev.stream(), ctypes.byref(h)), "pairlist_build_pruned")
     del keep_alive
-    return ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+    plist = ClusterPairList(h, grid, r_list, n_lane, build_step, supercluster_size)
+    if molecules is not None:  # after the fused prune: a row kept only by an excluded pair stays (no pairs)
+        exclude_molecules(plist, molecules)
+    return plist
 
 
 def _positions_ptr(plist: ClusterPairList, positions):
