@@ -158,11 +158,14 @@ int nbx_super_download(const nbx_list_t* list, int64_t* super_offsets, int64_t* 
                        int64_t* super_pair_idx, void* stream);
 /* Extension (rigid water / molecular topologies; the reference masks only
  * fillers and the diagonal, pairlist.py:106-112): clear, in place, every mask
- * bit (canonical and inner force masks) whose two particles carry the same
- * molecule id.  mol: device int32 per particle, original order.  n_removed
- * (host, may be NULL; syncs when given): admitted slot pairs removed. */
-int nbx_list_exclude(nbx_list_t* list, const nbx_grid_t* grid, const int32_t* mol, void* stream,
-                     int64_t* n_removed);
+ * bit (canonical and inner force masks) whose two particles belong to the
+ * same molecule.  Device int32 arrays: atom_mol (n) molecule id per particle
+ * (original order), mol_first (n_mol + 1) / mol_atoms (n) the atoms of each
+ * molecule (CSR).  n_removed (host, may be NULL; syncs when given): admitted
+ * slot pairs removed.  Cost ~ n x (atoms per molecule) x log(entries per
+ * group): a per-particle search of the partners' entries. */
+int nbx_list_exclude(nbx_list_t* list, const nbx_grid_t* grid, const int32_t* atom_mol, const int32_t* mol_first,
+                     const int32_t* mol_atoms, void* stream, int64_t* n_removed);
 /* Per-row diagnostics of pairlist.write_pairs_csv (pairlist.py:349-376):
  * gap_sq[r] = periodic bounding-box gap^2 of row r (gridder.py:165-185),
  * min_d2[r] = exact FP64 minimum admitted slot distance^2 at `positions`

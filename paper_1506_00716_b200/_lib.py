@@ -110,7 +110,7 @@ def load():
         "nbx_dd_p2p_open": (ctypes.c_int, [P, P, P]),
         "nbx_dd_p2p_error": (ctypes.c_int, [P, P]),
         "nbx_list_diagnostics": (ctypes.c_int, [P, P, P, P, P, P, P]),
-        "nbx_list_exclude": (ctypes.c_int, [P, P, P, P, P]),
+        "nbx_list_exclude": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "nbx_settle": (ctypes.c_int, [P, P, P, I64, D, D, D, D, D, I32, P, P]),
     }
     for name, (res, args) in sig.items():

@@ -1947,75 +1947,98 @@ fail:
 // member row always keeps pairs with other molecules: a cluster pair never
 // holds only one molecule's atoms when m >= 2 and molecules have <= m atoms
 // ... and when it does, the row simply evaluates nothing).
-__global__ void k_mol_slots(const int32_t* __restrict__ mol, const int32_t* __restrict__ perm,
-                            const uint8_t* __restrict__ fill, int64_t n_slots, int32_t* __restrict__ out) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= n_slots) return;
-  out[s] = fill[s] ? (int32_t)(-1 - s) : mol[perm[s]];  // fillers never match
+// One thread per slot: for each partner atom of the slot's molecule that
+// the half list pairs it with (cluster cj > ci, or cj == ci and b > a), find
+// the entry (group of ci, cj) by binary search over the group's entries in
+// ascending j (ent_jorder) and clear the bit; a pruned row is simply absent.
+// The molecules come as a CSR (mol_first / mol_atoms: the atoms of each
+// molecule) plus the per-atom id (atom_mol); any id layout works.
+__global__ void k_cluster_group(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
+                                int64_t n_groups, int32_t* __restrict__ cgroup) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  for (int k = 0; k < grp_nmem[g]; ++k) cgroup[grp_first[g] + k] = (int32_t)g;
 }
 
-__global__ void k_exclude(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
-                          int64_t n_groups, const int32_t* __restrict__ ent_off, const int32_t* __restrict__ ent_j,
-                          const int32_t* __restrict__ mol_slot, int m, uint64_t* __restrict__ ent_mask,
+// per group, the entries' j-clusters in ascending order (binary-search keys)
+// (t < ent_off[n_groups]: a pruned list's storage may hold unused slots past the live entries)
+__global__ void k_sorted_j(const int32_t* __restrict__ jorder, const int32_t* __restrict__ ent_j, int64_t n,
+                           const int32_t* __restrict__ live_end, int32_t* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n && t < *live_end) out[t] = ent_j[jorder ? jorder[t] : t];
+}
+
+constexpr int EXCL_SPLIT = 3;  // threads per slot (partners q, q + 3, ...)
+__global__ void k_exclude(const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
+                          const uint8_t* __restrict__ fill, int64_t n_slots, const int32_t* __restrict__ mol_atoms,
+                          const int32_t* __restrict__ mol_first, const int32_t* __restrict__ atom_mol,
+                          const int32_t* __restrict__ cgroup, const int32_t* __restrict__ grp_first,
+                          const int32_t* __restrict__ ent_off, const int32_t* __restrict__ jorder,
+                          const int32_t* __restrict__ sj_sorted, int m, uint64_t* __restrict__ ent_mask,
                           uint64_t* __restrict__ ent_fmask, unsigned long long* __restrict__ n_removed) {
-  const int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (g >= n_groups) return;
-  const int lane = threadIdx.x & 31;
-  const int32_t first = grp_first[g];
-  const int nmem = grp_nmem[g];
-  const int W = (m == 8) ? 2 : 1, mm = m * m;
-  // the group's i-slot molecule ids (<= 16 slots): lane i holds slot i
-  const int ni = nmem * m;
-  const int32_t mi = lane < ni ? mol_slot[(int64_t)first * m + lane] : INT32_MIN;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t si = tid / EXCL_SPLIT;
+  const int part = (int)(tid - si * EXCL_SPLIT);
   unsigned long long removed = 0;
-  for (int32_t e = ent_off[g] + lane; __any_sync(0xffffffffu, e < ent_off[g + 1]); e += 32) {
-    const bool valid = e < ent_off[g + 1];
-    const int32_t cj = valid ? ent_j[e] : 0;
-    int32_t mj[8];
-    for (int b = 0; b < m; ++b) mj[b] = valid ? mol_slot[(int64_t)cj * m + b] : INT32_MIN;
-    uint64_t clr[2] = {0ull, 0ull};
-    for (int ia = 0; ia < ni; ++ia) {
-      const int32_t mia = __shfl_sync(0xffffffffu, mi, ia);
-      const int k = ia / m, a = ia - k * m;
-      for (int b = 0; b < m; ++b)
-        if (valid && mia == mj[b]) {
-          const int bit = (W == 2) ? a * m + b : k * mm + a * m + b;
-          clr[W == 2 ? k : 0] |= 1ull << bit;
-        }
-    }
-    if (valid) {
-      for (int q = 0; q < W; ++q) {
-        if (!clr[q]) continue;
-        const uint64_t old = ent_mask[(int64_t)e * W + q];
-        removed += __popcll(old & clr[q]);
-        ent_mask[(int64_t)e * W + q] = old & ~clr[q];
-        if (ent_fmask) ent_fmask[(int64_t)e * W + q] &= ~clr[q];
+  if (si < n_slots && !fill[si]) {
+    const int32_t oi = __ldg(perm + si), mo = __ldg(atom_mol + oi);
+    const int64_t ci = si / m;
+    const int a = (int)(si - ci * m);
+    const int32_t g = __ldg(cgroup + ci), k = (int32_t)(ci - __ldg(grp_first + g));
+    const int W = (m == 8) ? 2 : 1, mm = m * m;
+    const int32_t t_lo = __ldg(ent_off + g), t_hi = __ldg(ent_off + g + 1);
+    for (int32_t q = __ldg(mol_first + mo) + part; q < __ldg(mol_first + mo + 1); q += EXCL_SPLIT) {
+      const int32_t op = __ldg(mol_atoms + q);
+      if (op == oi) continue;
+      const int64_t sj = __ldg(inv_perm + op);
+      const int64_t cj = sj / m;
+      const int b = (int)(sj - cj * m);
+      if (cj < ci || (cj == ci && b <= a)) continue;  // held by the other atom's row (or nowhere)
+      int32_t lo = t_lo, hi = t_hi;                    // first t with sorted j >= cj
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (__ldg(sj_sorted + mid) < cj) lo = mid + 1;
+        else hi = mid;
       }
+      if (lo >= t_hi || __ldg(sj_sorted + lo) != cj) continue;
+      const int32_t e = jorder ? __ldg(jorder + lo) : lo;
+      const int bit = (W == 2) ? a * m + b : k * mm + a * m + b;
+      const int64_t w = (int64_t)e * W + (W == 2 ? k : 0);
+      const uint64_t bm = 1ull << bit;
+      const unsigned long long old = atomicAnd(reinterpret_cast<unsigned long long*>(ent_mask + w), ~bm);
+      removed += (old & bm) ? 1ull : 0ull;
+      if (ent_fmask) atomicAnd(reinterpret_cast<unsigned long long*>(ent_fmask + w), ~bm);
     }
   }
   for (int o = 16; o; o >>= 1) removed += __shfl_xor_sync(0xffffffffu, removed, o);
-  if (lane == 0 && removed) atomicAdd(n_removed, removed);
+  if ((threadIdx.x & 31) == 0 && removed) atomicAdd(n_removed, removed);
 }
 
-extern "C" int nbx_list_exclude(nbx_list_t* l, const nbx_grid_t* grid, const int32_t* mol, void* stream,
-                                int64_t* n_removed) {
-  if (!l || !grid || (grid->n > 0 && !mol) || grid->m != l->m || grid->n_clusters != l->n_clusters) {
+extern "C" int nbx_list_exclude(nbx_list_t* l, const nbx_grid_t* grid, const int32_t* atom_mol,
+                                const int32_t* mol_first, const int32_t* mol_atoms, void* stream, int64_t* n_removed) {
+  if (!l || !grid || (grid->n > 0 && (!atom_mol || !mol_first || !mol_atoms)) || grid->m != l->m ||
+      grid->n_clusters != l->n_clusters) {
     set_error("nbx_list_exclude: bad argument");
     return NBX_ERR_PARAM;
   }
   cudaStream_t s = to_stream(stream);
-  DBuf<int32_t> ms;
+  DBuf<int32_t> cg, sj;
   DBuf<unsigned long long> cnt;
   unsigned long long h = 0;
   const int64_t ns = grid->n_slots();
   TRY(cnt.alloc(1, s));
   TRY(cudaMemsetAsync(cnt.p, 0, 8, s));
-  if (ns > 0 && l->n_groups > 0) {
-    TRY(ms.alloc(ns, s));
-    count_launch(2);
-    k_mol_slots<<<nb(ns, 256), 256, 0, s>>>(mol, grid->perm.p, grid->fill.p, ns, ms.p);
-    k_exclude<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups, l->ent_offsets.p,
-                                                  l->ent_j.p, ms.p, l->m, l->ent_mask.p, l->ent_fmask.p, cnt.p);
+  if (ns > 0 && l->n_groups > 0 && l->n_entries > 0) {
+    TRY(cg.alloc(l->n_clusters, s));
+    TRY(sj.alloc(l->n_entries, s));
+    count_launch(3);
+    k_cluster_group<<<nb(l->n_groups, 256), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups, cg.p);
+    k_sorted_j<<<nb(l->n_entries, 256), 256, 0, s>>>(l->ent_jorder.p, l->ent_j.p, l->n_entries,
+                                                      l->ent_offsets.p + l->n_groups, sj.p);
+    k_exclude<<<nb(ns * EXCL_SPLIT, 128), 128, 0, s>>>(grid->perm.p, grid->inverse_perm.p, grid->fill.p, ns,
+                                                        mol_atoms, mol_first, atom_mol, cg.p, l->group_first.p,
+                                                        l->ent_offsets.p, l->ent_jorder.p, sj.p, l->m, l->ent_mask.p,
+                                                        l->ent_fmask.p, cnt.p);
     TRY(cudaGetLastError());
   }
   // canonical rows and the reference super layout are re-derived from the
@@ -2028,11 +2051,13 @@ extern "C" int nbx_list_exclude(nbx_list_t* l, const nbx_grid_t* grid, const int
     TRY(cudaStreamSynchronize(s));
     *n_removed = (int64_t)h;
   }
-  ms.release(s);
+  cg.release(s);
+  sj.release(s);
   cnt.release(s);
   return NBX_OK;
 fail:
-  ms.release(s);
+  cg.release(s);
+  sj.release(s);
   cnt.release(s);
   return NBX_ERR_CUDA;
 }

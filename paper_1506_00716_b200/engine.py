@@ -27,7 +27,7 @@ from .gridder import ClusterGrid, build_cluster_grid
 from .kernels import KernelLayout, compute_nonbonded_original
 from .model import (BOLTZMANN_KJ_MOL_K, ForcesEnergies, NonbondedParams, ParameterError, ParticleSystem,
                     SimBox, wrap_position)
-from .pairlist import ClusterPairList, build_pair_list, prune_pair_list
+from .pairlist import ClusterPairList, Molecules, build_pair_list, prune_pair_list
 
 
 # ---------------------------------------------------------------- timing (host bookkeeping)
@@ -386,7 +386,7 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     mol = None
     if constraints is not None:
         m_o, m_h = constraints.check(system)
-        mol = dev.to_device(constraints.molecules(system.n), torch.int64)
+        mol = Molecules(constraints.molecules(system.n))  # device topology, built once
     with timer.section("setup"):
         state = init_state(system, params, layout, supercluster_size=supercluster_size, policy=policy,
                            n_slabs=n_slabs, slab_min_width=slab_min_width, target_occupancy=target_occupancy,

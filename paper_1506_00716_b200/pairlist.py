@@ -184,19 +184,42 @@ def build_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, *, superclust
     return plist
 
 
+class Molecules:
+    """Molecule topology on the device for exclude_molecules: per-atom ids
+    and the atoms of each molecule (CSR), built once and reused by every
+    list rebuild.  ``ids``: one int per particle in [0, n)."""
+
+    def __init__(self, ids):
+        t = dev.to_device(ids, torch.int64)
+        n = int(t.shape[0])
+        if t.dim() != 1:
+            raise ParameterError("molecule ids must be one int per particle")
+        if n and not (0 <= int(t.min()) and int(t.max()) < n):
+            raise ParameterError(f"molecule ids must lie in [0, n={n})")
+        order = torch.argsort(t, stable=True)
+        counts = torch.bincount(t, minlength=n)
+        first = torch.zeros(n + 1, dtype=torch.int64, device=t.device)
+        first[1:] = torch.cumsum(counts, 0)
+        self.n = n
+        self.atom_mol = t.to(torch.int32).contiguous()
+        self.mol_first = first.to(torch.int32).contiguous()
+        self.mol_atoms = order.to(torch.int32).contiguous()
+
+
 def exclude_molecules(plist: ClusterPairList, molecules, count: bool = False):
     """Extension (SPC / rigid water; the reference masks only fillers and the
     diagonal, pairlist.py:106-112): remove, in place, every admitted slot pair
-    whose two particles share a molecule id (``molecules``: one int per
-    particle, original order; numpy or CUDA tensor).  Applied before the
-    prune, excluded pairs also no longer keep a row alive.  Returns the number
-    of removed slot pairs when ``count`` (one host sync), else None."""
+    whose two particles share a molecule (``molecules``: a Molecules topology,
+    or one int id per particle, original order).  Applied before the prune,
+    excluded pairs also no longer keep a row alive.  Returns the number of
+    removed slot pairs when ``count`` (one host sync), else None."""
     g = plist.grid
-    mol = dev.to_device(molecules, torch.int64).to(torch.int32).contiguous()
-    if mol.shape != (g.n,):
-        raise ParameterError(f"molecules must have shape ({g.n},), got {tuple(mol.shape)}")
+    mol = molecules if isinstance(molecules, Molecules) else Molecules(molecules)
+    if mol.n != g.n:
+        raise ParameterError(f"molecules describe {mol.n} particles, the grid has {g.n}")
     out = ctypes.c_int64(0)
-    _lib.check(_lib.load().nbx_list_exclude(plist.handle, g.handle, _lib.ptr(mol), dev.stream(),
+    _lib.check(_lib.load().nbx_list_exclude(plist.handle, g.handle, _lib.ptr(mol.atom_mol), _lib.ptr(mol.mol_first),
+                                            _lib.ptr(mol.mol_atoms), dev.stream(),
                                             ctypes.byref(out) if count else None), "list_exclude")
     plist._host = None
     plist._super = None
