@@ -654,9 +654,13 @@ def run_ours(args):
 
 def run_dd(args, world, rank, local):
     """N > 1: strong scaling of the same box over N GPUs with the slab
-    decomposition (paper_1506_00716_b200/dd.py): per step NCCL halo exchange
-    (coordinates in, forces back), local search every nstlist steps after an
-    all-gather of home positions, energies all-reduced on energy steps."""
+    decomposition (paper_1506_00716_b200/dd.py): per step halo exchange
+    (coordinates in, forces back: NVLink peer stores, NCCL fallback), local
+    search every nstlist steps after an all-gather of home positions,
+    energies all-reduced on energy steps.  Positions follow the same moving
+    trajectory as N = 1 (each rank takes its home rows of step k); lists are
+    rebuilt every nstlist steps (the trajectory's 10-step displacement stays
+    inside the buffer, so no cross-rank drift guard is needed)."""
     import datetime
 
     import torch
@@ -673,35 +677,52 @@ def run_dd(args, world, rank, local):
     system, table, occ = workload(args)
     params = make_params(args, table)
     box = system.box
+    W = max(3, args.warmup)
+    S0 = 10 * args.nstlist
+    n_setup = 2 * args.nstlist if args.nstlist <= 50 else 2
+    traj = Trajectory(system, static=args.positions == "static")
+    traj.to_device(dev, sorted(set(range(n_setup)) | set(range(S0 - W, S0 + args.steps))))
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
     dd.enable_native()
     p2p = dd.enable_p2p(system.n)  # per-step halo exchanges as NVLink peer stores (NBX_DD_P2P=0: NCCL)
     df = DomainForces(dd, system, params, M, occ, r_inner=args.rinner)
-    pos_glob = torch.from_numpy(np.array(system.positions)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    lay = df.rebuild(pos_glob)
+    lay = df.rebuild(traj.device(0))
+    homes = {}
 
-    def step(k, home_pos=None):
+    def step(k, home_pos=None, counts=None):
         nonlocal lay
+        homes[k] = lay.home  # the home set whose step-k positions this rank supplies
+        if home_pos is None:
+            home_pos = traj.device(k).index_select(0, lay.home)
         if k % args.nstlist == 0:
-            cur = df.local_pos[:lay.n_home] if home_pos is None else home_pos
-            glob = dd.allgather_home(lay.home, cur, system.n)
+            glob = dd.allgather_home(lay.home, home_pos, system.n)
             lay = df.rebuild(glob)
-        elif home_pos is not None:
+            if counts is not None:
+                counts[k] = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, box,
+                                                  R_CUT).n_within_cutoff
+        else:
             df.local_pos[:lay.n_home].copy_(home_pos)
         return df.forces(energy=(k % args.nstlist == 0))
 
-    W = max(3, args.warmup)
-    for k in range(2 * args.nstlist if args.nstlist <= 50 else 2):  # setup: memory pool steady state
+    for k in range(n_setup):  # setup: memory pool steady state
         step(k)
-    for k in range(W):
-        step(k)
+    counts = {}
+    for k in range(S0 - W, S0 + args.steps):  # counting pass over the timed steps (same rebuilds)
+        step(k, counts=counts)
     torch.cuda.synchronize()
-    st = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, box, R_CUT)
-    cnt = torch.tensor([st.n_within_cutoff, st.n_admitted], dtype=torch.int64, device=dev)
+    builds = sorted(counts)
+    within = [counts[max(b for b in builds if b <= k)] for k in range(S0, S0 + args.steps)] if builds else [0]
+    cnt = torch.tensor([float(sum(within))], dtype=torch.float64, device=dev)
     dist.all_reduce(cnt)
-    n_within, n_admitted = int(cnt[0].item()), int(cnt[1].item())
-    n_force_rank = df.plist.force_pairs(inner=True)  # this rank's kernel work (inner list if any)
+    n_within_total = float(cnt.item())
+    st = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, box, R_CUT)
+    adm = torch.tensor([st.n_admitted], dtype=torch.int64, device=dev)
+    dist.all_reduce(adm)
+    n_admitted = int(adm.item())
+    n_force_rank = df.plist.force_pairs(inner=bool(args.rinner))  # this rank's kernel work
+    for k in range(S0 - W, S0):
+        step(k)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(local)
     lib.nbx_timing_query(None, None)
@@ -712,7 +733,7 @@ def run_dd(args, world, rank, local):
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record()
-        step(W + i)
+        step(S0 + i)
         ev[i][1].record()
     torch.cuda.synchronize()
     launches = lib.nbx_launch_count() - launches0
@@ -720,24 +741,28 @@ def run_dd(args, world, rank, local):
     fk_ms, fk_n = np.zeros(1), np.zeros(1, dtype=np.int64)
     _lib.check(lib.nbx_timing_query(_lib.ptr(fk_ms), _lib.ptr(fk_n)), "timing")
     clk = clocks.stop()
+    if os.environ.get("NBX_BENCH_DEBUG"):
+        print(f"rank {rank} per-step ms:", [round(a.elapsed_time(b), 3) for a, b in ev], file=sys.stderr)
     t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
-    # e2e: home positions H2D from pinned host memory, home forces + energies D2H, every step
-    home_h = df.local_pos[:lay.n_home].cpu().pin_memory()
+    clk_all = [None] * world
+    dist.all_gather_object(clk_all, clk)
+    # e2e: this rank's home positions of step k H2D from pinned host memory,
+    # home forces + energies D2H, every step (the home sets of the timed pass)
+    host_home = {k: torch.from_numpy(traj.host(k)[homes[k].cpu().numpy()]).pin_memory()
+                 for k in range(S0 - W, S0 + args.steps)}
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     bytes_io = torch.zeros(2, dtype=torch.int64, device=dev)
-    for i in range(W + args.steps):
+    for i, k in enumerate(range(S0 - W, S0 + args.steps)):
         if i >= W:
             flush.zero_()
             ev2[i - W][0].record()
-        if home_h.shape[0] != lay.n_home:
-            home_h = df.local_pos[:lay.n_home].cpu().pin_memory()
-        hp = home_h.to(dev, non_blocking=True)
-        f, e = step(W + args.steps + i, home_pos=hp)
+        hp = host_home[k].to(dev, non_blocking=True)
+        f, e = step(k, home_pos=hp)
         f_host = torch.empty(f.shape, dtype=f.dtype).pin_memory()
         f_host.copy_(f, non_blocking=True)
-        e_host = e.to("cpu", non_blocking=True)
+        e.to("cpu", non_blocking=True)
         if i >= W:
             ev2[i - W][1].record()
             bytes_io[0] += hp.numel() * 8
@@ -755,18 +780,26 @@ def run_dd(args, world, rank, local):
     fk_avg_ms = float(fk_ms[0]) / max(1, int(fk_n[0]))
     achieved = n_force_rank * flops_per_pair(params) / (fk_avg_ms * 1e-3) / 1e12
     if rank == 0:
+        good = [c for c in clk_all if c]
+        clocks_line = None
+        if good:
+            clocks_line = {"sm_mhz": min(c["sm_mhz"] for c in good), "sm_max_mhz": max(c["sm_max_mhz"] for c in good),
+                           "reasons": sorted(set(r for c in good for r in c["reasons"])),
+                           "samples": sum(c["samples"] for c in good), "source": "nvml, all ranks (min median)"}
         line = {
             "metric": "nonbonded pair-interactions/s (useful, r<=r_c)",
-            "value": n_within * args.steps / (t_ms * 1e-3), "unit": "pairs/s", "n_gpus": world,
+            "value": n_within_total / (t_ms * 1e-3), "unit": "pairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": W, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (pair math; fp64 energy + final force accumulation)",
-            "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe)",
+            "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe; moving-trajectory stand-in)",
             "config": config(args, occ, {"parallelism": f"slab DD x{world} (half-shell halo, r_comm=r_list, "
                                                          f"{'NVLink peer stores' if p2p else 'NCCL send/recv'})"}),
             "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
-            "pairs_per_step": {"within_rc": n_within, "admitted": n_admitted},
-            "e2e": {"value": n_within * args.steps / (e2e_ms * 1e-3), "unit": "pairs/s",
+            "ns_per_day_note": "steps/s of the timed hot-path loop x 2 fs (no integrator)",
+            "pairs_per_step": {"within_rc": n_within_total / args.steps, "admitted": n_admitted},
+            "e2e": {"value": n_within_total / (e2e_ms * 1e-3), "unit": "pairs/s",
+                    "kind": "device API per rank, pinned home positions in / home forces out every step; CUDA events",
                     "h2d_bytes_per_step": int(bytes_io[0].item()) // args.steps,
                     "d2h_bytes_per_step": int(bytes_io[1].item()) // args.steps, "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": int(launches),
@@ -774,10 +807,11 @@ def run_dd(args, world, rank, local):
                          "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None, "kernel_ms": fk_avg_ms,
                          "flops_per_pair": flops_per_pair(params),
                          "pairs": "force_kernel of rank 0 (admitted pairs the kernel evaluates)"},
-            "clocks": clk,
+            "clocks": clocks_line,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
+    dd.close()
     dist.destroy_process_group()
 
 

@@ -1270,8 +1270,12 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
     t1 = t_first[c + 1];
   }
   // U transposed items per lane in flight (index loads, then partial loads);
-  // the summation order is unchanged (ascending t per lane)
+  // each lane sums its items (ascending t) in FP32 -- a handful of FP32
+  // partials, no per-item FP64 conversions -- and the lanes' sums are
+  // combined in FP64 by a fixed shuffle tree: the order never changes, so
+  // forces stay bit-reproducible
   constexpr int U = 4;
+  float sx = 0.f, sy = 0.f, sz = 0.f;
   for (int32_t t0 = tb + sidx; t0 < t1; t0 += S * U) {
     int32_t it[U];
 #pragma unroll
@@ -1293,11 +1297,14 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (it[u] < 0) break;
-      fx += pj[u].x;
-      fy += pj[u].y;
-      fz += pj[u].z;
+      sx += pj[u].x;
+      sy += pj[u].y;
+      sz += pj[u].z;
     }
   }
+  fx = sx;
+  fy = sy;
+  fz = sz;
   for (int o = 16; o >= m; o >>= 1) {
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
     fy += __shfl_xor_sync(0xffffffffu, fy, o);

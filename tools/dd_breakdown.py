@@ -40,7 +40,40 @@ def t(fn):
     return r, 1e3 * (time.perf_counter() - t0)
 
 
+def rebuild_phases(glob):
+    """DomainForces.rebuild split into its phases (same calls)."""
+    from paper_1506_00716_b200 import build_cluster_grid, build_pair_list, prune_pair_list
+    from paper_1506_00716_b200.dd import _Domain, local_occupancy
+
+    out = {}
+    lay, out["assign"] = t(lambda: dd.assign(glob))
+    ids = lay.local_ids
+
+    def gather():
+        df.local_pos = glob.index_select(0, ids).contiguous()
+        df.q = df.q_all.index_select(0, ids)
+        df.t = df.t_all.index_select(0, ids)
+        h = torch.zeros(lay.n_local, dtype=torch.uint8, device=dev)
+        h[lay.n_home:] = 1
+        df.halo = h
+    _, out["gather"] = t(gather)
+    o = occ
+    if world > 1:
+        o = local_occupancy(occ, lay.n_local, s.n, s.box.lengths, float(np.diff(dd.boundaries).max()), dd.r_comm)
+    grid, out["grid"] = t(lambda: build_cluster_grid(_Domain(lay.n_local, s.box), 4, o, positions=df.local_pos))
+    built, out["search"] = t(lambda: build_pair_list(grid, s.box, 1.1, halo=df.halo))
+    plist, out["prune"] = t(lambda: prune_pair_list(built, grid.clustered_positions_device, s.box, r_inner=0.0))
+    df.grid, df.plist = grid, plist
+    df.f = torch.empty((lay.n_local, 3), dtype=torch.float64, device=dev)
+    _, out["first_force(layout)"] = t(lambda: df.forces(energy=False))
+    return lay, out
+
+
 for rep in range(4):
+    glob, t_ag = t(lambda: dd.allgather_home(lay.home, df.local_pos[:lay.n_home], s.n))
+    lay, ph = rebuild_phases(glob)
+    if rank == 0:
+        print(f"N={world} rep {rep} phases (ms): allgather {t_ag:.3f} " + " ".join(f"{k} {v:.3f}" for k, v in ph.items()))
     glob, t_ag = t(lambda: dd.allgather_home(lay.home, df.local_pos[:lay.n_home], s.n))
     _, t_as = t(lambda: dd.assign(glob))
     lay, t_rb = t(lambda: df.rebuild(glob))
