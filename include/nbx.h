@@ -233,6 +233,17 @@ int nbx_dd_set_layout(nbx_dd_t* dd, const int64_t* send_local, int64_t n_send, i
 int nbx_dd_exchange_positions(nbx_dd_t* dd, double* local_pos, void* stream);
 /* forces: rows [n_home, ...) -> rank+1 (owner); forces from rank-1 added to send_local rows */
 int nbx_dd_reduce_forces(nbx_dd_t* dd, double* local_f, void* stream);
+/* One domain's force pass with its halo exchange (replaces the sequence
+ * nbx_dd_exchange_positions -> nbx_force -> nbx_dd_reduce_forces): on the
+ * NVLink peer path the exchange overlaps the force kernel -- the work items
+ * of the domain list that read no halo coordinate (interior groups, first in
+ * the list's work order) run while the halo rows travel; then the halo rows
+ * are taken, the boundary items run, and the halo forces are returned.
+ * Same arguments and results as nbx_force (no i_sel, no NBX_FORCE_CANONICAL);
+ * f_out: device (n_local, 3) in local order.  NCCL path: sequential. */
+int nbx_dd_force(nbx_dd_t* dd, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
+                 const double* charges, const int64_t* lj_type, const nbx_params_t* params, const double box[3],
+                 int32_t flags, double* f_out, double* e_out, int64_t* bad, void* stream);
 int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
 /* rebuild-time bookkeeping (dd.SlabDecomposition.assign): from global
  * positions (device n x 3) and host boundaries (N+1), the rank's home / halo

@@ -190,6 +190,25 @@ fail:
   return NBX_ERR_CUDA;
 }
 
+// P2P position exchange in two halves: put my face rows into rank-1's
+// region (and publish the sequence number), take rank+1's rows into my halo
+// rows (bounded wait on my flag)
+static void p2p_put_positions(nbx_dd* d, const double* local_pos, cudaStream_t s) {
+  const unsigned long long seq = ++d->seq_pos;
+  const int64_t cap = d->cap;
+  double* peer_pos = reinterpret_cast<double*>(d->peer_down);
+  unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_down + 48 * cap);
+  count_launch();
+  k_p2p_put<<<16, 256, 0, s>>>(local_pos, d->send_local.p, d->n_send, peer_pos, peer_flag, seq, d->err + 1);
+}
+static void p2p_take_positions(nbx_dd* d, double* local_pos, cudaStream_t s) {
+  const int64_t cap = d->cap;
+  const double* own = reinterpret_cast<const double*>(d->p2p_base);
+  const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap);
+  count_launch();
+  k_p2p_take<<<16, 256, 0, s>>>(flag, d->seq_pos, own, d->n_halo, nullptr, local_pos + 3 * d->n_home, 0, d->err);
+}
+
 extern "C" int nbx_dd_exchange_positions(nbx_dd_t* d, double* local_pos, void* stream) {
   if (!d || !local_pos) {
     set_error("nbx_dd_exchange_positions: bad argument");
@@ -198,16 +217,8 @@ extern "C" int nbx_dd_exchange_positions(nbx_dd_t* d, double* local_pos, void* s
   if (d->nranks == 1) return NBX_OK;
   cudaStream_t s = to_stream(stream);
   if (d->p2p) {
-    const unsigned long long seq = ++d->seq_pos;
-    const int64_t cap = d->cap;
-    double* peer_pos = reinterpret_cast<double*>(d->peer_down);
-    unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_down + 48 * cap);
-    unsigned int* done = d->err + 1;
-    count_launch(2);
-    k_p2p_put<<<16, 256, 0, s>>>(local_pos, d->send_local.p, d->n_send, peer_pos, peer_flag, seq, done);
-    const double* own = reinterpret_cast<const double*>(d->p2p_base);
-    const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap);
-    k_p2p_take<<<16, 256, 0, s>>>(flag, seq, own, d->n_halo, nullptr, local_pos + 3 * d->n_home, 0, d->err);
+    p2p_put_positions(d, local_pos, s);
+    p2p_take_positions(d, local_pos, s);
     cudaError_t e = cudaGetLastError();
     if (e) {
       set_error("nbx_dd_exchange_positions: %s", cudaGetErrorString(e));
@@ -533,4 +544,35 @@ fail:
   rb.release(s);
   set_error("nbx_dd_allgather_home: %s", cudaGetErrorString(e));
   return NBX_ERR_CUDA;
+}
+
+// One domain's force pass with the halo exchange overlapped (NVLink peer
+// path): the face rows go to rank-1 first, the work items that read no halo
+// coordinate run while the halo travels, the halo rows are taken, the
+// boundary work items run, and the halo forces go back / the face forces
+// come in (nbx_dd_reduce_forces).  NCCL path and one rank: sequential.
+extern "C" int nbx_dd_force(nbx_dd_t* d, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
+                            const double* charges, const int64_t* lj_type, const nbx_params_t* params,
+                            const double box[3], int32_t flags, double* f_out, double* e_out, int64_t* bad,
+                            void* stream) {
+  if (!d || !list || !grid || !local_pos || !params || !box || !f_out || (flags & NBX_FORCE_CANONICAL)) {
+    set_error("nbx_dd_force: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  if (d->nranks == 1 || !d->p2p) {
+    int st = nbx_dd_exchange_positions(d, local_pos, stream);
+    if (!st) st = nbx_force(list, grid, local_pos, charges, lj_type, params, box, nullptr, 0, flags, f_out, e_out, bad,
+                            stream);
+    if (!st) st = nbx_dd_reduce_forces(d, f_out, stream);
+    return st;
+  }
+  p2p_put_positions(d, local_pos, s);
+  int st = force_split(list, grid, local_pos, charges, lj_type, params, box, flags, f_out, e_out, bad, stream,
+                       [&]() {
+                         p2p_take_positions(d, local_pos, s);
+                         return NBX_OK;
+                       });
+  if (st) return st;
+  return nbx_dd_reduce_forces(d, f_out, stream);
 }

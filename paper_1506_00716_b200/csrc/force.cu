@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 
 #include "internal.cuh"
 
@@ -1644,10 +1645,31 @@ static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clu
 
 using namespace nbx;
 
-extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
-                         const double* charges, const int64_t* lj_type, const nbx_params_t* p,
-                         const double box[3], const int32_t* i_sel, int64_t n_sel, int32_t flags,
-                         double* f_out, double* e_out, int64_t* bad, void* stream) {
+namespace nbx {
+// One force evaluation in phases, so that a caller (the domain decomposition,
+// dd.cu) can interleave communication: force_setup (validation, workspace,
+// force layout, LJ table, scalars, k_gather), force_launch over a range of
+// work items, force_regather (k_gather again after halo rows changed),
+// force_finish (k_reduce, energies, rolling prune).
+struct ForceCall {
+  nbx_list* l = nullptr;
+  const nbx_grid_t* grid = nullptr;
+  cudaStream_t s = nullptr;
+  ForceArgs A{};
+  const int32_t* sel0 = nullptr;
+  double* e_grp0 = nullptr;
+  bool canonical = false, sorted_j = false, ewald = false, band = false, use_krf = false;
+  int m = 0, flags = 0;
+  int64_t ns = 0, n_work = 0;
+  const double* positions = nullptr;
+  const double* charges = nullptr;
+  const int64_t* lj_type = nullptr;
+  Box bx{};
+};
+
+static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
+                       const double* charges, const int64_t* lj_type, const nbx_params_t* p, const double box[3],
+                       const int32_t* i_sel, int64_t n_sel, int32_t flags, double* f_out, void* stream) {
   if (!lc || !grid || !p || !box || !f_out) {
     set_error("nbx_force: null argument");
     return NBX_ERR_PARAM;
@@ -1666,23 +1688,35 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     return NBX_ERR_PARAM;
   }
   cudaStream_t s = to_stream(stream);
+  C.l = l;
+  C.grid = grid;
+  C.s = s;
+  C.flags = flags;
+  C.positions = positions;
+  C.charges = charges;
+  C.lj_type = lj_type;
   ForceWork& wk = l->work;
   const int m = l->m;
+  C.m = m;
   const int64_t ns = l->n_clusters * m;
+  C.ns = ns;
   const bool canonical = (i_sel != nullptr) || (flags & NBX_FORCE_CANONICAL);
+  C.canonical = canonical;
   if (canonical) {
-    if (cudaError_t e0 = ensure_rows(l, to_stream(stream))) {
+    if (cudaError_t e0 = ensure_rows(l, s)) {
       set_error("nbx_force: %s", cudaGetErrorString(e0));
       return NBX_ERR_CUDA;
     }
   }
   const int64_t n_items = canonical ? l->n_rows : l->n_entries;
   const int64_t n_work = canonical ? (i_sel ? n_sel : l->n_clusters) : l->n_groups;
+  C.n_work = n_work;
   Box bx;
   for (int d = 0; d < 3; ++d) {
     bx.L[d] = box[d];
     bx.invL[d] = 1.0 / box[d];
   }
+  C.bx = bx;
   cudaError_t e;
   double* dtab = nullptr;
   // workspace (cached across calls on this list)
@@ -1750,9 +1784,10 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
       if (ns > 0 && (e = cudaMemsetAsync(wk.part_i.p, 0, sizeof(float4) * ns, s))) goto cuda_fail;
       if (i_sel && n_items > 0 && (e = cudaMemsetAsync(wk.part_j.p, 0, sizeof(float4) * n_items * m, s))) goto cuda_fail;
     }
-    ForceArgs A{};
+    ForceArgs& A = C.A;
     A.n_work = n_work;
     A.sel = canonical ? i_sel : l->group_order.p;
+    C.sel0 = A.sel;
     A.grp_first = canonical ? nullptr : l->group_first.p;
     A.grp_nmem = canonical ? nullptr : l->group_nmem.p;
     A.ent_off = canonical ? l->offsets.p : l->ent_offsets.p;
@@ -1761,6 +1796,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.ent_mask = canonical ? l->mask.p : l->ent_mask.p;
     // k_force_h (grouped, m = 4, 8) writes partials in j-cluster order
     const bool sorted_j = !canonical && (m == 4 || m == 8) && !use_legacy_force();
+    C.sorted_j = sorted_j;
     A.ent_tpos = sorted_j ? wk.t_pos.p : nullptr;
     // inner list only where it is safe by a margin over FP32 rounding
     // (r_inner >= r_c + 2e-4 nm); validity is decided on the device
@@ -1776,6 +1812,7 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.part_i = wk.part_i.p;
     A.part_j = wk.part_j.p;
     A.e_grp = wk.e_grp.p;
+    C.e_grp0 = wk.e_grp.p;
     A.scalars = wk.scalars.p;
     const double rc = p->r_cut;
     A.rc2 = (float)(rc * rc);
@@ -1829,37 +1866,112 @@ extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const dou
     A.pos = positions;
     A.perm = grid->perm.p;
     A.box = bx;
-    const bool band = !ewald;
-    const bool use_krf = !ewald && krf != 0.0;
-    if ((e = launch_force(m, !canonical, A, ewald ? FE_EWALD : FE_RF, use_krf, (flags & NBX_FORCE_ENERGY) != 0, band, s)))
-      goto cuda_fail;
-    if (ns > 0)
-      count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, canonical ? wk.tc_first.p : wk.t_first.p,
-                                           canonical ? wk.tc_items.p : (sorted_j ? nullptr : wk.t_items.p), grid->perm.p,
-                                           grid->fill.p, l->n_clusters, m, flags, f_out, wk.scalars.p + 1,
-                                           !canonical && wk.t_split,
-                                           (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
-                                           wk.scalars.p + A.inner_slot);
-    if (!(flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
-      // nothing else to produce
-    } else {
-      if (!(flags & NBX_FORCE_ENERGY)) {
-        count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, 0, nullptr, wk.scalars.p, bad);
-      } else {
-        count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, n_work, e_out, wk.scalars.p, bad);
-      }
-    }
-    if ((e = cudaGetLastError())) goto cuda_fail;
-    // rolling prune at this call's coordinates (after the pass that used the old masks)
-    if ((flags & NBX_FORCE_REPRUNE) && sorted_j && l->ent_fmask.p && ns > 0 &&
-        (e = reprune_inner(l, wk.xyzq.p, wk.scalars.p, grid->bbox.p, grid->cpos.p, box, s)))
-      goto cuda_fail;
+    C.ewald = ewald;
+    C.band = !ewald;
+    C.use_krf = !ewald && krf != 0.0;
   }
+  if ((e = cudaGetLastError())) goto cuda_fail;
   return NBX_OK;
 cuda_fail:
   if (dtab) cudaFreeAsync(dtab, s);
   set_error("nbx_force: %s", cudaGetErrorString(e));
   return NBX_ERR_CUDA;
+}
+
+// the force kernel over work items [w0, w1) of the work order (persistent
+// warps claim them through scalars[4], reset here; energies per item land at
+// e_grp[2 (w0 + i)], so the ranges of one evaluation add up in k_energy)
+static cudaError_t force_launch(ForceCall& C, int64_t w0, int64_t w1) {
+  if (w1 <= w0) return cudaSuccess;
+  ForceArgs A = C.A;
+  A.sel = C.sel0 ? C.sel0 + w0 : nullptr;
+  if (!C.sel0 && w0 != 0) return cudaErrorInvalidValue;  // identity order: one range only
+  A.n_work = w1 - w0;
+  A.e_grp = C.e_grp0 + 2 * w0;
+  cudaError_t e = cudaMemsetAsync(A.scalars + 4, 0, sizeof(unsigned int), C.s);
+  if (e) return e;
+  return launch_force(C.m, !C.canonical, A, C.ewald ? FE_EWALD : FE_RF, C.use_krf,
+                      (C.flags & NBX_FORCE_ENERGY) != 0, C.band, C.s);
+}
+
+static cudaError_t force_regather(ForceCall& C) {
+  if (C.ns <= 0) return cudaSuccess;
+  ForceWork& wk = C.l->work;
+  count_launch();
+  k_gather<<<nb(C.ns, 256), 256, 0, C.s>>>(C.positions, C.charges, C.lj_type, C.grid->perm.p, C.grid->fill.p,
+                                           C.grid->cpos.p, C.grid->bbox.p, C.m, C.ns, C.bx, wk.xyzq.p, wk.type.p,
+                                           wk.scalars.p, C.canonical ? nullptr : C.l->xprune.p);
+  return cudaGetLastError();
+}
+
+static int force_finish(ForceCall& C, const double box[3], double* f_out, double* e_out, int64_t* bad) {
+  nbx_list* l = C.l;
+  ForceWork& wk = l->work;
+  cudaStream_t s = C.s;
+  const ForceArgs& A = C.A;
+  cudaError_t e;
+  if (C.ns > 0)
+    count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, C.canonical ? wk.tc_first.p : wk.t_first.p,
+                                         C.canonical ? wk.tc_items.p : (C.sorted_j ? nullptr : wk.t_items.p), C.grid->perm.p,
+                                         C.grid->fill.p, l->n_clusters, C.m, C.flags, f_out, wk.scalars.p + 1,
+                                         !C.canonical && wk.t_split,
+                                         (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
+                                         wk.scalars.p + A.inner_slot);
+  if (!(C.flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
+    // nothing else to produce
+  } else {
+    if (!(C.flags & NBX_FORCE_ENERGY)) {
+      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, 0, nullptr, wk.scalars.p, bad);
+    } else {
+      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, C.n_work, e_out, wk.scalars.p, bad);
+    }
+  }
+  if ((e = cudaGetLastError())) goto cuda_fail;
+  // rolling prune at this call's coordinates (after the pass that used the old masks)
+  if ((C.flags & NBX_FORCE_REPRUNE) && C.sorted_j && l->ent_fmask.p && C.ns > 0 &&
+      (e = reprune_inner(l, wk.xyzq.p, wk.scalars.p, C.grid->bbox.p, C.grid->cpos.p, box, s)))
+    goto cuda_fail;
+  return NBX_OK;
+cuda_fail:
+  set_error("nbx_force: %s", cudaGetErrorString(e));
+  return NBX_ERR_CUDA;
+}
+
+int force_split(const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions, const double* charges,
+                const int64_t* lj_type, const nbx_params_t* p, const double box[3], int32_t flags, double* f_out,
+                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between) {
+  ForceCall C;
+  int st = force_setup(C, lc, grid, positions, charges, lj_type, p, box, nullptr, 0, flags, f_out, stream);
+  if (st) return st;
+  const int64_t n_int = C.canonical ? -1 : C.l->n_interior;
+  cudaError_t e;
+  if (n_int < 0) {  // no interior / boundary split: one range, the caller's hook first
+    if ((st = between())) return st;
+    if ((e = force_regather(C)) || (e = force_launch(C, 0, C.n_work))) goto fail;
+    return force_finish(C, box, f_out, e_out, bad);
+  }
+  if ((e = force_launch(C, 0, n_int))) goto fail;
+  if ((st = between())) return st;
+  if ((e = force_regather(C)) || (e = force_launch(C, n_int, C.n_work))) goto fail;
+  return force_finish(C, box, f_out, e_out, bad);
+fail:
+  set_error("nbx_force: %s", cudaGetErrorString(e));
+  return NBX_ERR_CUDA;
+}
+}  // namespace nbx
+
+extern "C" int nbx_force(const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
+                         const double* charges, const int64_t* lj_type, const nbx_params_t* p,
+                         const double box[3], const int32_t* i_sel, int64_t n_sel, int32_t flags,
+                         double* f_out, double* e_out, int64_t* bad, void* stream) {
+  ForceCall C;
+  int st = force_setup(C, lc, grid, positions, charges, lj_type, p, box, i_sel, n_sel, flags, f_out, stream);
+  if (st) return st;
+  if (cudaError_t e = force_launch(C, 0, C.n_work)) {
+    set_error("nbx_force: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return force_finish(C, box, f_out, e_out, bad);
 }
 
 namespace nbx {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -142,6 +143,10 @@ struct List {
   DBuf<int32_t> super_offsets, super_j, super_pair;
   ForceWork work;
   bool ordered = false;  // finalize_force_layout done
+  // domain lists: per-cluster halo bits and the number of interior work
+  // items (groups touching no halo particle, first in group_order; -1: none)
+  DBuf<uint8_t> halo_cl;
+  int64_t n_interior = -1;
   int mask_words() const { return m == 8 ? 2 : 1; }
 };
 
@@ -161,6 +166,11 @@ cudaError_t ensure_rows(List* l, cudaStream_t s);
 // (k_gather output; scalars[0] = their max displacement since the build)
 cudaError_t reprune_inner(List* l, const float4* xyzq, const unsigned int* scalars, const double* bbox,
                           const double* cpos, const double box[3], cudaStream_t s);
+// one force evaluation with a hook between the interior and the boundary
+// work items of a domain list (force.cu; dd.cu runs the halo exchange there)
+int force_split(const nbx_list_t* l, const nbx_grid_t* grid, const double* positions, const double* charges,
+                const int64_t* lj_type, const nbx_params_t* p, const double box[3], int32_t flags, double* f_out,
+                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

@@ -1133,9 +1133,32 @@ __global__ void k_group_keys(const int32_t* __restrict__ ent_off, const int32_t*
 }
 
 // force-kernel work order: groups by descending estimated cost (LPT)
+// domain lists (halo bits): a group is BOUNDARY when one of its clusters or
+// one of its entries' j-clusters holds a halo particle; bit 30 of its work
+// key, so interior groups -- which read no halo coordinates -- come first
+// and the halo exchange can overlap them (dd.cu nbx_dd_force).  One warp per
+// group; counts the interior groups.
+__global__ void k_group_boundary(const int32_t* __restrict__ grp_first, const int32_t* __restrict__ grp_nmem,
+                                 int64_t n_groups, const int32_t* __restrict__ ent_off,
+                                 const int32_t* __restrict__ ent_j, const uint8_t* __restrict__ halo_cl,
+                                 int32_t* __restrict__ keys, unsigned int* __restrict__ n_interior) {
+  const int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const int lane = threadIdx.x & 31;
+  bool b = lane < grp_nmem[g] && halo_cl[grp_first[g] + lane] != 0;
+  for (int32_t e = ent_off[g] + lane; e < ent_off[g + 1]; e += 32) b = b || halo_cl[ent_j[e]] != 0;
+  const bool boundary = __any_sync(0xffffffffu, b);
+  if (lane == 0) {
+    if (boundary) keys[g] |= 1 << 30;
+    else atomicAdd(n_interior, 1u);
+  }
+}
+
 static cudaError_t order_groups(List* l, cudaStream_t s) {
   DBuf<int32_t> keys, keys2, vals;
+  DBuf<unsigned int> nint;
   cudaError_t e;
+  l->n_interior = -1;
   if ((e = l->group_order.alloc(l->n_groups, s))) return e;
   if (l->n_groups == 0) return cudaSuccess;
   if ((e = keys.alloc(l->n_groups, s)) || (e = keys2.alloc(l->n_groups, s)) || (e = vals.alloc(l->n_groups, s)))
@@ -1143,8 +1166,20 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
   count_launch();
   k_group_keys<<<nb(l->n_groups, 256), 256, 0, s>>>(l->ent_offsets.p, l->group_nmem.p, l->ent_fend.p, l->n_groups,
                                                      keys.p, vals.p);
-  e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, 30, s);
-  keys.release(s); keys2.release(s); vals.release(s);
+  const bool split = l->halo_cl.p != nullptr;
+  if (split) {
+    if ((e = nint.alloc(1, s)) || (e = cudaMemsetAsync(nint.p, 0, 4, s))) return e;
+    count_launch();
+    k_group_boundary<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups,
+                                                         l->ent_offsets.p, l->ent_j.p, l->halo_cl.p, keys.p, nint.p);
+  }
+  e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, split ? 31 : 30, s);
+  if (!e && split) {
+    unsigned int h = 0;
+    if (!(e = cudaMemcpyAsync(&h, nint.p, 4, cudaMemcpyDeviceToHost, s)) && !(e = cudaStreamSynchronize(s)))
+      l->n_interior = h;
+  }
+  keys.release(s); keys2.release(s); vals.release(s); nint.release(s);
   return e;
 }
 
@@ -1384,6 +1419,7 @@ static void list_release(nbx_list* l, cudaStream_t s) {
   l->group_first.release(s);
   l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
   l->ent_delta.release(s); l->ent_mask.release(s); l->ent_pres.release(s); l->ent_jorder.release(s);
+  l->halo_cl.release(s);
   l->ent_fmask.release(s); l->ent_fend.release(s); l->xprune.release(s);
   l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
   ForceWork& w = l->work;
@@ -1530,6 +1566,7 @@ static int pairlist_build_impl(const nbx_grid_t* grid, const double box[3], doub
   }
   TRY(cudaGetLastError());
   ent_count.release(s); stash.release(s);
+  if (hbits.p) std::swap(l->halo_cl, hbits);  // per-cluster halo bits: interior / boundary work split
   hbits.release(s); xl.release(s);
   *out = l;
   return NBX_OK;
@@ -1642,6 +1679,10 @@ extern "C" int nbx_pairlist_prune_inner(const nbx_list_t* in, const nbx_grid_t* 
   }
   TRY(cudaGetLastError());
   l->entries_ordered = true;
+  if (in->halo_cl.p) {  // the domain's halo bits travel with the list
+    TRY(l->halo_cl.alloc(nc, s));
+    TRY(cudaMemcpyAsync(l->halo_cl.p, in->halo_cl.p, nc, cudaMemcpyDeviceToDevice, s));
+  }
   alive.release(s); xl.release(s); ekeep.release(s); dmax.release(s);
   *out = l;
   return NBX_OK;

@@ -19,6 +19,7 @@ from paper_1506_00716_b200.systems import spc_water, tuned_occupancy  # noqa: E4
 ap = argparse.ArgumentParser()
 ap.add_argument("--atoms", type=int, default=96000)
 ap.add_argument("--torch-p2p", action="store_true")
+ap.add_argument("--p2p", action="store_true", help="NVLink peer-store exchanges (overlapped with the force pass)")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -34,8 +35,12 @@ pos = torch.from_numpy(np.array(s.positions)).to(dev)
 dd = SlabDecomposition(L, world, rank, r_comm=1.1)
 if '--torch-p2p' not in sys.argv:
     dd.enable_native()
+    if a.p2p:
+        print(f"rank {rank}: p2p {dd.enable_p2p(s.n)}")
+df_overlap = a.p2p
 df = DomainForces(dd, s, params, 4, occ)
 lay = df.rebuild(pos)
+df.overlap = a.p2p  # the overlapped nbx_dd_force path
 home_f, e = df.forces(energy=True)
 glob = dd.allgather_home(lay.home, home_f, s.n)
 st = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, s.box, 1.0)

@@ -51,10 +51,13 @@ def run(tag):
     return f0, e0
 
 
-fn, en = run("nccl")
+fn, en = run("nccl (sequential)")
 ok = dd.enable_p2p(s.n)
-fp, ep = run("p2p " + str(ok))
-same = torch.equal(fn, fp) and torch.equal(en, ep)
+df.overlap = False
+fs, es = run("p2p sequential " + str(ok))
+df.overlap = True
+fp, ep = run("p2p overlapped (nbx_dd_force) " + str(ok))
+same = torch.equal(fn, fp) and torch.equal(en, ep) and torch.equal(fn, fs) and torch.equal(en, es)
 flag = torch.tensor([0 if same else 1], device=dev)
 dist.all_reduce(flag)
 err = dd.p2p_error()
