@@ -195,6 +195,48 @@ class SlabDecomposition:
         except Exception:  # never raise from a finaliser (interpreter exit)
             pass
 
+    # ---------------------------------------------------------------- load balance
+    def rebalance(self, times, alpha: float = 0.5) -> np.ndarray:
+        """Move the slab boundaries toward equal force time per rank (the
+        role of the reference's rebalance_slabs, engine.py:208-263, by a
+        different rule).  Each slab's measured time is spread uniformly over
+        its width, giving a piecewise-linear cumulative cost along x; the new
+        boundaries are its N-quantiles (equal cost per slab), blended with
+        the old ones by ``alpha`` (damping), then widened where needed so
+        every slab keeps the single-neighbour halo (>= r_comm) and the
+        periodic-image bound of the constructor.  ``times`` (one positive
+        float per rank) must be identical on every rank (e.g. all-gathered),
+        so every rank computes the same boundaries.  Returns them."""
+        t = np.asarray(times, dtype=np.float64).reshape(-1)
+        if t.shape != (self.N,):
+            raise ParameterError(f"expected {self.N} per-rank times, got shape {t.shape}")
+        if not np.all(np.isfinite(t)) or np.any(t <= 0.0):
+            raise ParameterError("per-rank times must be positive and finite")
+        if not 0.0 < alpha <= 1.0:
+            raise ParameterError(f"alpha must be in (0, 1], got {alpha}")
+        if self.N == 1:
+            return self.boundaries
+        b = self.boundaries
+        cum = np.concatenate([[0.0], np.cumsum(t)])
+        quant = np.interp(cum[-1] * np.arange(self.N + 1) / self.N, cum, b)
+        new = alpha * quant + (1.0 - alpha) * b
+        new[0], new[-1] = b[0], b[-1]
+        Lx = float(self.L[0])
+        w_max = Lx - 2.0 * self.r_comm - 1e-9 * Lx
+        w = np.diff(new)
+        for _ in range(2 * self.N):  # clamp to [r_comm, w_max], redistribute the excess / deficit
+            lo, hi = w < self.r_comm, w > w_max
+            if not (lo.any() or hi.any()):
+                break
+            w = np.clip(w, self.r_comm, w_max)
+            free = ~(lo | hi)
+            if free.any():
+                w[free] += (Lx - w.sum()) * w[free] / w[free].sum()
+        new = np.concatenate([[b[0]], b[0] + np.cumsum(w)])
+        new[-1] = b[-1]
+        self.boundaries = new
+        return new
+
     # ---------------------------------------------------------------- geometry
     def owner(self, x) -> np.ndarray:
         xw = _wrap_np(np.asarray(x, dtype=np.float64), self.L[0])
@@ -406,10 +448,22 @@ class DomainForces:
         self.grid = None
         self.plist = None
 
-    def rebuild(self, positions_global: torch.Tensor) -> DomainLayout:
+    def rebuild(self, positions_global: torch.Tensor, balance: bool = False) -> DomainLayout:
+        """Re-decompose (optionally rebalancing the slabs from the ranks'
+        measured force-pass times first: collective) and rebuild the local
+        grid and list."""
         from . import build_cluster_grid, build_pair_list, prune_pair_list
 
         self.dd.check_p2p()
+        if balance and self.dd.N > 1 and getattr(self, "_ev", None) is not None:
+            import torch.distributed as dist
+
+            self._ev[1].synchronize()
+            t = torch.tensor([max(self._ev[0].elapsed_time(self._ev[1]), 1e-6)], dtype=torch.float64,
+                             device=positions_global.device)
+            allt = [torch.zeros_like(t) for _ in range(self.dd.N)]
+            dist.all_gather(allt, t, group=self.dd.group)
+            self.dd.rebalance(torch.cat(allt).cpu().numpy())
         lay = self.dd.assign(positions_global)
         dev = positions_global.device
         ids = lay.local_ids
@@ -455,6 +509,10 @@ class DomainForces:
         from . import compute_nonbonded_device
 
         overlap = getattr(self, "overlap", os.environ.get("NBX_DD_OVERLAP", "0") == "1")
+        if self.local_pos.is_cuda:  # this rank's force-pass time (slab rebalancing)
+            if getattr(self, "_ev", None) is None:
+                self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self._ev[0].record()
         if self.dd._native is not None and self.local_pos.is_cuda and overlap:
             import ctypes
 
@@ -470,11 +528,14 @@ class DomainForces:
                 _lib.ptr(self.bad), _device.stream()), "dd_force")
             del table
             home_f = self.f[:self.dd.layout.n_home]
+            self._ev[1].record()
             e = self.dd.allreduce_energies(self.e.clone()) if energy else self.e
             return home_f, e
         self.dd.exchange_positions(self.local_pos)
         compute_nonbonded_device(self.plist, self.grid, self.local_pos, self.q, self.t, self.params,
                                  self.system.box, energy=energy, out=self.f, e_out=self.e, bad=self.bad)
         home_f = self.dd.reduce_halo_forces(self.f)
+        if self.local_pos.is_cuda:
+            self._ev[1].record()
         e = self.dd.allreduce_energies(self.e.clone()) if energy else self.e
         return home_f, e

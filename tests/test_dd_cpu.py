@@ -110,3 +110,92 @@ def test_slab_geometry_checks():
     assert lay.home.tolist() == [1, 2, 3]          # slab 1 = [2.45, 4.9)
     assert lay.send.tolist() == [1, 2]             # within r_comm of its -x face
     assert lay.halo.tolist() == [4, 5]             # slab 2 within r_comm of 4.9
+
+
+def test_rebalance_rule():
+    """Equal times keep the slabs; a slow rank's slab shrinks toward the cost
+    quantile (damped by alpha); widths stay >= r_comm and below the
+    periodic-image bound; every rank computes the same boundaries."""
+    from paper_1506_00716_b200.dd import SlabDecomposition
+    from paper_1506_00716_b200.model import ParameterError
+
+    L = [24.6, 24.6, 24.6]
+    dd = SlabDecomposition(L, 4, 0, r_comm=1.1)
+    b0 = dd.boundaries.copy()
+    assert np.allclose(dd.rebalance([1.0, 1.0, 1.0, 1.0]), b0)
+    dd = SlabDecomposition(L, 4, 0, r_comm=1.1)
+    b = dd.rebalance([2.0, 1.0, 1.0, 1.0], alpha=1.0)
+    # slab 0 holds 2/5 of the cost in 6.15 nm: the first quantile (1/4 of the
+    # cost) sits at 6.15 * (5/4) / 2 = 3.84 nm
+    assert abs(b[1] - 6.15 * 1.25 / 2.0) < 1e-9
+    assert np.all(np.diff(b) >= 1.1 - 1e-12) and b[0] == 0.0 and b[-1] == 24.6
+    other = SlabDecomposition(L, 4, 3, r_comm=1.1)
+    assert np.array_equal(other.rebalance([2.0, 1.0, 1.0, 1.0], alpha=1.0), b)
+    dd = SlabDecomposition(L, 4, 0, r_comm=2.0)
+    b = dd.rebalance([1000.0, 1.0, 1.0, 1.0], alpha=1.0)  # extreme: quantiles 1.54 nm apart, clamped at r_comm
+    assert np.allclose(b, [0.0, 2.0, 4.0, 6.0, 24.6])
+    with pytest.raises(ParameterError):
+        dd.rebalance([1.0, -1.0, 1.0, 1.0])
+
+
+def _worker_uneven(rank, world, port, out_q):
+    """as _worker, with the slab boundaries moved by the rebalancing rule"""
+    import datetime
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
+    try:
+        from oracle import forces as of
+        from paper_1506_00716_b200.dd import SlabDecomposition
+        from paper_1506_00716_b200.systems import spc_water
+
+        s, table = spc_water(3000 * 4)
+        L = s.box.lengths
+        phys = of.Physics(r_cut=1.0, lj_table=table, shift_potential=True)
+        dd = SlabDecomposition(L, world, rank, r_comm=1.1)
+        t = torch.tensor([1.0 + rank], dtype=torch.float64)  # rank 1 "slower"
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        dd.rebalance(torch.cat(allt).numpy(), alpha=0.5)
+        lay = dd.assign(s.positions)
+        ids = lay.local_ids.numpy()
+        local = torch.zeros((lay.n_local, 3), dtype=torch.float64)
+        local[:lay.n_home] = torch.from_numpy(s.positions[lay.home.numpy()])
+        dd.exchange_positions(local)
+        halo = np.zeros(lay.n_local, dtype=bool)
+        halo[lay.n_home:] = True
+        f, elj, ec = _local_oracle_forces(local.numpy(), s.charges[ids], s.lj_type[ids], halo, L, phys)
+        home_f = dd.reduce_halo_forces(torch.from_numpy(f))
+        e = dd.allreduce_energies(torch.tensor([elj, ec], dtype=torch.float64))
+        glob = dd.allgather_home(lay.home, home_f, s.n)
+        if rank == 0:
+            out_q.put((glob.numpy(), e.numpy(), dd.boundaries.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rebalanced_decomposition_equals_single_domain():
+    from oracle import forces as of
+    from oracle import native, search
+    from paper_1506_00716_b200.systems import spc_water
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uneven, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    f_dd, e_dd, bnd = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    s, table = spc_water(12000)
+    L = s.box.lengths
+    assert abs(bnd[1] - 0.5 * L[0]) > 0.1  # the boundary did move
+    og = search.build_grid(s.positions, L, 4, None)
+    ol = native.prune_list(native.search_list(og, L, 1.1), og["clustered_positions"], L)
+    fc, elj, ec = native.list_forces(ol, og, s.positions, s.charges, s.lj_type, L,
+                                     of.Physics(r_cut=1.0, lj_table=table, shift_potential=True), threads=2)
+    f_ref = search.scatter_to_original(og, fc)
+    assert np.abs(f_dd - f_ref).max() <= 1e-9 * np.abs(f_ref).max()
+    assert abs(e_dd[0] - elj) <= 1e-9 * abs(elj) and abs(e_dd[1] - ec) <= 1e-9 * abs(ec)
