@@ -363,9 +363,9 @@ extern "C" void nbx_dd_free(nbx_dd_t* d) {
   if (d->p2p_base) cudaFree(d->p2p_base);
   if (d->err) cudaFree(d->err);
   if (d->comm) ncclCommDestroy(d->comm);
-  d->send_local.release(0);
-  d->sendbuf.release(0);
-  d->recvbuf.release(0);
+  d->send_local.drop(0);
+  d->sendbuf.drop(0);
+  d->recvbuf.drop(0);
   delete d;
 }
 

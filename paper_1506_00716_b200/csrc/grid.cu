@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -243,6 +244,45 @@ cudaMemPool_t nbx::device_pool() {
   return pool;
 }
 
+namespace {
+struct CacheKey {
+  int dev;
+  cudaStream_t s;
+  size_t bytes;
+  bool operator<(const CacheKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (s != o.s) return s < o.s;
+    return bytes < o.bytes;
+  }
+};
+std::mutex g_cmu;
+std::map<CacheKey, std::vector<void*>> g_cache;
+size_t g_cached = 0;
+constexpr size_t kCacheMax = size_t(4) << 30;  // held in the cache at most
+}  // namespace
+
+void* nbx::cache_take(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_cmu);
+  auto it = g_cache.find(CacheKey{dev, s, bytes});
+  if (it == g_cache.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  g_cached -= bytes;
+  return p;
+}
+
+bool nbx::cache_put(void* p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  if (!p || bytes == 0 || cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(g_cmu);
+  if (g_cached + bytes > kCacheMax) return false;
+  g_cache[CacheKey{dev, s, bytes}].push_back(p);
+  g_cached += bytes;
+  return true;
+}
+
 cudaError_t nbx::pool_malloc(void** p, size_t bytes, cudaStream_t s) {
   cudaMemPool_t pool = device_pool();
   if (!pool) return cudaMallocAsync(p, bytes, s);
@@ -447,9 +487,9 @@ extern "C" int nbx_scatter_to_original(const nbx_grid_t* g, const double* cluste
 extern "C" void nbx_grid_free(nbx_grid_t* g) {
   if (!g) return;
   cudaStream_t s = 0;
-  g->perm.release(s); g->inverse_perm.release(s); g->fill.release(s);
-  g->cell_of_cluster.release(s); g->col_first.release(s); g->cpos.release(s);
-  g->bbox.release(s); g->zr.release(s); g->bbf.release(s); g->nreal.release(s);
-  g->group_first.release(s); g->group_nmem.release(s);
+  g->perm.drop(s); g->inverse_perm.drop(s); g->fill.drop(s);
+  g->cell_of_cluster.drop(s); g->col_first.drop(s); g->cpos.drop(s);
+  g->bbox.drop(s); g->zr.drop(s); g->bbf.drop(s); g->nreal.drop(s);
+  g->group_first.drop(s); g->group_nmem.drop(s);
   delete g;
 }

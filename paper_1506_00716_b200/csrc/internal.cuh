@@ -18,16 +18,32 @@ namespace nbx {
 cudaMemPool_t device_pool();
 cudaError_t pool_malloc(void** p, size_t bytes, cudaStream_t s);
 
+// Per-call temporaries are recycled through a small host-side cache of freed
+// blocks keyed by (device, stream, size class) before the stream-ordered pool:
+// a list step allocates and frees ~60 temporaries, and the ~2 us host cost of
+// each pool call was a visible share of the host time that leaves the GPU idle
+// between the list step's small kernels.  A block is reused only on the
+// stream it was freed on (stream order keeps that safe); long-lived buffers
+// of grids and lists are returned to the pool directly (drop()).
+void* cache_take(size_t bytes, cudaStream_t s);
+bool cache_put(void* p, size_t bytes, cudaStream_t s);
+
 // Device buffer with stream-ordered allocation.
 template <typename T>
 struct DBuf {
   T* p = nullptr;
   int64_t n = 0;
+  size_t bytes = 0;
   cudaError_t alloc(int64_t count, cudaStream_t s) {
     release(s);
     n = count;
     if (count <= 0) return cudaSuccess;
-    return pool_malloc(reinterpret_cast<void**>(&p), size_class(sizeof(T) * (size_t)count), s);
+    bytes = size_class(sizeof(T) * (size_t)count);
+    if (void* c = cache_take(bytes, s)) {
+      p = reinterpret_cast<T*>(c);
+      return cudaSuccess;
+    }
+    return pool_malloc(reinterpret_cast<void**>(&p), bytes, s);
   }
   // round up to {1, 1.25, 1.5, 1.75} x 2^k so that the per-rebuild buffers of
   // slightly different sizes reuse the same pool blocks
@@ -39,9 +55,16 @@ struct DBuf {
     return ((b + q - 1) / q) * q;
   }
   void release(cudaStream_t s) {
+    if (p && !cache_put(p, bytes, s)) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+    bytes = 0;
+  }
+  void drop(cudaStream_t s) {  // back to the pool (buffers of grids / lists)
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    bytes = 0;
   }
 };
 

@@ -1415,17 +1415,17 @@ out:
 using namespace nbx;
 
 static void list_release(nbx_list* l, cudaStream_t s) {
-  l->offsets.release(s); l->j.release(s); l->mask.release(s); l->delta.release(s);
-  l->group_first.release(s);
-  l->group_nmem.release(s); l->group_order.release(s); l->ent_offsets.release(s); l->ent_j.release(s);
-  l->ent_delta.release(s); l->ent_mask.release(s); l->ent_pres.release(s); l->ent_jorder.release(s);
-  l->halo_cl.release(s);
-  l->ent_fmask.release(s); l->ent_fend.release(s); l->xprune.release(s);
-  l->super_offsets.release(s); l->super_j.release(s); l->super_pair.release(s);
+  l->offsets.drop(s); l->j.drop(s); l->mask.drop(s); l->delta.drop(s);
+  l->group_first.drop(s);
+  l->group_nmem.drop(s); l->group_order.drop(s); l->ent_offsets.drop(s); l->ent_j.drop(s);
+  l->ent_delta.drop(s); l->ent_mask.drop(s); l->ent_pres.drop(s); l->ent_jorder.drop(s);
+  l->halo_cl.drop(s);
+  l->ent_fmask.drop(s); l->ent_fend.drop(s); l->xprune.drop(s);
+  l->super_offsets.drop(s); l->super_j.drop(s); l->super_pair.drop(s);
   ForceWork& w = l->work;
-  w.xyzq.release(s); w.type.release(s); w.part_i.release(s); w.part_j.release(s);
-  w.e_grp.release(s); w.scalars.release(s); w.lj.release(s); w.t_first.release(s);
-  w.t_items.release(s); w.t_pos.release(s); w.tc_first.release(s); w.tc_items.release(s);
+  w.xyzq.drop(s); w.type.drop(s); w.part_i.drop(s); w.part_j.drop(s);
+  w.e_grp.drop(s); w.scalars.drop(s); w.lj.drop(s); w.t_first.drop(s);
+  w.t_items.drop(s); w.t_pos.drop(s); w.tc_first.drop(s); w.tc_items.drop(s);
 }
 
 extern "C" void nbx_list_free(nbx_list_t* l) {
