@@ -961,7 +961,7 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
         for (int q = 0; q < W; ++q) cp_async(&S.em[slot][lane][q], emask + (int64_t)e * W + q, 8);
         cp_async(&S.cj[slot][lane], A.ent_j + e, 4);
-        if (A.ent_tpos) cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
+        cp_async(&S.tp[slot][lane], A.ent_tpos + e, 4);
       }
     };
     auto stage_jatoms = [&](int xslot, int eslot) {
@@ -1028,7 +1028,6 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
     for (int h = 0; h < 4; ++h) fi[h][0] = fi[h][1] = fi[h][2] = make_float2(0.f, 0.f);
     double elj_acc = 0.0, ec_acc = 0.0;
-    float4* pj = A.part_j + (int64_t)(e_beg + r) * M + ba;
     const int sha_ = 8 * ih * (W == 1) + 32 * ih * (W == 2) + 2 * jp;  // mask shift of the lane's pairs
 
     int es = 0;
@@ -1054,7 +1053,7 @@ k_force_h(const ForceArgs A) {
       es = es == 2 ? 0 : es + 1;
       const int32_t c_end = min(ec0 + CH, e_end);
 #pragma unroll 1
-    for (int32_t e0 = ec0, ci = 0; e0 < c_end; e0 += R, ci += R, pj += R * M) {
+    for (int32_t e0 = ec0, ci = 0; e0 < c_end; e0 += R, ci += R) {
       const bool valid = e0 + r < e_end;
       const int ce = ci + r;  // entry within the chunk
       const float4 d = c_ed[ce];
@@ -1132,16 +1131,12 @@ k_force_h(const ForceArgs A) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) out[c] = fj[0][c] + __shfl_xor_sync(0xffffffffu, fj[1][c], 16);
       if (valid) {
-        // partials land in j-cluster order (t_pos), so k_reduce streams them
-        // (packed xyz, 12 B per partial: a quarter less traffic than float4)
-        if (A.ent_tpos) {
-          float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)c_tp[ce] * M + ba) * 3;
-          dst[0] = out[0];
-          dst[1] = out[1];
-          dst[2] = out[2];
-        } else {
-          *pj = make_float4(out[0], out[1], out[2], 0.f);
-        }
+        // partials land in j-cluster order (t_pos, always set for this
+        // kernel), so k_reduce streams them (packed xyz, 12 B per partial)
+        float* dst = reinterpret_cast<float*>(A.part_j) + ((int64_t)c_tp[ce] * M + ba) * 3;
+        dst[0] = out[0];
+        dst[1] = out[1];
+        dst[2] = out[2];
       }
       if (ENERGY) {
         elj_acc += (double)elj;
@@ -1867,7 +1862,11 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
     A.perm = grid->perm.p;
     A.box = bx;
     C.ewald = ewald;
-    C.band = !ewald;
+    // FP64 re-check of cutoff decisions near r_c only where the Coulomb force
+    // jumps there: plain cutoff (the reference's physics) and a
+    // reaction field with finite eps_rf.  eps_rf = inf (2 k_rf r_c^3 = 1) and
+    // Ewald have F_c(r_c) ~ 0, so a rounding flip at r_c changes nothing.
+    C.band = !ewald && fabs(1.0 - 2.0 * krf * rc * rc * rc) > 1e-6;
     C.use_krf = !ewald && krf != 0.0;
   }
   if ((e = cudaGetLastError())) goto cuda_fail;

@@ -9,7 +9,7 @@ from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) > 1 and r[0].startswith("0x")]
 iA, iS = hdr.index("Address"), hdr.index("Source")
 iW, iE = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 base = int(data[0][iA], 16)
