@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -432,6 +433,10 @@ extern "C" int nbx_grid_info(const nbx_grid_t* g, int64_t out[5]) {
 template <typename TD, typename TH>
 static cudaError_t download_widen(const TD* d, int64_t count, TH* h, cudaStream_t s) {
   if (!h || count <= 0) return cudaSuccess;
+  if (std::is_same<TD, TH>::value) {  // no widening: straight into the caller's buffer
+    cudaError_t e = cudaMemcpyAsync(h, d, sizeof(TD) * (size_t)count, cudaMemcpyDeviceToHost, s);
+    return e ? e : cudaStreamSynchronize(s);
+  }
   TD* tmp = (TD*)malloc(sizeof(TD) * (size_t)count);
   cudaError_t e = cudaMemcpyAsync(tmp, d, sizeof(TD) * (size_t)count, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);

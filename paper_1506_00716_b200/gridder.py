@@ -81,30 +81,42 @@ class ClusterGrid:
         """The build-time clustered positions without leaving the device."""
         return DeviceArray(self.clustered_positions_device_ptr(), (self.n_slots, 3), self)
 
-    # -- host materialisation
-    def _materialise(self) -> dict:
+    # -- host materialisation (per field: a caller that reads one field --
+    # e.g. clustered_positions to hand it back to prune_pair_list -- does not
+    # pay for the downloads of the others)
+    _FIELDS = ("perm", "inverse_perm", "fill_mask", "cell_of_cluster", "clustered_positions", "bboxes")
+
+    def _field(self, name: str) -> np.ndarray:
         if self._host is None:
+            self._host = {}
+        if name not in self._host:
             ns, nc, n = self.n_slots, self.n_clusters, self.n
-            perm = np.empty(ns, dtype=np.int64)
-            inv = np.empty(n, dtype=np.int64)
-            fill = np.empty(ns, dtype=np.uint8)
-            coc = np.empty(nc, dtype=np.int64)
-            cpos = np.empty((ns, 3), dtype=np.float64)
-            bb = np.empty((nc, 2, 3), dtype=np.float64)
+            shapes = dict(perm=((ns,), np.int64), inverse_perm=((n,), np.int64), fill_mask=((ns,), np.uint8),
+                          cell_of_cluster=((nc,), np.int64), clustered_positions=((ns, 3), np.float64),
+                          bboxes=((nc, 2, 3), np.float64))
+            shape, dt = shapes[name]
+            buf = np.empty(shape, dtype=dt)
+            args = [None] * 6
+            args[self._FIELDS.index(name)] = buf
             torch.cuda.synchronize()
-            _lib.check(_lib.load().nbx_grid_download(
-                self._h, _lib.ptr(perm), _lib.ptr(inv), _lib.ptr(fill), _lib.ptr(coc),
-                _lib.ptr(cpos), _lib.ptr(bb), dev.stream()), "grid_download")
-            self._host = dict(perm=_ro(perm), inverse_perm=_ro(inv), fill_mask=_ro(fill.astype(bool)),
-                              cell_of_cluster=_ro(coc), clustered_positions=_ro(cpos), bboxes=_ro(bb))
+            _lib.check(_lib.load().nbx_grid_download(self._h, *(_lib.ptr(a) for a in args), dev.stream()),
+                       "grid_download")
+            if name == "fill_mask":
+                buf = buf.astype(bool)
+            self._host[name] = _ro(buf)
+        return self._host[name]
+
+    def _materialise(self) -> dict:
+        for name in self._FIELDS:
+            self._field(name)
         return self._host
 
-    perm = property(lambda self: self._materialise()["perm"])
-    inverse_perm = property(lambda self: self._materialise()["inverse_perm"])
-    fill_mask = property(lambda self: self._materialise()["fill_mask"])
-    cell_of_cluster = property(lambda self: self._materialise()["cell_of_cluster"])
-    clustered_positions = property(lambda self: self._materialise()["clustered_positions"])
-    bboxes = property(lambda self: self._materialise()["bboxes"])
+    perm = property(lambda self: self._field("perm"))
+    inverse_perm = property(lambda self: self._field("inverse_perm"))
+    fill_mask = property(lambda self: self._field("fill_mask"))
+    cell_of_cluster = property(lambda self: self._field("cell_of_cluster"))
+    clustered_positions = property(lambda self: self._field("clustered_positions"))
+    bboxes = property(lambda self: self._field("bboxes"))
 
     def cluster_centers(self) -> np.ndarray:
         """Bounding-box midpoints (gridder.py:64-66)."""
@@ -131,7 +143,11 @@ def build_cluster_grid(system: ParticleSystem, m: int, target_occupancy: float |
         raise ParameterError(f"target occupancy must be positive, got {target_occupancy}")
     n = system.n
     cells = grid_cells(n, m, target_occupancy)
-    pos = dev.to_device(system.positions if positions is None else positions, torch.float64, (n, 3))
+    src = system.positions if positions is None else positions
+    if dev.is_device_tensor(src):
+        pos = dev.to_device(src, torch.float64, (n, 3))
+    else:  # host arrays through the pinned staging of the drop-in API
+        pos = dev.stage_in(np.asarray(src, dtype=np.float64).reshape(n, 3), torch.float64, "grid_positions")
     box = _lib.box3(system.box.lengths)
     h = ctypes.c_void_p()
     _lib.check(_lib.load().nbx_grid_build(_lib.ptr(pos), n, _lib.ptr(box), m, cells, dev.stream(),

@@ -244,12 +244,17 @@ def compute_nonbonded_original(plist: ClusterPairList, grid: ClusterGrid, positi
     if len(pos_shape) != 2 or pos_shape[1] != 3:
         raise ParameterError(f"positions must have shape ({grid.n}, 3), got {pos_shape}")
     _check_shapes(plist, grid, layout, pos_shape[0])
-    pos_t = dev.to_device(positions, torch.float64)
-    f, e, bad = compute_nonbonded_device(plist, grid, pos_t, dev.to_device(charges, torch.float64),
-                                         dev.to_device(lj_types, torch.int64), params, box)
-    f_h, e_h, bad_h = f.cpu().numpy(), e.cpu().numpy(), bad.cpu().numpy()
+    # host arrays move through pinned staging (read-only charges / types are
+    # recognised and uploaded once); results come back in one synchronisation
+    pos_t = dev.stage_in(positions, torch.float64, "positions")
+    f, e, bad = compute_nonbonded_device(plist, grid, pos_t, dev.stage_in(charges, torch.float64, "charges"),
+                                         dev.stage_in(lj_types, torch.int64, "lj_types"), params, box)
+    eb = torch.cat([e, bad.to(torch.float64)])
+    eb_h = dev.stage_out(eb, "energies")
+    f_h = dev.stage_out(f, "forces")  # a fresh array (ForcesEnergies freezes it in place)
+    bad_h = eb_h[2:].astype(np.int64)
     _raise_if_singular(plist, grid, pos_t, bad_h, params, box)
-    return ForcesEnergies(forces=f_h, e_lj=float(e_h[0]), e_coulomb=float(e_h[1]))
+    return ForcesEnergies(forces=f_h, e_lj=float(eb_h[0]), e_coulomb=float(eb_h[1]))
 
 
 def flop_count(plist: ClusterPairList, grid: ClusterGrid, layout: KernelLayout, box: SimBox,

@@ -269,7 +269,7 @@ def _positions_ptr(plist: ClusterPairList, positions):
     g = plist.grid
     if isinstance(positions, DeviceArray):
         return positions.ptr, positions
-    if g._host is not None and positions is g._host["clustered_positions"]:
+    if g._host is not None and positions is g._host.get("clustered_positions"):
         return g.clustered_positions_device_ptr(), None
     if dev.is_device_tensor(positions):
         t = positions.to(torch.float64).contiguous()
