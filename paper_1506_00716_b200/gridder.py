@@ -31,6 +31,14 @@ class DeviceArray:
         self.owner = owner
 
 
+class _CudaView:
+    """__cuda_array_interface__ over a library-owned FP64 device buffer."""
+
+    def __init__(self, ptr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 def _ro(a: np.ndarray) -> np.ndarray:
     a.setflags(write=False)
     return a
@@ -95,6 +103,14 @@ class ClusterGrid:
                           cell_of_cluster=((nc,), np.int64), clustered_positions=((ns, 3), np.float64),
                           bboxes=((nc, 2, 3), np.float64))
             shape, dt = shapes[name]
+            if name == "clustered_positions":
+                # the largest field, read back by every drop-in rebuild: one
+                # D2H into pinned staging (a pageable cudaMemcpy runs at a
+                # fraction of the link), then one host copy
+                cpos = torch.as_tensor(_CudaView(self.clustered_positions_device_ptr().value, shape),
+                                       device=dev.require_cuda())
+                self._host[name] = _ro(dev.stage_out(cpos, "grid_clustered_positions"))
+                return self._host[name]
             buf = np.empty(shape, dtype=dt)
             args = [None] * 6
             args[self._FIELDS.index(name)] = buf
