@@ -42,22 +42,32 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
         df.forces(energy=False)
     torch.cuda.synchronize()
 dist.barrier()
+out = Path("gpurun_out")
+out.mkdir(exist_ok=True)
+prof.export_chrome_trace(str(out / f"dd_step_trace_r{rank}.json"))
+ev = json.load(open(out / f"dd_step_trace_r{rank}.json"))["traceEvents"]
+kern = sorted((e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
+              if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"))
+span = kern[-1][1] - kern[0][0]
+busy, end = 0.0, kern[0][0]
+for t0, t1, _ in kern:
+    busy += max(0.0, t1 - max(t0, end))
+    end = max(end, t1)
+tot = defaultdict(lambda: [0, 0.0])
+ntake = 0
+for t0, t1, name in kern:
+    key = name.split("(")[0][:60]
+    if "k_p2p_take" in key:  # 1st take of a step: halo positions in; 2nd: halo forces back
+        key += " (positions)" if ntake % 2 == 0 else " (forces)"
+        ntake += 1
+    tot[key][0] += 1
+    tot[key][1] += t1 - t0
+lines = [f"N={world} rank {rank}: {K} force steps, span {span / K:.1f} us/step, busy {busy / K:.1f}, "
+         f"idle {(span - busy) / K:.1f}, home {df.dd.layout.n_home} local {df.dd.layout.n_local}"]
+for k, (c, d) in sorted(tot.items(), key=lambda x: -x[1][1]):
+    lines.append(f"   {c // K:3d}x {d / K:8.1f} us/step  {k}")
+allv = [None] * world
+dist.all_gather_object(allv, "\n".join(lines))
 if rank == 0:
-    out = Path("gpurun_out")
-    prof.export_chrome_trace(str(out / "dd_step_trace.json"))
-    ev = json.load(open(out / "dd_step_trace.json"))["traceEvents"]
-    kern = sorted((e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
-                  if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"))
-    span = kern[-1][1] - kern[0][0]
-    busy, end = 0.0, kern[0][0]
-    for t0, t1, _ in kern:
-        busy += max(0.0, t1 - max(t0, end))
-        end = max(end, t1)
-    tot = defaultdict(lambda: [0, 0.0])
-    for t0, t1, name in kern:
-        tot[name.split("(")[0][:60]][0] += 1
-        tot[name.split("(")[0][:60]][1] += t1 - t0
-    print(f"N={world} rank 0: {K} force steps, span {span / K:.1f} us/step, busy {busy / K:.1f}, idle {(span - busy) / K:.1f}")
-    for k, (c, d) in sorted(tot.items(), key=lambda x: -x[1][1]):
-        print(f"   {c // K:3d}x {d / K:8.1f} us/step  {k}")
+    print("\n".join(allv))
 dist.destroy_process_group()
