@@ -93,7 +93,11 @@ __device__ __forceinline__ void image_delta(const double* bi, const double* oi, 
 
 constexpr int SEARCH_WARPS = 4;
 constexpr int GMAX = 16;
-constexpr int STASH = 512;   // hits kept per group between the two passes (overflow: recompute)
+#ifndef NBX_STASH
+#define NBX_STASH 1024
+#endif
+constexpr int STASH = NBX_STASH;   // hits kept per group between the two passes (overflow: recompute;
+                                   // 512 overflowed on relaxed-water MD boxes: pass 1 49 -> 170 us at 96k)
 
 struct SearchOut {
   // fused prune (nbx_pairlist_build_pruned): positions the exact criterion uses

@@ -403,7 +403,7 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
         f = torch.empty_like(x)
         e = torch.zeros(2, dtype=torch.float64, device=d)
         bad = torch.empty(2, dtype=torch.int64, device=d)
-        d_max = 0.0
+        d_max = d_last = 0.0
         d_pin = torch.zeros(1, dtype=torch.float64).pin_memory()
         d_ev = torch.cuda.Event()
 
@@ -449,7 +449,15 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                 interval_due = state.step - state.plist.build_step >= policy.rebuild_interval
                 guard_due = False
                 speculative = False
-                if not interval_due:
+                # d_max grows about linearly between rebuilds: when this step's
+                # extrapolated value would fire the guard, a speculative pass
+                # would likely be thrown away -- read d_max first instead
+                likely = 2.0 * (2.0 * d_max - d_last) > buffer
+                d_last = d_max
+                if not interval_due and likely:
+                    d_max = max(d_max, float(max_displacement_device(ref, x, box).item()))
+                    guard_due = 2.0 * d_max > buffer
+                elif not interval_due:
                     # drift guard without stalling the GPU: d_max goes to
                     # pinned memory ahead of a speculative force pass on the
                     # current list; the host reads it while that pass runs and,
@@ -478,7 +486,7 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                             state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box,
                                                           r_inner=min(policy.r_inner, params.r_list))
                     ref.copy_(x)
-                    d_max = 0.0
+                    d_max = d_last = 0.0
                     state.n_rebuilds += 1
             if not speculative:
                 with timer.section("forces"):

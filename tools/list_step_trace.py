@@ -18,11 +18,16 @@ from paper_1506_00716_b200.systems import spc_water, tuned_occupancy  # noqa: E4
 ap = argparse.ArgumentParser()
 ap.add_argument("--atoms", type=int, default=96000)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--md", type=int, default=0, help="take positions after this many rigid-water run_md steps")
 a = ap.parse_args()
 s, table = spc_water(a.atoms)
 occ = tuned_occupancy(a.atoms, float(s.box.lengths[0]), 4)
 params = nbx.NonbondedParams(r_cut=1.0, r_list=1.1, lj_table=table, shift_potential=True, elec="ewald",
                              ewald_beta=nbx.ewald_beta(1.0))
+if a.md:
+    s, _ = spc_water(a.atoms, seed=2024, temperature=300.0)
+    s = nbx.run_md(s, params, nbx.KernelLayout(4, 4), 0.002, a.md, report_interval=a.md, target_occupancy=occ,
+                   constraints=nbx.RigidWater()).state.system
 dev = torch.device("cuda", 0)
 pos = torch.from_numpy(np.array(s.positions)).to(dev)
 q = torch.from_numpy(np.array(s.charges)).to(dev)
