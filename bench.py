@@ -423,9 +423,7 @@ def run_ours(args):
     st = {}
 
     def rebuild(k, pos, counts):
-        grid = nbx.build_cluster_grid(system, M, occ, positions=pos)
-        plist = nbx.prune_pair_list(nbx.build_pair_list(grid, box, R_LIST), grid.clustered_positions_device, box,
-                                    r_inner=args.rinner)
+        grid, plist = nbx.list_step(system, M, occ, box, R_LIST, positions=pos, r_inner=args.rinner)
         st.update(grid=grid, plist=plist, build=k, rebuilds=st.get("rebuilds", 0) + 1)
         ref_d.copy_(pos)
         if counts is not None:

@@ -166,6 +166,21 @@ int nbx_super_download(const nbx_list_t* list, int64_t* super_offsets, int64_t* 
  * group): a per-particle search of the partners' entries. */
 int nbx_list_exclude(nbx_list_t* list, const nbx_grid_t* grid, const int32_t* atom_mol, const int32_t* mol_first,
                      const int32_t* mol_atoms, void* stream, int64_t* n_removed);
+/* Extension (list step in one call, for device-resident drivers: run_md,
+ * the domain decomposition, bench): nbx_grid_build -> nbx_pairlist_build_ex
+ * (halo) -> nbx_list_exclude (when atom_mol != NULL) -> nbx_pairlist_prune_inner
+ * at the grid's build positions (flags & NBX_STEP_PRUNE) -> the grouped force
+ * layout and its j-cluster transpose (what the first nbx_force call would
+ * build).  The same lists as the separate calls, with no host work between
+ * the phases (their only host syncs are the grid's cluster count and the
+ * search's entry count).  Replaces the rebuild sequence of
+ * engine.py:294-334 (_rebuild: build_cluster_grid, build_pair_list,
+ * prune_pair_list).  On success *grid_out and *list_out are new handles. */
+#define NBX_STEP_PRUNE 1
+int nbx_list_step(const double* positions, int64_t n, const double box[3], int32_t m, int64_t cells, double r_list,
+                  double r_inner, const uint8_t* halo, const int32_t* atom_mol, const int32_t* mol_first,
+                  const int32_t* mol_atoms, int32_t flags, void* stream, nbx_grid_t** grid_out,
+                  nbx_list_t** list_out);
 /* Per-row diagnostics of pairlist.write_pairs_csv (pairlist.py:349-376):
  * gap_sq[r] = periodic bounding-box gap^2 of row r (gridder.py:165-185),
  * min_d2[r] = exact FP64 minimum admitted slot distance^2 at `positions`

@@ -1662,6 +1662,37 @@ struct ForceCall {
   Box bx{};
 };
 
+// The grouped force layout (work order, member-pattern entry order) and the
+// j-cluster transpose k_reduce reads, built once per list -- by its first
+// force call, or ahead of it by nbx_list_step.
+cudaError_t force_prepare(List* l, cudaStream_t s) {
+  ForceWork& wk = l->work;
+  const int m = l->m;
+  cudaError_t e;
+  if (!l->ordered) {
+    if ((e = finalize_force_layout(l, s))) return e;
+    wk.t_ready = false;
+  }
+  if (wk.t_ready) return cudaSuccess;
+  // with an inner list (k_force_h only): key 2 j + (no inner member), so
+  // that k_reduce can stop before the entries k_force_h skipped
+  wk.t_split = l->ent_fmask.p && (m == 4 || m == 8) && !use_legacy_force() && l->n_entries > 0;
+  if (wk.t_split) {
+    DBuf<int32_t> tkeys;
+    if ((e = tkeys.alloc(l->n_entries, s))) return e;
+    count_launch();
+    k_split_keys<<<nb(l->n_entries, 256), 256, 0, s>>>(l->ent_j.p, l->ent_fmask.p, l->n_entries, l->mask_words(),
+                                                        tkeys.p);
+    e = build_transpose(tkeys.p, l->n_entries, 2 * l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos);
+    tkeys.release(s);
+    if (e) return e;
+  } else if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos))) {
+    return e;
+  }
+  wk.t_ready = true;
+  return cudaSuccess;
+}
+
 static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
                        const double* charges, const int64_t* lj_type, const nbx_params_t* p, const double box[3],
                        const int32_t* i_sel, int64_t n_sel, int32_t flags, double* f_out, void* stream) {
@@ -1725,29 +1756,7 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
     if ((e = wk.lj.alloc((int64_t)p->n_types * p->n_types, s))) goto cuda_fail;
     wk.lj_key.clear();
   }
-  if (!canonical && !l->ordered) {
-    if ((e = finalize_force_layout(l, s))) goto cuda_fail;
-    wk.t_ready = false;
-  }
-  if (!canonical && !wk.t_ready) {
-    // with an inner list (k_force_h only): key 2 j + (no inner member), so
-    // that k_reduce can stop before the entries k_force_h skipped
-    wk.t_split = l->ent_fmask.p && (m == 4 || m == 8) && !use_legacy_force() && l->n_entries > 0;
-    if (wk.t_split) {
-      DBuf<int32_t> tkeys;
-      if ((e = tkeys.alloc(l->n_entries, s))) goto cuda_fail;
-      count_launch();
-      k_split_keys<<<nb(l->n_entries, 256), 256, 0, s>>>(l->ent_j.p, l->ent_fmask.p, l->n_entries,
-                                                          l->mask_words(), tkeys.p);
-      e = build_transpose(tkeys.p, l->n_entries, 2 * l->n_clusters, wk.t_first, wk.t_items, s, &wk.t_pos);
-      tkeys.release(s);
-      if (e) goto cuda_fail;
-    } else if ((e = build_transpose(l->ent_j.p, l->n_entries, l->n_clusters, wk.t_first, wk.t_items, s,
-                                    &wk.t_pos))) {
-      goto cuda_fail;
-    }
-    wk.t_ready = true;
-  }
+  if (!canonical && (e = force_prepare(l, s))) goto cuda_fail;
   if (canonical && (e = ensure_row_delta(l, s))) goto cuda_fail;
   if (canonical && !wk.tc_ready) {
     if ((e = build_transpose(l->j.p, l->n_rows, l->n_clusters, wk.tc_first, wk.tc_items, s))) goto cuda_fail;

@@ -183,6 +183,7 @@ void timing_record(cudaEvent_t a, cudaEvent_t b);
 
 struct List;
 cudaError_t finalize_force_layout(List* l, cudaStream_t s);
+cudaError_t force_prepare(List* l, cudaStream_t s);  // force layout + j transpose (force.cu)
 cudaError_t ensure_row_delta(List* l, cudaStream_t s);
 cudaError_t ensure_rows(List* l, cudaStream_t s);
 // rolling prune: inner masks of `l` at the force-frame coordinates xyzq

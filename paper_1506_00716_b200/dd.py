@@ -452,7 +452,7 @@ class DomainForces:
         """Re-decompose (optionally rebalancing the slabs from the ranks'
         measured force-pass times first: collective) and rebuild the local
         grid and list."""
-        from . import build_cluster_grid, build_pair_list, prune_pair_list
+        from . import list_step
 
         self.dd.check_p2p()
         if balance and self.dd.N > 1 and getattr(self, "_ev", None) is not None:
@@ -483,10 +483,8 @@ class DomainForces:
         if occ is not None and self.dd.N > 1:
             w = float(np.diff(self.dd.boundaries).max())
             occ = local_occupancy(occ, n, self.system.n, self.system.box.lengths, w, self.dd.r_comm)
-        self.grid = build_cluster_grid(sys_local, self.m, occ, positions=self.local_pos)
-        built = build_pair_list(self.grid, self.system.box, self.params.r_list, halo=self.halo)
-        self.plist = prune_pair_list(built, self.grid.clustered_positions_device, self.system.box,
-                                     r_inner=self.r_inner)
+        self.grid, self.plist = list_step(sys_local, self.m, occ, self.system.box, self.params.r_list,
+                                          positions=self.local_pos, r_inner=self.r_inner, halo=self.halo)
         self.f = torch.empty((n, 3), dtype=torch.float64, device=dev)
         self.e = torch.zeros(2, dtype=torch.float64, device=dev)
         self.bad = torch.empty(2, dtype=torch.int64, device=dev)

@@ -27,7 +27,7 @@ from .gridder import ClusterGrid, build_cluster_grid
 from .kernels import KernelLayout, compute_nonbonded_original
 from .model import (BOLTZMANN_KJ_MOL_K, ForcesEnergies, NonbondedParams, ParameterError, ParticleSystem,
                     SimBox, wrap_position)
-from .pairlist import ClusterPairList, Molecules, build_pair_list, prune_pair_list
+from .pairlist import ClusterPairList, Molecules, build_pair_list, list_step, prune_pair_list
 
 
 # ---------------------------------------------------------------- timing (host bookkeeping)
@@ -422,11 +422,12 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
         dof = constraints.dof(system.n)
 
     def record():
-        bad_h = bad.cpu().numpy()
+        # one device->host read: energies, kinetic energy, singular-pair key
+        vals = torch.cat([e, torch.einsum("k,kd,kd->", m, v, v).reshape(1), bad.to(torch.float64)]).cpu().numpy()
+        bad_h = vals[3:5].astype(np.int64)
         _raise_if_singular(state.plist, state.grid, x, bad_h, params, box)
-        ke = 0.5 * float(torch.einsum("k,kd,kd->", m, v, v).item())
-        eh = e.cpu().numpy()
-        pe = float(eh[0] + eh[1])
+        ke = 0.5 * float(vals[2])
+        pe = float(vals[0] + vals[1])
         steps.append(state.step)
         e_kin.append(ke)
         e_pot.append(pe)
@@ -476,15 +477,14 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                     if guard_due:
                         state.n_drift_rebuilds += 1
                     with timer.section("rebuild"):
-                        state.grid = build_cluster_grid(_DeviceSystem(system, x), state.grid.m,
-                                                        state.target_occupancy, positions=x)
-                        state.plist = build_pair_list(state.grid, box, params.r_list,
-                                                      supercluster_size=state.plist.supercluster_size,
-                                                      n_lane=state.plist.n_lane, build_step=state.step,
-                                                      molecules=mol)
-                        if policy.prune_on_build and policy.rebuild_interval > 1:
-                            state.plist = prune_pair_list(state.plist, state.grid.clustered_positions_device, box,
-                                                          r_inner=min(policy.r_inner, params.r_list))
+                        # grid + search (+ exclusions) + prune + force layout in one
+                        # native call: no interpreter time between the phases
+                        state.grid, state.plist = list_step(
+                            _DeviceSystem(system, x), state.grid.m, state.target_occupancy, box, params.r_list,
+                            positions=x, r_inner=min(policy.r_inner, params.r_list),
+                            prune=policy.prune_on_build and policy.rebuild_interval > 1, molecules=mol,
+                            supercluster_size=state.plist.supercluster_size, n_lane=state.plist.n_lane,
+                            build_step=state.step)
                     ref.copy_(x)
                     d_max = d_last = 0.0
                     state.n_rebuilds += 1

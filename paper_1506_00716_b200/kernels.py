@@ -118,12 +118,19 @@ def pair_interaction(r2, type_i, type_j, q_i, q_j, params: NonbondedParams):
     return e_lj + e_c, f_over_r
 
 
+_last_params: list = []  # [(params, struct, table)]: run_md / the bench call with one params object
+
+
 def _params_struct(params: NonbondedParams):
+    if _last_params and _last_params[0][0] is params:
+        return _last_params[0][1], _last_params[0][2]
     table = np.ascontiguousarray(params.lj_table, dtype=np.float64)
     p = _lib.NbxParams(
         n_types=params.n_types, lj_table=table.ctypes.data, coulomb_scale=params.coulomb_scale,
         r_cut=params.r_cut, shift_potential=int(bool(params.shift_potential)),
         elec=_lib.ELEC[params.elec], k_rf=params.k_rf, c_rf=params.c_rf, ewald_beta=params.ewald_beta)
+    if getattr(params, "__dataclass_params__", None) is not None and params.__dataclass_params__.frozen:
+        _last_params[:] = [(params, p, table)]
     return p, table
 
 

@@ -226,6 +226,53 @@ def exclude_molecules(plist: ClusterPairList, molecules, count: bool = False):
     return int(out.value) if count else None
 
 
+def list_step(system, m: int, target_occupancy, box: SimBox, r_list: float, *, positions=None,
+              r_inner: float = 0.0, prune: bool = True, halo=None, molecules=None, supercluster_size: int = 1,
+              n_lane: int = 1, build_step: int = 0) -> tuple[ClusterGrid, ClusterPairList]:
+    """The rebuild of a device-resident driver (engine.py:294-334 _rebuild)
+    in one native call (nbx_list_step): ``build_cluster_grid`` ->
+    ``build_pair_list`` (``halo``, ``molecules``) -> ``prune_pair_list`` at
+    the grid's build positions (``prune``, ``r_inner``) -> the force layout
+    the first force call would build.  Same grid and list as the separate
+    calls; the GPU does not wait on the interpreter between the phases.
+    ``positions``: CUDA tensor (n, 3), default system.positions."""
+    from .gridder import grid_cells
+
+    if m not in (1, 2, 4, 8):
+        raise ParameterError(f"cluster size m must be one of (1, 2, 4, 8), got {m}")
+    if target_occupancy is None:
+        target_occupancy = 2.0 * m
+    if target_occupancy <= 0:
+        raise ParameterError(f"target occupancy must be positive, got {target_occupancy}")
+    if r_list <= 0.0:
+        raise ParameterError(f"r_list must be positive, got {r_list}")
+    if np.any(box.lengths < 2.0 * r_list):
+        raise ParameterError(f"every box edge must be >= 2*r_list={2.0 * r_list} "
+                             f"for the single-image convention, got {box.lengths}")
+    if r_inner and not (0.0 < r_inner <= r_list):
+        raise ParameterError(f"r_inner must be 0 (off) or in (0, r_list={r_list}], got {r_inner}")
+    if supercluster_size not in VALID_SUPERCLUSTER_SIZES:
+        raise ParameterError(f"supercluster_size must be one of {VALID_SUPERCLUSTER_SIZES}, "
+                             f"got {supercluster_size}")
+    n = system.n
+    src = system.positions if positions is None else positions
+    pos = dev.to_device(src, torch.float64, (n, 3))
+    mol = None
+    if molecules is not None:
+        mol = molecules if isinstance(molecules, Molecules) else Molecules(molecules)
+        if mol.n != n:
+            raise ParameterError(f"molecules describe {mol.n} particles, the grid has {n}")
+    L = _lib.box3(box.lengths)
+    hg, hl = ctypes.c_void_p(), ctypes.c_void_p()
+    _lib.check(_lib.load().nbx_list_step(
+        _lib.ptr(pos), n, _lib.ptr(L), m, grid_cells(n, m, target_occupancy), float(r_list), float(r_inner or 0.0),
+        _lib.ptr(halo), _lib.ptr(mol.atom_mol) if mol else None, _lib.ptr(mol.mol_first) if mol else None,
+        _lib.ptr(mol.mol_atoms) if mol else None, 1 if prune else 0, dev.stream(), ctypes.byref(hg),
+        ctypes.byref(hl)), "list_step")
+    grid = ClusterGrid(hg, box.lengths)
+    return grid, ClusterPairList(hl, grid, r_list, n_lane, build_step, supercluster_size)
+
+
 def build_pruned_pair_list(grid: ClusterGrid, box: SimBox, r_list: float, positions=None, *,
                            supercluster_size: int = 1, n_lane: int = 1, build_step: int = 0,
                            halo=None, molecules=None) -> ClusterPairList:
