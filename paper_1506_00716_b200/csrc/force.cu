@@ -1587,14 +1587,18 @@ __global__ void k_iota(int32_t* v, int64_t n) {
   if (i < n) v[i] = (int32_t)i;
 }
 
+// bucket starts of the sorted keys and (optional) the inverse permutation
+// pos[items[i]] = i, in one pass
 __global__ void k_first_sorted(const int32_t* __restrict__ keys, int64_t n, int64_t n_keys,
-                               int32_t* __restrict__ first) {
+                               int32_t* __restrict__ first, const int32_t* __restrict__ items,
+                               int32_t* __restrict__ pos) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   // keys >= n_keys are unused storage slots (sorted last)
   const int32_t prev = i == 0 ? -1 : min(keys[i - 1], (int32_t)n_keys);
   const int32_t cur = i == n ? (int32_t)n_keys : min(keys[i], (int32_t)n_keys);
   for (int32_t c = prev + 1; c <= cur; ++c) first[c] = (int32_t)i;
+  if (pos && i < n) pos[items[i]] = (int32_t)i;
 }
 
 // split-transpose keys: 2 j + 1 for entries without an inner member (unused
@@ -1606,11 +1610,6 @@ __global__ void k_split_keys(const int32_t* __restrict__ ej, const uint64_t* __r
   uint64_t any = fmask[i * W];
   if (W == 2) any |= fmask[i * W + 1];
   keys[i] = 2 * ej[i] + (any ? 0 : 1);
-}
-
-__global__ void k_inverse(const int32_t* __restrict__ items, int64_t n, int32_t* __restrict__ pos) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) pos[items[i]] = (int32_t)i;
 }
 
 static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clusters, DBuf<int32_t>& first,
@@ -1626,11 +1625,9 @@ static cudaError_t build_transpose(const int32_t* keys, int64_t n, int64_t n_clu
     count_launch(), k_iota<<<nb(n, 256), 256, 0, s>>>(vals.p, n);
     if ((e = sort_pairs_i32(keys, skeys.p, vals.p, items.p, n, end_bit, s))) return e;
   }
-  count_launch(), k_first_sorted<<<nb(n + 1, 256), 256, 0, s>>>(skeys.p, n, n_clusters, first.p);
-  if (pos) {
-    if ((e = pos->alloc(n, s))) return e;
-    if (n > 0) count_launch(), k_inverse<<<nb(n, 256), 256, 0, s>>>(items.p, n, pos->p);
-  }
+  if (pos && (e = pos->alloc(n, s))) return e;
+  count_launch(), k_first_sorted<<<nb(n + 1, 256), 256, 0, s>>>(skeys.p, n, n_clusters, first.p, items.p,
+                                                               pos ? pos->p : nullptr);
   vals.release(s);
   skeys.release(s);
   return cudaGetLastError();

@@ -1132,13 +1132,15 @@ __global__ void k_group_keys(const int32_t* __restrict__ ent_off, const int32_t*
   const int32_t e_end = fend ? fend[g] : ent_off[g + 1];
   const int64_t cost = (int64_t)(e_end - ent_off[g]) * (2 + 5 * (nmem ? nmem[g] : 1)) +
                        (fend ? (ent_off[g + 1] - e_end) / 4 : 0);
-  keys[g] = 0x3fffffff - (int32_t)min(cost, (int64_t)0x3ffffffe);  // ascending key = descending cost
+  // ascending key = descending cost, 16 bits (cost / 4, saturated): two radix
+  // passes instead of four for a 30-bit key
+  keys[g] = 0xffff - (int32_t)min(cost >> 2, (int64_t)0xffff);
   vals[g] = (int32_t)g;
 }
 
 // force-kernel work order: groups by descending estimated cost (LPT)
 // domain lists (halo bits): a group is BOUNDARY when one of its clusters or
-// one of its entries' j-clusters holds a halo particle; bit 30 of its work
+// one of its entries' j-clusters holds a halo particle; bit 16 of its work
 // key, so interior groups -- which read no halo coordinates -- come first
 // and the halo exchange can overlap them (dd.cu nbx_dd_force).  One warp per
 // group; counts the interior groups.
@@ -1153,7 +1155,7 @@ __global__ void k_group_boundary(const int32_t* __restrict__ grp_first, const in
   for (int32_t e = ent_off[g] + lane; e < ent_off[g + 1]; e += 32) b = b || halo_cl[ent_j[e]] != 0;
   const bool boundary = __any_sync(0xffffffffu, b);
   if (lane == 0) {
-    if (boundary) keys[g] |= 1 << 30;
+    if (boundary) keys[g] |= 1 << 16;
     else atomicAdd(n_interior, 1u);
   }
 }
@@ -1177,7 +1179,7 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
     k_group_boundary<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups,
                                                          l->ent_offsets.p, l->ent_j.p, l->halo_cl.p, keys.p, nint.p);
   }
-  e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, split ? 31 : 30, s);
+  e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, split ? 17 : 16, s);
   if (!e && split) {
     unsigned int h = 0;
     if (!(e = cudaMemcpyAsync(&h, nint.p, 4, cudaMemcpyDeviceToHost, s)) && !(e = cudaStreamSynchronize(s)))
