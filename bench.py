@@ -74,6 +74,7 @@ def parse():
                          "for static; 0 = off)")
     ap.add_argument("--positions", default="moving", choices=["moving", "static"])
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
+    ap.add_argument("--m", type=int, default=4, choices=[4, 8], help="cluster size (4x4 or 8x8 cluster pairs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-md", action="store_true", help="skip the rigid-water run_md ns/day measurement")
     ap.add_argument("--md-steps", type=int, default=200)
@@ -555,8 +556,8 @@ def run_ours(args):
 
     # ---- e2e with the device API and pinned host buffers (CUDA events)
     pin_pos = [torch.from_numpy(p).pin_memory() for p in host_pos]
-    q_h = torch.from_numpy(charges).pin_memory()
-    t_h = torch.from_numpy(types).pin_memory()
+    q_h = torch.from_numpy(np.array(charges)).pin_memory()  # (the drop-in call froze them in place)
+    t_h = torch.from_numpy(np.array(types)).pin_memory()
     f_h = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     e_h = torch.empty(2, dtype=torch.float64).pin_memory()
     q_s, t_s = torch.empty_like(q_d), torch.empty_like(t_d)
@@ -827,10 +828,11 @@ def run_dd(args, world, rank, local):
 
 
 def main():
-    global R_LIST
+    global R_LIST, M
     faulthandler.enable()
     args = parse()
     R_LIST = args.rlist
+    M = args.m
     if args.rinner is None:
         args.rinner = 0.0 if args.positions == "moving" else min(R_CUT + 0.02, R_LIST)
     if args.impl == "reference":
