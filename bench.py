@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--positions", default="moving", choices=["moving", "static"])
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
     ap.add_argument("--m", type=int, default=4, choices=[4, 8], help="cluster size (4x4 or 8x8 cluster pairs)")
+    ap.add_argument("--slabs", default="count", choices=["count", "equal"],
+                    help="N > 1: initial slab boundaries (equal particle counts, or equal widths)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-md", action="store_true", help="skip the rigid-water run_md ns/day measurement")
     ap.add_argument("--md-steps", type=int, default=200)
@@ -686,6 +688,8 @@ def run_dd(args, world, rank, local):
     traj = Trajectory(system, static=args.positions == "static")
     traj.to_device(dev, sorted(set(range(n_setup)) | set(range(S0 - W, S0 + args.steps))))
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
+    if args.slabs == "count":  # equal particle counts per slab at step 0 (same on every rank)
+        dd.balance_counts(traj.host(0)[:, 0])
     dd.enable_native()
     p2p = dd.enable_p2p(system.n)  # per-step halo exchanges as NVLink peer stores (NBX_DD_P2P=0: NCCL)
     df = DomainForces(dd, system, params, M, occ, r_inner=args.rinner)
@@ -805,7 +809,7 @@ def run_dd(args, world, rank, local):
             "data": "synthetic (seeded SPC-geometry water, BASELINE.md recipe; moving-trajectory stand-in)",
             "config": config(args, occ, {"parallelism": f"slab DD x{world} (half-shell halo, r_comm=r_list, "
                                                          f"{'NVLink peer stores' if p2p else 'NCCL send/recv'}, "
-                                                         f"{'slabs rebalanced by force time at every rebuild' if args.balance else 'equal slabs'})",
+                                                         f"{'slabs rebalanced by force time at every rebuild' if args.balance else ('count-balanced slabs' if args.slabs == 'count' else 'equal slabs')})",
                                          "slab_boundaries_nm": [round(float(x), 4) for x in dd.boundaries]}),
             "ns_per_day": args.steps / (t_ms * 1e-3) * DT_PS * 86.4,
             "ns_per_day_note": "steps/s of the timed hot-path loop x 2 fs (no integrator)",

@@ -220,6 +220,14 @@ class SlabDecomposition:
         cum = np.concatenate([[0.0], np.cumsum(t)])
         quant = np.interp(cum[-1] * np.arange(self.N + 1) / self.N, cum, b)
         new = alpha * quant + (1.0 - alpha) * b
+        self.boundaries = self._clamped(new)
+        return self.boundaries
+
+    def _clamped(self, new) -> np.ndarray:
+        """Boundaries ``new`` with every slab width in [r_comm, L - 2 r_comm]
+        (excess / deficit redistributed over the free slabs)."""
+        b = self.boundaries
+        new = np.asarray(new, dtype=np.float64).copy()
         new[0], new[-1] = b[0], b[-1]
         Lx = float(self.L[0])
         w_max = Lx - 2.0 * self.r_comm - 1e-9 * Lx
@@ -234,8 +242,23 @@ class SlabDecomposition:
                 w[free] += (Lx - w.sum()) * w[free] / w[free].sum()
         new = np.concatenate([[b[0]], b[0] + np.cumsum(w)])
         new[-1] = b[-1]
-        self.boundaries = new
         return new
+
+    def balance_counts(self, x) -> np.ndarray:
+        """Boundaries with equal particle counts per slab for the x
+        coordinates ``x`` (all particles; identical on every rank): the
+        count quantiles of x, widths clamped as in ``rebalance``.  A one-time set-up for boxes whose density is not uniform
+        along x (the generated water boxes fill their last lattice layers
+        partially), with no per-rebuild cost."""
+        if self.N == 1:
+            return self.boundaries
+        xs = np.sort(_wrap_np(np.asarray(x, dtype=np.float64).reshape(-1), self.L[0]))
+        n = xs.shape[0]
+        k = (np.arange(1, self.N) * n) // self.N
+        new = self.boundaries.copy()
+        new[1:-1] = 0.5 * (xs[np.maximum(k - 1, 0)] + xs[np.minimum(k, n - 1)])
+        self.boundaries = self._clamped(new)
+        return self.boundaries
 
     # ---------------------------------------------------------------- geometry
     def owner(self, x) -> np.ndarray:

@@ -199,3 +199,22 @@ def test_rebalanced_decomposition_equals_single_domain():
     f_ref = search.scatter_to_original(og, fc)
     assert np.abs(f_dd - f_ref).max() <= 1e-9 * np.abs(f_ref).max()
     assert abs(e_dd[0] - elj) <= 1e-9 * abs(elj) and abs(e_dd[1] - ec) <= 1e-9 * abs(ec)
+
+
+def test_balance_counts_equal_particles_per_slab():
+    from paper_1506_00716_b200.dd import SlabDecomposition
+
+    rng = np.random.default_rng(5)
+    L = np.array([12.0, 5.0, 5.0])
+    # density falls off along x (a partially filled last layer)
+    x = np.concatenate([rng.uniform(0.0, 9.0, 9000), rng.uniform(9.0, 12.0, 1000)])
+    for n_ranks in (2, 3, 4):
+        d = SlabDecomposition(L, n_ranks, 0, r_comm=1.1)
+        b = d.balance_counts(x)
+        counts = np.bincount(d.owner(x), minlength=n_ranks)
+        assert counts.max() - counts.min() <= 2, counts
+        assert b[0] == 0.0 and b[-1] == L[0] and np.all(np.diff(b) >= 1.1)
+    # the width clamps win over the counts (a slab may not be narrower than r_comm)
+    d = SlabDecomposition(L, 4, 0, r_comm=1.1)
+    b = d.balance_counts(np.full(100, 3.0))
+    assert np.all(np.diff(b) >= 1.1 - 1e-12) and np.all(np.diff(b) <= L[0] - 2.2 + 1e-9)
