@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--positions", default="moving", choices=["moving", "static"])
     ap.add_argument("--occupancy", default="tuned", choices=["tuned", "default"])
     ap.add_argument("--m", type=int, default=4, choices=[4, 8], help="cluster size (4x4 or 8x8 cluster pairs)")
+    ap.add_argument("--migrate", action="store_true",
+                    help="N > 1: list steps by neighbour-only particle migration (SlabDecomposition.migrate) "
+                         "instead of the all-gather of home positions")
     ap.add_argument("--slabs", default="count", choices=["count", "equal"],
                     help="N > 1: initial slab boundaries (equal particle counts, or equal widths)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -661,7 +664,8 @@ def run_dd(args, world, rank, local):
     """N > 1: strong scaling of the same box over N GPUs with the slab
     decomposition (paper_1506_00716_b200/dd.py): per step halo exchange
     (coordinates in, forces back: NVLink peer stores, NCCL fallback), local
-    search every nstlist steps after an all-gather of home positions,
+    search every nstlist steps after an all-gather of the home positions
+    (--migrate: neighbour-only particle migration instead),
     energies all-reduced on energy steps.  Positions follow the same moving
     trajectory as N = 1 (each rank takes its home rows of step k); lists are
     rebuilt every nstlist steps (the trajectory's 10-step displacement stays
@@ -704,8 +708,10 @@ def run_dd(args, world, rank, local):
         if home_pos is None:
             home_pos = traj.device(k).index_select(0, lay.home)
         if k % args.nstlist == 0:
-            glob = dd.allgather_home(lay.home, home_pos, system.n)
-            lay = df.rebuild(glob, balance=balance[0])  # slabs rebalanced from the ranks' force times
+            if args.migrate and not balance[0]:  # particles migrate to the neighbour slabs, no all-gather
+                lay = df.rebuild_local(lay.home, home_pos)
+            else:  # all-gather the home positions, re-assign (slabs rebalanced first with --balance)
+                lay = df.rebuild(dd.allgather_home(lay.home, home_pos, system.n), balance=balance[0])
             if counts is not None:
                 counts[k] = nbx.interaction_stats(df.plist, df.grid, df.grid.clustered_positions_device, box,
                                                   R_CUT).n_within_cutoff

@@ -268,6 +268,15 @@ int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
 int nbx_dd_assign(nbx_dd_t* dd, const double* positions, int64_t n, double box_x, const double* boundaries,
                   double r_comm, int64_t* home, int64_t* halo, int64_t* send_local, int64_t* counts_out,
                   void* stream);
+/* particle migration at a list step (dd.SlabDecomposition.migrate): for the
+ * rank's own particles (device n x 3) the new owner rank (same rule and
+ * arithmetic as nbx_dd_assign: np.mod wrap, searchsorted(bnd[1:-1], x,
+ * side="right")) and whether the particle lies within r_comm above its new
+ * owner's lower boundary (a face particle: halo of the rank below).  Device
+ * outputs owner (int32, n) and face (uint8, n); no sync.  Stateless: no
+ * nbx_dd_t needed. */
+int nbx_dd_classify(const double* positions, int64_t n, double box_x, const double* boundaries, int32_t nranks,
+                    double r_comm, int32_t* owner, uint8_t* face, void* stream);
 /* global positions from every rank's home rows: one ncclAllGather of
  * (id, x, y, z) records padded to cap >= max home count. */
 int nbx_dd_allgather_home(nbx_dd_t* dd, const int64_t* home_ids, const double* home_pos, int64_t n_home,

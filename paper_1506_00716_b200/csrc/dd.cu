@@ -401,6 +401,18 @@ __global__ void k_dd_flags(const double* __restrict__ pos, int64_t n, double Lx,
     if (s_cnt[r]) atomicAdd(&counts[r], s_cnt[r]);
 }
 
+// migration: new owner + face flag of this rank's particles (k_dd_flags' rule)
+__global__ void k_dd_classify(const double* __restrict__ pos, int64_t n, double Lx, const double* __restrict__ bnd,
+                              int nranks, double r_comm, int32_t* __restrict__ owner, uint8_t* __restrict__ face) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = wrap_coord(pos[3 * i], Lx);
+  int own = 0;
+  while (own < nranks - 1 && x >= bnd[own + 1]) ++own;
+  owner[i] = own;
+  face[i] = (x - bnd[own]) < r_comm;
+}
+
 __global__ void k_iota64(int64_t* v, int64_t n) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = i;
@@ -510,6 +522,33 @@ fail:
   fh.release(s); fl.release(s); fs.release(s); fsh.release(s); iota.release(s); cnt.release(s); bnd.release(s);
   set_error("nbx_dd_assign: %s", cudaGetErrorString(e));
   return NBX_ERR_CUDA;
+}
+
+extern "C" int nbx_dd_classify(const double* pos, int64_t n, double Lx, const double* boundaries, int32_t nranks,
+                               double r_comm, int32_t* owner, uint8_t* face, void* stream) {
+  if (n < 0 || (n > 0 && (!pos || !owner || !face)) || !boundaries || nranks < 1 || nranks > 64) {
+    set_error("nbx_dd_classify: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  if (n == 0) return NBX_OK;
+  cudaStream_t s = to_stream(stream);
+  DBuf<double> bnd;
+  cudaError_t e;
+  if ((e = bnd.alloc(nranks + 1, s)) ||
+      (e = cudaMemcpyAsync(bnd.p, boundaries, sizeof(double) * (nranks + 1), cudaMemcpyHostToDevice, s))) {
+    bnd.release(s);
+    set_error("nbx_dd_classify: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  count_launch();
+  k_dd_classify<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pos, n, Lx, bnd.p, nranks, r_comm, owner, face);
+  e = cudaGetLastError();
+  bnd.release(s);
+  if (e) {
+    set_error("nbx_dd_classify: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
 }
 
 // Global positions (n x 3, device) from every rank's home rows: one

@@ -324,6 +324,104 @@ class SlabDecomposition:
                    "dd_set_layout")
         return self.layout
 
+    # ---------------------------------------------------------------- migration
+    def _classify(self, pos: torch.Tensor):
+        """(owner rank, face flag) of particles ``pos`` (n, 3) by assign()'s
+        rule; face: within r_comm above the owner's lower boundary."""
+        n = pos.shape[0]
+        if pos.is_cuda:
+            from . import _device, _lib
+
+            own = torch.empty(n, dtype=torch.int32, device=pos.device)
+            face = torch.empty(n, dtype=torch.uint8, device=pos.device)
+            bnd = np.ascontiguousarray(self.boundaries, dtype=np.float64)
+            _lib.check(_lib.load().nbx_dd_classify(_lib.ptr(pos.contiguous()), n, float(self.L[0]), _lib.ptr(bnd),
+                                                   self.N, self.r_comm, _lib.ptr(own), _lib.ptr(face),
+                                                   _device.stream()), "dd_classify")
+            return own.long(), face.bool()
+        Lx = float(self.L[0])
+        x = torch.remainder(pos[:, 0], Lx)
+        x = torch.where(x >= Lx, x - Lx, x)
+        inner = torch.as_tensor(self.boundaries[1:-1], dtype=torch.float64, device=pos.device)
+        own = torch.bucketize(x, inner, right=True).clamp_(0, self.N - 1)
+        lo = torch.as_tensor(self.boundaries, dtype=torch.float64, device=pos.device)[own]
+        return own, (x - lo) < self.r_comm
+
+    def _exchange(self, sends: list, recv_from: list) -> list:
+        """Variable-length neighbour exchange: ``sends`` = [(peer, rows
+        (k, 4) float64)], ``recv_from`` = [peer] (same length, pairwise
+        matched across ranks).  Counts first, then the rows; returns the
+        received (k', 4) tensors in ``recv_from`` order."""
+        import torch.distributed as dist
+
+        dev = sends[0][1].device if sends else torch.device("cpu")
+        cnt_out = [torch.tensor([t.shape[0]], dtype=torch.int64, device=dev) for _, t in sends]
+        cnt_in = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in recv_from]
+        ops = [dist.P2POp(dist.irecv, c, peer, group=self.group) for c, peer in zip(cnt_in, recv_from)]
+        ops += [dist.P2POp(dist.isend, c, peer, group=self.group) for c, (peer, _) in zip(cnt_out, sends)]
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+        got = [torch.empty((int(c.item()), 4), dtype=torch.float64, device=dev) for c in cnt_in]
+        ops = [dist.P2POp(dist.irecv, g, peer, group=self.group) for g, peer in zip(got, recv_from) if g.numel()]
+        ops += [dist.P2POp(dist.isend, t.contiguous(), peer, group=self.group) for peer, t in sends if t.numel()]
+        if ops:
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+        return got
+
+    def migrate(self, home_ids: torch.Tensor, home_pos: torch.Tensor):
+        """List-step bookkeeping from this rank's own particles only (the
+        scalable replacement of allgather_home + assign): particles that left
+        the slab go to the neighbour that now owns them, the new home set is
+        sorted by global id, and the face particles travel down as the lower
+        neighbour's halo.  The same layout as ``assign`` on the gathered
+        positions, with two neighbour exchanges instead of an all-gather of
+        every position and an O(N_total) scan on every rank.  Requires that
+        no particle moved by more than one slab since the last list step
+        (raises otherwise -- use assign).  Returns (layout, local positions
+        (n_home + n_halo, 3): home rows then halo rows)."""
+        N, r = self.N, self.rank
+        ids = torch.as_tensor(home_ids, device=home_pos.device).reshape(-1).to(torch.int64)
+        pos = home_pos.reshape(-1, 3)
+        if N == 1:
+            self.assign(pos)  # one slab: everything is home
+            return self.layout, pos.contiguous()
+        own, _ = self._classify(pos)
+        up, down = (r + 1) % N, (r - 1) % N
+        stay = own == r
+        rec = torch.cat([ids.to(torch.float64)[:, None], pos], 1)  # ids < 2^53: exact in FP64
+        if N == 2:
+            leave = [(up, ~stay)]
+            recv_from = [up]
+        else:
+            leave = [(up, own == up), (down, own == down)]
+            recv_from = [down, up]
+        far = ~stay
+        for _, m in leave:
+            far &= ~m
+        if bool(far.any()):
+            raise RuntimeError("migrate: a particle moved by more than one slab since the last list step; "
+                               "use assign on the gathered positions")
+        got = self._exchange([(peer, rec[m]) for peer, m in leave], recv_from)
+        allrec = torch.cat([rec[stay]] + got, 0)
+        order = torch.argsort(allrec[:, 0])
+        allrec = allrec[order]
+        home = allrec[:, 0].to(torch.int64)
+        hpos = allrec[:, 1:].contiguous()
+        own2, face = self._classify(hpos)
+        send_local = torch.nonzero(face).flatten()
+        halo_rec = self._exchange([(down, allrec[send_local])], [up])[0]
+        halo = halo_rec[:, 0].to(torch.int64)
+        self.layout = DomainLayout(home=home, halo=halo, send=home[send_local], send_local=send_local)
+        self.home_counts = None  # per-rank counts are no longer known here (allgather_home recounts)
+        if self._native is not None:
+            from . import _device, _lib
+
+            _lib.check(_lib.load().nbx_dd_set_layout(self._native, _lib.ptr(send_local), int(send_local.numel()),
+                                                     int(home.numel()), int(halo.numel()), _device.stream()),
+                       "dd_set_layout")
+        return self.layout, torch.cat([hpos, halo_rec[:, 1:]], 0)
+
     # ---------------------------------------------------------------- exchanges
     def _p2p(self, send_t: torch.Tensor | None, send_to: int, recv_t: torch.Tensor | None, recv_from: int):
         """One grouped send + receive (ncclGroupStart/End under NCCL): both
@@ -475,8 +573,6 @@ class DomainForces:
         """Re-decompose (optionally rebalancing the slabs from the ranks'
         measured force-pass times first: collective) and rebuild the local
         grid and list."""
-        from . import list_step
-
         self.dd.check_p2p()
         if balance and self.dd.N > 1 and getattr(self, "_ev", None) is not None:
             import torch.distributed as dist
@@ -488,13 +584,25 @@ class DomainForces:
             dist.all_gather(allt, t, group=self.dd.group)
             self.dd.rebalance(torch.cat(allt).cpu().numpy())
         lay = self.dd.assign(positions_global)
-        dev = positions_global.device
+        return self._build_local(lay, positions_global.index_select(0, lay.local_ids).contiguous())
+
+    def rebuild_local(self, home_ids: torch.Tensor, home_pos: torch.Tensor) -> DomainLayout:
+        """List step from this rank's own particles (SlabDecomposition.migrate:
+        neighbour exchanges only, no global all-gather), same slabs."""
+        self.dd.check_p2p()
+        lay, local_pos = self.dd.migrate(home_ids, home_pos)
+        return self._build_local(lay, local_pos.contiguous())
+
+    def _build_local(self, lay: DomainLayout, local_pos: torch.Tensor) -> DomainLayout:
+        from . import list_step
+
+        dev = local_pos.device
         ids = lay.local_ids
         self.ids = ids
         if not hasattr(self, "q_all"):
             self.q_all = torch.as_tensor(np.array(self.system.charges), device=dev)
             self.t_all = torch.as_tensor(np.array(self.system.lj_type), device=dev)
-        self.local_pos = positions_global.index_select(0, ids).contiguous()
+        self.local_pos = local_pos
         self.q = self.q_all.index_select(0, ids)
         self.t = self.t_all.index_select(0, ids)
         halo = torch.zeros(lay.n_local, dtype=torch.uint8, device=dev)

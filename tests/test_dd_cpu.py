@@ -218,3 +218,58 @@ def test_balance_counts_equal_particles_per_slab():
     d = SlabDecomposition(L, 4, 0, r_comm=1.1)
     b = d.balance_counts(np.full(100, 3.0))
     assert np.all(np.diff(b) >= 1.1 - 1e-12) and np.all(np.diff(b) <= L[0] - 2.2 + 1e-9)
+
+
+def _migrate_worker(rank, world, port, out_q):
+    import datetime
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
+    try:
+        from paper_1506_00716_b200.dd import SlabDecomposition
+
+        rng = np.random.default_rng(11)
+        L = np.array([3.3 * world + 1.0, 4.0, 4.0])
+        n = 4000
+        x0 = rng.uniform(0.0, 1.0, (n, 3)) * L
+        dd = SlabDecomposition(L, world, rank, r_comm=1.1)
+        lay = dd.assign(torch.from_numpy(x0))
+        ok = True
+        for step in range(3):  # displacements up to 0.5 nm (< the slab width), wrapped or not
+            x1 = x0 + rng.uniform(-0.5, 0.5, (n, 3))
+            if step == 1:
+                x1 = np.mod(x1, L)
+            lay_m, local = dd.migrate(lay.home, torch.from_numpy(x1[lay.home.numpy()]))
+            ref = SlabDecomposition(L, world, rank, r_comm=1.1).assign(torch.from_numpy(x1))
+            ok &= all(torch.equal(getattr(lay_m, f), getattr(ref, f)) for f in ("home", "halo", "send", "send_local"))
+            ok &= bool(np.array_equal(local.numpy(), x1[ref.local_ids.numpy()]))
+            lay, x0 = lay_m, x1
+        # a particle two slabs away (possible from 4 slabs on) is refused
+        far = torch.from_numpy(x0[lay.home.numpy()])
+        if world >= 4 and far.shape[0]:
+            far[0, 0] += 2.0 * 3.3
+            try:
+                dd.migrate(lay.home, far)
+                ok = False
+            except RuntimeError:
+                pass
+        out_q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_migrate_equals_assign(world):
+    """Neighbour-only migration (the list step without the global all-gather)
+    gives every rank the layout and local positions assign() computes from
+    the gathered positions."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res

@@ -38,3 +38,9 @@ def test_dd_overlapped_p2p_matches_one_gpu():
 def test_dd_exchange_paths_bit_identical():
     out = _torchrun(2, "dd_p2p_check.py", "96000", port=29572)
     assert "bit-identical on every rank: True" in out and "timeouts: False" in out, out
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_dd_migration_matches_allgather_assign():
+    out = _torchrun(2, "dd_migrate_check.py", "96000", port=29573)
+    assert "MIGRATE PARITY OK" in out, out
