@@ -1,3 +1,4 @@
+"""NVML clock / throttle sampling check of bench.Clocks on the GPU box."""
 import sys, time
 sys.path.insert(0, "/root/repo")
 import faulthandler; faulthandler.enable()

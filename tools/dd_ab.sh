@@ -1,3 +1,4 @@
+# A/B of the 1.5M 4-GPU bench: equal vs count-balanced slabs vs the overlapped force pass (gpurun --gpus 4)
 for rep in 1 2; do
 for v in "--slabs equal" "--slabs count" "--slabs count OVERLAP"; do
   E=""; A="$v"

@@ -1,3 +1,4 @@
+# 2-GPU DD tests + two 1.5M 4-GPU bench lines + the per-rank force-step trace (gpurun --gpus 4)
 timeout 600 python -m pytest -q -x tests/test_gpu_dd.py 2>&1 | tail -2
 for rep in 1 2; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 2956$rep bench.py --gpus 4 --atoms 1500000 --steps 40 --warmup 5 > gpurun_out/ddab.json 2> gpurun_out/ddab.err

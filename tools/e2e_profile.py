@@ -1,3 +1,5 @@
+"""Drop-in (numpy) API cost breakdown at 96k: compute_nonbonded_original vs its staging, device force and
+read-back pieces; list rebuild pieces (ParticleSystem, grid, build, clustered_positions, prune)."""
 import sys, time; sys.path.insert(0, "/root/repo")
 import numpy as np, torch, cProfile, pstats
 import paper_1506_00716_b200 as nbx

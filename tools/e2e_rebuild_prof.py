@@ -1,3 +1,4 @@
+"""Drop-in list rebuild at 96k: per-phase wall time with a sync after each phase, staging costs, cProfile."""
 import sys, time; sys.path.insert(0, "/root/repo")
 import numpy as np, torch, cProfile, pstats
 import paper_1506_00716_b200 as nbx

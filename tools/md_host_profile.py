@@ -1,3 +1,4 @@
+"""cProfile of 400 rigid-water run_md steps at 96k (host time per call of the MD loop)."""
 import sys, cProfile, pstats; sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 import paper_1506_00716_b200 as nbx
