@@ -1270,7 +1270,10 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
   // partials, no per-item FP64 conversions -- and the lanes' sums are
   // combined in FP64 by a fixed shuffle tree: the order never changes, so
   // forces stay bit-reproducible
-  constexpr int U = 4;
+#ifndef NBX_REDUCE_U
+#define NBX_REDUCE_U 4
+#endif
+  constexpr int U = NBX_REDUCE_U;
   float sx = 0.f, sy = 0.f, sz = 0.f;
   for (int32_t t0 = tb + sidx; t0 < t1; t0 += S * U) {
     int32_t it[U];
