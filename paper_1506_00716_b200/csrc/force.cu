@@ -56,6 +56,9 @@ struct ForceArgs {
   float inner_dmax;           // inner masks valid while d_max (scalars[inner_slot]) <= this
   int inner_slot;             // 0: displacement since the build, 5: since the rolling prune
   const int32_t* ent_tpos;    // k_force_h: entry -> partial-force slot in j-cluster order (NULL: entry order)
+  int split;                  // k_force_h: work items per group (1, 2, 4, 8: parts of its entry range)
+  int64_t wbase;              // k_force_h: global index of this launch's first work item
+  int64_t ns;                 // slots (one i-partial plane per part)
   // per-slot inputs
   const float4* xyzq;         // cluster-local coordinates (relative to bbox low corner)
   const double* bbox;         // grid bboxes (origins of the local frames)
@@ -942,14 +945,21 @@ k_force_h(const ForceArgs A) {
     if (lane == 0) wi = (int64_t)atomicAdd(A.scalars + 4, 1u);
     wi = __shfl_sync(0xffffffffu, wi, 0);
     if (wi >= A.n_work) break;
-    const int32_t g = A.sel ? A.sel[wi] : (int32_t)wi;
+    // work item -> (group in work order, part of its entry range)
+    const int64_t wg = A.wbase + wi;
+    const int part = (int)(wg % A.split);
+    const int64_t gi = wg / A.split;
+    const int32_t g = A.sel ? A.sel[gi] : (int32_t)gi;
     const int32_t first = A.grp_first[g];
     const int nmem = A.grp_nmem[g];
     // inner list: entries past ent_fend have no member within r_inner; they
     // are not evaluated and k_reduce skips their (unwritten) partials (split
     // transpose: per j-cluster the entries with an inner member come first)
-    const int32_t e_beg = A.ent_off[g], e_all = A.ent_off[g + 1];
-    const int32_t e_end = use_inner ? A.ent_fend[g] : e_all;
+    const int32_t g_beg = A.ent_off[g];
+    const int32_t g_end = use_inner ? A.ent_fend[g] : A.ent_off[g + 1];
+    const int32_t g_cnt = g_end - g_beg;
+    const int32_t e_beg = g_beg + (int32_t)(((int64_t)g_cnt * part) / A.split);
+    const int32_t e_end = g_beg + (int32_t)(((int64_t)g_cnt * (part + 1)) / A.split);
     const int32_t e_last = e_end > e_beg ? e_end - 1 : e_beg;
 
     // chunk staging: entry fields of chunk c (lanes < CH), j-atoms of chunk
@@ -1181,7 +1191,7 @@ k_force_h(const ForceArgs A) {
     }
     __syncwarp();
     if (lane < nmem * M) {
-      A.part_i[(int64_t)first * M + lane] =
+      A.part_i[part * A.ns + (int64_t)first * M + lane] =
           make_float4(s_ws[w].red[0][3 * lane], s_ws[w].red[0][3 * lane + 1], s_ws[w].red[0][3 * lane + 2], 0.f);
     }
     if (ENERGY) {
@@ -1246,7 +1256,7 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
                          const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
                          int64_t n_clusters, int m, int flags, double* __restrict__ f_out,
                          unsigned int* __restrict__ flag, int split, float inner_dmax,
-                         const unsigned int* __restrict__ dref) {
+                         const unsigned int* __restrict__ dref, int parts, int64_t ns) {
   const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= n_clusters) return;
@@ -1311,10 +1321,12 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
   }
   if (sidx != 0) return;
   const int64_t s = c * m + b;
-  const float4 pi = part_i[s];
-  fx += pi.x;
-  fy += pi.y;
-  fz += pi.z;
+  for (int q = 0; q < parts; ++q) {  // i-partials of the group's parts, fixed order
+    const float4 pi = part_i[q * ns + s];
+    fx += pi.x;
+    fy += pi.y;
+    fz += pi.z;
+  }
   if (!isfinite(fx) || !isfinite(fy) || !isfinite(fz)) atomicOr(flag, 1u);
   int64_t o;
   if (flags & NBX_FORCE_CLUSTERED) {
@@ -1693,6 +1705,28 @@ cudaError_t force_prepare(List* l, cudaStream_t s) {
   return cudaSuccess;
 }
 
+// work items per group of k_force_h: the smallest power of two (<= 8) that
+// gives at least two work items per resident warp, while parts keep >= 32
+// entries on average; NBX_FORCE_SPLIT=1|2|4|8 overrides (A/B)
+static int force_parts(const List* l) {
+  if (l->n_groups <= 0) return 1;
+  if (const char* e = getenv("NBX_FORCE_SPLIT")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) return v;
+  }
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int64_t resident = (int64_t)n_sm * NBX_FORCEH_MINB * FW;
+  int p = 1;
+  while (p < 8 && l->n_groups * p < 2 * resident && l->n_entries >= (int64_t)64 * l->n_groups * p) p *= 2;
+  return p;
+}
+
 static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions,
                        const double* charges, const int64_t* lj_type, const nbx_params_t* p, const double box[3],
                        const int32_t* i_sel, int64_t n_sel, int32_t flags, double* f_out, void* stream) {
@@ -1735,7 +1769,12 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
     }
   }
   const int64_t n_items = canonical ? l->n_rows : l->n_entries;
-  const int64_t n_work = canonical ? (i_sel ? n_sel : l->n_clusters) : l->n_groups;
+  // k_force_h: groups split into `parts` work items (consecutive entry
+  // ranges) when there are too few groups to fill the GPU -- small boxes and
+  // domain-decomposed ranks -- each part with its own i-partial plane
+  const bool grouped_h = !canonical && (m == 4 || m == 8) && !use_legacy_force();
+  const int parts = grouped_h ? force_parts(l) : 1;
+  const int64_t n_work = canonical ? (i_sel ? n_sel : l->n_clusters) : l->n_groups * parts;
   C.n_work = n_work;
   Box bx;
   for (int d = 0; d < 3; ++d) {
@@ -1748,7 +1787,7 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
   // workspace (cached across calls on this list)
   if (wk.xyzq.n < ns) { if ((e = wk.xyzq.alloc(ns, s))) goto cuda_fail; }
   if (wk.type.n < ns) { if ((e = wk.type.alloc(ns, s))) goto cuda_fail; }
-  if (wk.part_i.n < ns) { if ((e = wk.part_i.alloc(ns, s))) goto cuda_fail; }
+  if (wk.part_i.n < parts * ns) { if ((e = wk.part_i.alloc(parts * ns, s))) goto cuda_fail; }
   if (wk.part_j.n < n_items * m) { if ((e = wk.part_j.alloc(n_items * m, s))) goto cuda_fail; }
   if (wk.e_grp.n < 2 * n_work) { if ((e = wk.e_grp.alloc(2 * n_work + 2, s))) goto cuda_fail; }
   if (wk.scalars.n < 8) { if ((e = wk.scalars.alloc(8, s))) goto cuda_fail; }
@@ -1790,6 +1829,9 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
     }
     ForceArgs& A = C.A;
     A.n_work = n_work;
+    A.split = parts;
+    A.wbase = 0;
+    A.ns = ns;
     A.sel = canonical ? i_sel : l->group_order.p;
     C.sel0 = A.sel;
     A.grp_first = canonical ? nullptr : l->group_first.p;
@@ -1892,8 +1934,13 @@ cuda_fail:
 static cudaError_t force_launch(ForceCall& C, int64_t w0, int64_t w1) {
   if (w1 <= w0) return cudaSuccess;
   ForceArgs A = C.A;
-  A.sel = C.sel0 ? C.sel0 + w0 : nullptr;
-  if (!C.sel0 && w0 != 0) return cudaErrorInvalidValue;  // identity order: one range only
+  if (C.sorted_j) {  // k_force_h: items index the work order through A.split
+    A.sel = C.sel0;
+    A.wbase = w0;
+  } else {
+    A.sel = C.sel0 ? C.sel0 + w0 : nullptr;
+    if (!C.sel0 && w0 != 0) return cudaErrorInvalidValue;  // identity order: one range only
+  }
   A.n_work = w1 - w0;
   A.e_grp = C.e_grp0 + 2 * w0;
   cudaError_t e = cudaMemsetAsync(A.scalars + 4, 0, sizeof(unsigned int), C.s);
@@ -1924,7 +1971,7 @@ static int force_finish(ForceCall& C, const double box[3], double* f_out, double
                                          C.grid->fill.p, l->n_clusters, C.m, C.flags, f_out, wk.scalars.p + 1,
                                          !C.canonical && wk.t_split,
                                          (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
-                                         wk.scalars.p + A.inner_slot);
+                                         wk.scalars.p + A.inner_slot, C.canonical ? 1 : A.split, C.ns);
   if (!(C.flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
     // nothing else to produce
   } else {
@@ -1951,7 +1998,7 @@ int force_split(const nbx_list_t* lc, const nbx_grid_t* grid, const double* posi
   ForceCall C;
   int st = force_setup(C, lc, grid, positions, charges, lj_type, p, box, nullptr, 0, flags, f_out, stream);
   if (st) return st;
-  const int64_t n_int = C.canonical ? -1 : C.l->n_interior;
+  const int64_t n_int = C.canonical ? -1 : (C.l->n_interior < 0 ? -1 : C.l->n_interior * C.A.split);
   cudaError_t e;
   if (n_int < 0) {  // no interior / boundary split: one range, the caller's hook first
     if ((st = between())) return st;
