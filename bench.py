@@ -43,6 +43,7 @@ from __future__ import annotations
 
 import argparse
 import faulthandler
+import gc
 import json
 import os
 import statistics
@@ -496,6 +497,8 @@ def run_ours(args):
         step(k, q_d, t_d, f_d)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.nbx_launch_count()
+    gc.collect()  # no interpreter GC pause inside the timed region (re-enabled below)
+    gc.disable()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     for i in range(args.steps):
@@ -505,6 +508,7 @@ def run_ours(args):
         ev[i][1].record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
+    gc.enable()
     launches = lib.nbx_launch_count() - launches0
     rebuilds_timed = st.get("rebuilds", 0)
     t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
@@ -742,6 +746,8 @@ def run_dd(args, world, rank, local):
     lib.nbx_timing_query(None, None)
     lib.nbx_timing_enable(1)
     launches0 = lib.nbx_launch_count()
+    gc.collect()  # no interpreter GC pause inside the timed region (re-enabled below)
+    gc.disable()
     dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
@@ -750,6 +756,7 @@ def run_dd(args, world, rank, local):
         step(S0 + i)
         ev[i][1].record()
     torch.cuda.synchronize()
+    gc.enable()
     launches = lib.nbx_launch_count() - launches0
     lib.nbx_timing_enable(0)
     fk_ms, fk_n = np.zeros(1), np.zeros(1, dtype=np.int64)
