@@ -80,6 +80,22 @@ def _probe(arr: np.ndarray):
     return flat[:16].copy(), flat[-16:].copy()
 
 
+# Large uploads go in pieces: the host copy of piece k+1 into pinned memory
+# overlaps the DMA of piece k (numpy copies run at ~18 GB/s, the link at ~45;
+# 96k positions: 0.29 -> 0.18 ms).  Read-backs stay one copy: piecewise
+# D2H measured no faster (the host copy into fresh memory dominates).
+_PIECE = 1 << 17  # elements (1 MB of FP64)
+
+
+def _h2d_pipelined(d: torch.Tensor, pin: torch.Tensor, src: np.ndarray) -> None:
+    n = src.size
+    pv = pin.numpy()
+    for a in range(0, n, _PIECE):
+        b = min(a + _PIECE, n)
+        np.copyto(pv[a:b], src[a:b])
+        d[a:b].copy_(pin[a:b], non_blocking=True)
+
+
 def stage_in(a, dtype: torch.dtype, name: str) -> torch.Tensor:
     """numpy (or tensor) -> CUDA tensor valid until the next stage_in under
     ``name`` on this stream (callers use it within one API call)."""
@@ -101,17 +117,17 @@ def stage_in(a, dtype: torch.dtype, name: str) -> torch.Tensor:
     src = np.ascontiguousarray(arr, dtype=npdt)
     n = src.size
     pin = _buffer(_pinned, name, n, dtype, pinned=True)
-    np.copyto(pin.numpy(), src.reshape(-1))
-    if immutable:  # own device copy, kept while the array is cached
-        d = torch.empty(n, dtype=dtype, device=require_cuda())
-        d.copy_(pin, non_blocking=True)
-        d = d.reshape(src.shape)
-        _ident.insert(0, (arr, _probe(arr), d))
-        del _ident[_IDENT_MAX:]
-        return d
-    d = _buffer(_devbuf, name, n, dtype, pinned=False)
-    d.copy_(pin, non_blocking=True)
-    return d.reshape(src.shape)
+    if not immutable:
+        d = _buffer(_devbuf, name, n, dtype, pinned=False)
+        _h2d_pipelined(d, pin, src.reshape(-1))
+        return d.reshape(src.shape)
+    # immutable: an own device copy, kept while the array is cached
+    d = torch.empty(n, dtype=dtype, device=require_cuda())
+    _h2d_pipelined(d, pin, src.reshape(-1))
+    d = d.reshape(src.shape)
+    _ident.insert(0, (arr, _probe(arr), d))
+    del _ident[_IDENT_MAX:]
+    return d
 
 
 def stage_out(t: torch.Tensor, name: str, copy: bool = True) -> np.ndarray:
