@@ -268,6 +268,14 @@ int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
 int nbx_dd_assign(nbx_dd_t* dd, const double* positions, int64_t n, double box_x, const double* boundaries,
                   double r_comm, int64_t* home, int64_t* halo, int64_t* send_local, int64_t* counts_out,
                   void* stream);
+/* nbx_dd_assign plus the rank's local inputs in [home; halo] order: local
+ * positions (n_local x 3), charges, types and halo flags (1 for halo rows)
+ * gathered from the global arrays into caller device buffers of capacity n
+ * (dd.DomainForces.rebuild: one call instead of assign + four gathers). */
+int nbx_dd_assign_local(nbx_dd_t* dd, const double* positions, const double* charges, const int64_t* lj_type,
+                        int64_t n, double box_x, const double* boundaries, double r_comm, int64_t* home,
+                        int64_t* halo, int64_t* send_local, double* local_positions, double* local_charges,
+                        int64_t* local_lj_type, uint8_t* local_halo, int64_t* counts_out, void* stream);
 /* particle migration at a list step (dd.SlabDecomposition.migrate): for the
  * rank's own particles (device n x 3) the new owner rank (same rule and
  * arithmetic as nbx_dd_assign: np.mod wrap, searchsorted(bnd[1:-1], x,

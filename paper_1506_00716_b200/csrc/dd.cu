@@ -551,6 +551,48 @@ extern "C" int nbx_dd_classify(const double* pos, int64_t n, double Lx, const do
   return NBX_OK;
 }
 
+__global__ void k_dd_gather_local(const double* __restrict__ pos, const double* __restrict__ q,
+                                  const int64_t* __restrict__ typ, const int64_t* __restrict__ home, int64_t nh,
+                                  const int64_t* __restrict__ halo, int64_t n_local, double* __restrict__ lpos,
+                                  double* __restrict__ lq, int64_t* __restrict__ lt, uint8_t* __restrict__ lhalo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  const int64_t id = i < nh ? home[i] : halo[i - nh];
+  lpos[3 * i] = pos[3 * id];
+  lpos[3 * i + 1] = pos[3 * id + 1];
+  lpos[3 * i + 2] = pos[3 * id + 2];
+  lq[i] = q[id];
+  lt[i] = typ[id];
+  lhalo[i] = i >= nh;
+}
+
+// nbx_dd_assign plus the rank's local arrays in [home; halo] order (the
+// inputs of its list step and force pass): positions, charges, types and the
+// halo flags, into caller buffers of capacity n.  One call, the syncs of
+// nbx_dd_assign only.
+extern "C" int nbx_dd_assign_local(nbx_dd_t* d, const double* pos, const double* charges, const int64_t* lj_type,
+                                   int64_t n, double Lx, const double* boundaries, double r_comm, int64_t* home,
+                                   int64_t* halo, int64_t* send_local, double* local_pos, double* local_q,
+                                   int64_t* local_t, uint8_t* local_halo, int64_t* counts_out, void* stream) {
+  if (n > 0 && (!charges || !lj_type || !local_pos || !local_q || !local_t || !local_halo)) {
+    set_error("nbx_dd_assign_local: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  int st = nbx_dd_assign(d, pos, n, Lx, boundaries, r_comm, home, halo, send_local, counts_out, stream);
+  if (st) return st;
+  const int64_t nh = counts_out[0], n_local = counts_out[0] + counts_out[1];
+  if (n_local > 0) {
+    count_launch();
+    k_dd_gather_local<<<(unsigned)((n_local + 255) / 256), 256, 0, to_stream(stream)>>>(
+        pos, charges, lj_type, home, nh, halo, n_local, local_pos, local_q, local_t, local_halo);
+    if (cudaError_t e = cudaGetLastError()) {
+      set_error("nbx_dd_assign_local: %s", cudaGetErrorString(e));
+      return NBX_ERR_CUDA;
+    }
+  }
+  return NBX_OK;
+}
+
 // Global positions (n x 3, device) from every rank's home rows: one
 // ncclAllGather of fixed-capacity (id, x, y, z) records; cap >= every rank's
 // home count (known to all ranks from the previous nbx_dd_assign).

@@ -301,6 +301,39 @@ class SlabDecomposition:
                        "dd_set_layout")
         return self.layout
 
+    def assign_local(self, pos: torch.Tensor, charges: torch.Tensor, lj_type: torch.Tensor):
+        """assign() plus the rank's local inputs in [home; halo] order, in one
+        native call (nbx_dd_assign_local): returns (layout, local positions,
+        charges, types, halo flags) -- the latter four views of buffers
+        reused by the next call."""
+        from . import _device, _lib
+
+        n = pos.shape[0]
+        dev = pos.device
+        if getattr(self, "_lbuf_n", -1) != n:
+            self._lbuf = dict(ids=torch.empty((3, max(n, 1)), dtype=torch.int64, device=dev),
+                              pos=torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev),
+                              q=torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+                              t=torch.empty(max(n, 1), dtype=torch.int64, device=dev),
+                              halo=torch.empty(max(n, 1), dtype=torch.uint8, device=dev))
+            self._lbuf_n = n
+        b = self._lbuf
+        counts = np.zeros(3 + self.N, dtype=np.int64)
+        bnd = np.ascontiguousarray(self.boundaries, dtype=np.float64)
+        _lib.check(_lib.load().nbx_dd_assign_local(
+            self._native, _lib.ptr(pos), _lib.ptr(charges), _lib.ptr(lj_type), n, float(self.L[0]), _lib.ptr(bnd),
+            self.r_comm, _lib.ptr(b["ids"][0]), _lib.ptr(b["ids"][1]), _lib.ptr(b["ids"][2]), _lib.ptr(b["pos"]),
+            _lib.ptr(b["q"]), _lib.ptr(b["t"]), _lib.ptr(b["halo"]), _lib.ptr(counts), _device.stream()),
+            "dd_assign_local")
+        nh, nl, ns = (int(c) for c in counts[:3])
+        self.home_counts = counts[3:].copy()
+        home = b["ids"][0, :nh].clone()  # the layout outlives the next rebuild's buffers
+        halo = b["ids"][1, :nl].clone()
+        send_local = b["ids"][2, :ns].clone()
+        self.layout = DomainLayout(home=home, halo=halo, send=home.index_select(0, send_local), send_local=send_local)
+        m = nh + nl
+        return self.layout, b["pos"][:m], b["q"][:m], b["t"][:m], b["halo"][:m]
+
     def _assign_native(self, pos: torch.Tensor) -> DomainLayout:
         """assign() inside libnbx (flags + stable compaction, one host sync)."""
         from . import _device, _lib
@@ -583,6 +616,10 @@ class DomainForces:
             allt = [torch.zeros_like(t) for _ in range(self.dd.N)]
             dist.all_gather(allt, t, group=self.dd.group)
             self.dd.rebalance(torch.cat(allt).cpu().numpy())
+        if self.dd._native is not None and positions_global.is_cuda:
+            self._ensure_globals(positions_global.device)
+            lay, lpos, lq, lt, lhalo = self.dd.assign_local(positions_global.contiguous(), self.q_all, self.t_all)
+            return self._build_local(lay, lpos, lq, lt, lhalo)
         lay = self.dd.assign(positions_global)
         return self._build_local(lay, positions_global.index_select(0, lay.local_ids).contiguous())
 
@@ -593,21 +630,24 @@ class DomainForces:
         lay, local_pos = self.dd.migrate(home_ids, home_pos)
         return self._build_local(lay, local_pos.contiguous())
 
-    def _build_local(self, lay: DomainLayout, local_pos: torch.Tensor) -> DomainLayout:
-        from . import list_step
-
-        dev = local_pos.device
-        ids = lay.local_ids
-        self.ids = ids
+    def _ensure_globals(self, dev) -> None:
         if not hasattr(self, "q_all"):
             self.q_all = torch.as_tensor(np.array(self.system.charges), device=dev)
             self.t_all = torch.as_tensor(np.array(self.system.lj_type), device=dev)
+
+    def _build_local(self, lay: DomainLayout, local_pos: torch.Tensor, q=None, t=None, halo=None) -> DomainLayout:
+        from . import list_step
+
+        dev = local_pos.device
+        self._ensure_globals(dev)
         self.local_pos = local_pos
-        self.q = self.q_all.index_select(0, ids)
-        self.t = self.t_all.index_select(0, ids)
-        halo = torch.zeros(lay.n_local, dtype=torch.uint8, device=dev)
-        halo[lay.n_home:] = 1
-        self.halo = halo
+        if q is None:
+            ids = lay.local_ids
+            q = self.q_all.index_select(0, ids)
+            t = self.t_all.index_select(0, ids)
+            halo = torch.zeros(lay.n_local, dtype=torch.uint8, device=dev)
+            halo[lay.n_home:] = 1
+        self.q, self.t, self.halo = q, t, halo
         n = lay.n_local
         sys_local = _Domain(n, self.system.box)
         occ = self.occ
@@ -616,9 +656,12 @@ class DomainForces:
             occ = local_occupancy(occ, n, self.system.n, self.system.box.lengths, w, self.dd.r_comm)
         self.grid, self.plist = list_step(sys_local, self.m, occ, self.system.box, self.params.r_list,
                                           positions=self.local_pos, r_inner=self.r_inner, halo=self.halo)
-        self.f = torch.empty((n, 3), dtype=torch.float64, device=dev)
-        self.e = torch.zeros(2, dtype=torch.float64, device=dev)
-        self.bad = torch.empty(2, dtype=torch.int64, device=dev)
+        if getattr(self, "_fcap", -1) < n:  # grow-only force / energy buffers
+            self._fbuf = torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev)
+            self._fcap = n
+            self.e = torch.zeros(2, dtype=torch.float64, device=dev)
+            self.bad = torch.empty(2, dtype=torch.int64, device=dev)
+        self.f = self._fbuf[:n]
         return lay
 
     def forces(self, energy: bool = True):
