@@ -300,6 +300,8 @@ int nbx_dd_allgather_home(nbx_dd_t* dd, const int64_t* home_ids, const double* h
 int nbx_dd_p2p_alloc(nbx_dd_t* dd, int64_t capacity, uint8_t handle_out[64]);
 int nbx_dd_p2p_open(nbx_dd_t* dd, const uint8_t down_handle[64], const uint8_t up_handle[64]);
 int nbx_dd_p2p_error(nbx_dd_t* dd, int32_t* out);
+/* the same flag as of the last nbx_dd_assign (read by its sync; no sync) */
+int nbx_dd_p2p_error_seen(const nbx_dd_t* dd, int32_t* out);
 void nbx_dd_free(nbx_dd_t* dd);
 
 /* Exact FP64 scan of every admitted pair for a coincident in-range pair

@@ -32,7 +32,7 @@ EXPORTS = (
     "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
     "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
-    "nbx_dd_assign", "nbx_dd_assign_local", "nbx_dd_classify", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error",
+    "nbx_dd_assign", "nbx_dd_assign_local", "nbx_dd_classify", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error", "nbx_dd_p2p_error_seen",
     "nbx_pairlist_prune_inner", "nbx_list_force_pairs", "nbx_list_diagnostics", "nbx_list_exclude", "nbx_settle", "nbx_dd_force", "nbx_list_step",
 )
 
@@ -111,6 +111,7 @@ def load():
         "nbx_dd_p2p_alloc": (ctypes.c_int, [P, I64, P]),
         "nbx_dd_p2p_open": (ctypes.c_int, [P, P, P]),
         "nbx_dd_p2p_error": (ctypes.c_int, [P, P]),
+        "nbx_dd_p2p_error_seen": (ctypes.c_int, [P, P]),
         "nbx_list_diagnostics": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "nbx_list_exclude": (ctypes.c_int, [P, P, P, P, P, P, P]),
         "nbx_list_step": (ctypes.c_int, [P, ctypes.c_int64, P, ctypes.c_int32, ctypes.c_int64, ctypes.c_double,

@@ -29,6 +29,7 @@ struct nbx_dd {
   char* peer_up = nullptr;        // rank+1's region (halo forces go there)
   unsigned long long seq_pos = 0, seq_f = 0;
   unsigned int* err = nullptr;    // device: set when a wait timed out
+  unsigned int err_seen = 0;      // host copy of err[0] taken by nbx_dd_assign's sync
 };
 
 namespace nbx {
@@ -360,6 +361,12 @@ extern "C" int nbx_dd_p2p_error(nbx_dd_t* d, int32_t* out) {
   return NBX_OK;
 }
 
+extern "C" int nbx_dd_p2p_error_seen(const nbx_dd_t* d, int32_t* out) {
+  if (!d || !out) return NBX_ERR_PARAM;
+  *out = (int32_t)d->err_seen;
+  return NBX_OK;
+}
+
 extern "C" void nbx_dd_free(nbx_dd_t* d) {
   if (!d) return;
   if (d->peer_down) cudaIpcCloseMemHandle(d->peer_down);
@@ -503,6 +510,8 @@ extern "C" int nbx_dd_assign(nbx_dd_t* d, const double* pos, int64_t n, double L
     if ((e = select_flagged<void>(iota.p, fl.p, halo, cnt.p + 1, n, s))) goto fail;
   }
   if ((e = cudaMemcpyAsync(hc, cnt.p, sizeof(int32_t) * (3 + N), cudaMemcpyDeviceToHost, s))) goto fail;
+  if (d->err && (e = cudaMemcpyAsync(&d->err_seen, d->err, sizeof(unsigned int), cudaMemcpyDeviceToHost, s)))
+    goto fail;
   if ((e = cudaStreamSynchronize(s))) goto fail;
   if (n > 0 && hc[0] > 0) {
     // send_local: positions inside the home list whose particle is on the -x face

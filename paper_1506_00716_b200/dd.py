@@ -56,7 +56,7 @@ class DomainLayout:
 
     home: torch.Tensor        # global ids owned here
     halo: torch.Tensor        # global ids received from the +x neighbour
-    send: torch.Tensor        # global ids (subset of home) sent to the -x neighbour
+    send: torch.Tensor | None  # global ids (subset of home) sent to the -x neighbour (None: native fast path)
     send_local: torch.Tensor  # their indices in the local array [home; halo]
 
     @property
@@ -163,8 +163,9 @@ class SlabDecomposition:
             raise RuntimeError(f"rank {self.rank}: NVLink peer exchange timed out (a neighbour stalled for > 5 s); "
                                "forces since the last check are invalid")
 
-    def p2p_error(self) -> bool:
-        """True when a peer wait timed out (host sync)."""
+    def p2p_error(self, seen: bool = False) -> bool:
+        """True when a peer wait timed out (host sync).  ``seen``: the flag as
+        read by the last native assign's own sync (no extra sync)."""
         if not getattr(self, "p2p", False):
             return False
         import ctypes
@@ -172,7 +173,8 @@ class SlabDecomposition:
         from . import _lib
 
         out = ctypes.c_int32(0)
-        _lib.check(_lib.load().nbx_dd_p2p_error(self._native, ctypes.byref(out)), "dd_p2p_error")
+        fn = _lib.load().nbx_dd_p2p_error_seen if seen else _lib.load().nbx_dd_p2p_error
+        _lib.check(fn(self._native, ctypes.byref(out)), "dd_p2p_error")
         return out.value != 0
 
     def close(self) -> None:
@@ -325,12 +327,16 @@ class SlabDecomposition:
             self.r_comm, _lib.ptr(b["ids"][0]), _lib.ptr(b["ids"][1]), _lib.ptr(b["ids"][2]), _lib.ptr(b["pos"]),
             _lib.ptr(b["q"]), _lib.ptr(b["t"]), _lib.ptr(b["halo"]), _lib.ptr(counts), _device.stream()),
             "dd_assign_local")
+        if self.p2p_error(seen=True):  # read by the assign's own sync
+            raise RuntimeError(f"rank {self.rank}: NVLink peer exchange timed out (a neighbour stalled for > 5 s); "
+                               "forces since the last check are invalid")
         nh, nl, ns = (int(c) for c in counts[:3])
         self.home_counts = counts[3:].copy()
-        home = b["ids"][0, :nh].clone()  # the layout outlives the next rebuild's buffers
-        halo = b["ids"][1, :nl].clone()
-        send_local = b["ids"][2, :ns].clone()
-        self.layout = DomainLayout(home=home, halo=halo, send=home.index_select(0, send_local), send_local=send_local)
+        # home ids outlive the buffers (callers keep them per step); halo and
+        # send_local are views until the next list step, send is not formed
+        # (the native exchanges use send_local)
+        home = b["ids"][0, :nh].clone()
+        self.layout = DomainLayout(home=home, halo=b["ids"][1, :nl], send=None, send_local=b["ids"][2, :ns])
         m = nh + nl
         return self.layout, b["pos"][:m], b["q"][:m], b["t"][:m], b["halo"][:m]
 
@@ -606,7 +612,9 @@ class DomainForces:
         """Re-decompose (optionally rebalancing the slabs from the ranks'
         measured force-pass times first: collective) and rebuild the local
         grid and list."""
-        self.dd.check_p2p()
+        native = self.dd._native is not None and positions_global.is_cuda
+        if not native:
+            self.dd.check_p2p()
         if balance and self.dd.N > 1 and getattr(self, "_ev", None) is not None:
             import torch.distributed as dist
 
@@ -616,7 +624,7 @@ class DomainForces:
             allt = [torch.zeros_like(t) for _ in range(self.dd.N)]
             dist.all_gather(allt, t, group=self.dd.group)
             self.dd.rebalance(torch.cat(allt).cpu().numpy())
-        if self.dd._native is not None and positions_global.is_cuda:
+        if native:  # the P2P timeout flag is checked by assign_local (no extra sync)
             self._ensure_globals(positions_global.device)
             lay, lpos, lq, lt, lhalo = self.dd.assign_local(positions_global.contiguous(), self.q_all, self.t_all)
             return self._build_local(lay, lpos, lq, lt, lhalo)
