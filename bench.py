@@ -224,8 +224,10 @@ class Clocks:
             return
         self._stop = threading.Event()
         self._sample()
-        self.th = threading.Thread(target=self._run, daemon=True)
-        self.th.start()
+        self.th = None
+        if os.environ.get("NBX_BENCH_CLOCK_THREAD", "1") != "0":  # 0: samples at start and stop only (A/B)
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
 
     @staticmethod
     def _handle(nv, torch, idx):
@@ -260,7 +262,8 @@ class Clocks:
         if self.h is None:
             return None
         self._stop.set()
-        self.th.join()
+        if self.th is not None:
+            self.th.join()
         self._sample()
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
@@ -694,7 +697,8 @@ def run_dd(args, world, rank, local):
     S0 = 10 * args.nstlist
     n_setup = 2 * args.nstlist if args.nstlist <= 50 else 2
     traj = Trajectory(system, static=args.positions == "static")
-    traj.to_device(dev, sorted(set(range(n_setup)) | set(range(S0 - W, S0 + args.steps))))
+    W2 = max(W, args.nstlist)  # the last warm-up covers a list step
+    traj.to_device(dev, sorted(set(range(n_setup)) | set(range(S0 - W2, S0 + args.steps))))
     dd = SlabDecomposition(box.lengths, world, rank, r_comm=R_LIST)
     if args.slabs == "count":  # equal particle counts per slab at step 0 (same on every rank)
         dd.balance_counts(traj.host(0)[:, 0])
@@ -739,15 +743,17 @@ def run_dd(args, world, rank, local):
     dist.all_reduce(adm)
     n_admitted = int(adm.item())
     n_force_rank = df.plist.force_pairs(inner=bool(args.rinner))  # this rank's kernel work
-    for k in range(S0 - W, S0):
-        step(k)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(local)
+    gc.collect()  # no interpreter GC pause inside the timed region (re-enabled below)
+    gc.disable()
+    # warm-up after the set-up above and over a whole list cycle: the first
+    # step after it (a list step) now and then stalled all ranks for 20-30 ms
+    for k in range(S0 - W2, S0):
+        step(k)
     lib.nbx_timing_query(None, None)
     lib.nbx_timing_enable(1)
     launches0 = lib.nbx_launch_count()
-    gc.collect()  # no interpreter GC pause inside the timed region (re-enabled below)
-    gc.disable()
     dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
