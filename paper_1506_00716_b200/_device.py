@@ -15,6 +15,8 @@ def require_cuda() -> torch.device:
     global _cuda_ok
     if _cuda_ok is None:
         _cuda_ok = torch.cuda.is_available()
+        if _cuda_ok:
+            torch.cuda.init()  # the raw current-device / stream lookups below need torch's CUDA state
     if not _cuda_ok:
         raise RuntimeError("the nbnxn path runs on a CUDA device (sm_100a); none is visible")
     return torch.device("cuda", torch._C._cuda_getDevice())
