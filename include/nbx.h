@@ -218,6 +218,11 @@ int nbx_force(const nbx_list_t* list, const nbx_grid_t* grid, const double* posi
  * reference operation order; bit-identical). */
 int nbx_max_displacement(const double* ref, const double* cur, int64_t n, const double box[3],
                          double* out_d2, void* stream);
+/* the same maximum in one launch (the drift guard of every MD / bench step):
+ * scratch = 16 B of device memory, zero before the first call and left zero
+ * by every call (one caller stream at a time); flags & 1: out = sqrt(max). */
+int nbx_max_displacement_ex(const double* ref, const double* cur, int64_t n, const double box[3],
+                            uint64_t* scratch, double* out, int32_t flags, void* stream);
 /* engine.velocity_verlet_step half steps (engine.py:556-579): v += f*(0.5 dt/m);
  * with move != 0 also x = wrap(x + v dt) (model.py:147-156).  Device arrays,
  * original order. */

@@ -29,7 +29,7 @@ EXPORTS = (
     "nbx_pairlist_build", "nbx_pairlist_prune", "nbx_list_info", "nbx_list_rows", "nbx_list_entries", "nbx_list_download",
     "nbx_super_layout", "nbx_super_download", "nbx_count_within", "nbx_list_free",
     "nbx_force", "nbx_find_singular", "nbx_launch_count", "nbx_timing_enable", "nbx_timing_query",
-    "nbx_max_displacement", "nbx_vv_update", "nbx_pairlist_build_ex",
+    "nbx_max_displacement", "nbx_max_displacement_ex", "nbx_vv_update", "nbx_pairlist_build_ex",
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
     "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
     "nbx_dd_assign", "nbx_dd_assign_local", "nbx_dd_classify", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error", "nbx_dd_p2p_error_seen",
@@ -96,6 +96,7 @@ def load():
         "nbx_timing_enable": (None, [I32]),
         "nbx_timing_query": (ctypes.c_int, [P, P]),
         "nbx_max_displacement": (ctypes.c_int, [P, P, I64, P, P, P]),
+        "nbx_max_displacement_ex": (ctypes.c_int, [P, P, I64, P, P, P, ctypes.c_int32, P]),
         "nbx_vv_update": (ctypes.c_int, [P, P, P, P, I64, D, I32, P, P]),
         "nbx_dd_unique_id": (ctypes.c_int, [P]),
         "nbx_dd_create": (ctypes.c_int, [P, I32, I32, PP]),

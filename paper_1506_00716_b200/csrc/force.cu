@@ -1347,7 +1347,8 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
 }
 
 __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __restrict__ e_out,
-                         const unsigned int* __restrict__ scalars, int64_t* __restrict__ bad) {
+                         const unsigned int* __restrict__ scalars, int64_t* __restrict__ bad,
+                         unsigned int* __restrict__ reset) {
   __shared__ double s[2][256];
   double a = 0.0, c = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += 256) {
@@ -1380,6 +1381,9 @@ __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __
         bad[1] = (int64_t)(key & 0xffffffffull);
       }
     }
+    // the next force call's k_init_scalars, done here (one launch fewer per call)
+    if (reset)
+      for (int i = 0; i < 7; ++i) reset[i] = (i == 2 || i == 3) ? 0xffffffffu : 0u;
   }
 }
 
@@ -1666,7 +1670,7 @@ struct ForceCall {
   const int32_t* sel0 = nullptr;
   double* e_grp0 = nullptr;
   bool canonical = false, sorted_j = false, ewald = false, band = false, use_krf = false;
-  int m = 0, flags = 0;
+  int m = 0, flags = 0, n_launched = 0;
   int64_t ns = 0, n_work = 0;
   const double* positions = nullptr;
   const double* charges = nullptr;
@@ -1817,8 +1821,8 @@ static int force_setup(ForceCall& C, const nbx_list_t* lc, const nbx_grid_t* gri
       wk.lj_key = key;
     }
     // scalars: [0] = 0 (max displacement), [1] = 0 (non-finite flag), [2..3] = ~0 (bad key)
-    count_launch();
-    k_init_scalars<<<1, 32, 0, s>>>(wk.scalars.p);
+    if (!wk.scalars_clean) count_launch(), k_init_scalars<<<1, 32, 0, s>>>(wk.scalars.p);
+    wk.scalars_clean = false;  // (re-set by this call's k_energy when it resets them)
     if (ns > 0)
       count_launch(), k_gather<<<nb(ns, 256), 256, 0, s>>>(positions, charges, lj_type, grid->perm.p, grid->fill.p,
                                            grid->cpos.p, grid->bbox.p, m, ns, bx, wk.xyzq.p, wk.type.p,
@@ -1943,7 +1947,9 @@ static cudaError_t force_launch(ForceCall& C, int64_t w0, int64_t w1) {
   }
   A.n_work = w1 - w0;
   A.e_grp = C.e_grp0 + 2 * w0;
-  cudaError_t e = cudaMemsetAsync(A.scalars + 4, 0, sizeof(unsigned int), C.s);
+  // the work counter is zero for a call's first launch (k_init_scalars or the
+  // previous call's k_energy reset it); later launches of the call reset it
+  cudaError_t e = C.n_launched++ ? cudaMemsetAsync(A.scalars + 4, 0, sizeof(unsigned int), C.s) : cudaSuccess;
   if (e) return e;
   return launch_force(C.m, !C.canonical, A, C.ewald ? FE_EWALD : FE_RF, C.use_krf,
                       (C.flags & NBX_FORCE_ENERGY) != 0, C.band, C.s);
@@ -1975,11 +1981,14 @@ static int force_finish(ForceCall& C, const double box[3], double* f_out, double
   if (!(C.flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
     // nothing else to produce
   } else {
+    // the rolling prune reads the scalars after this kernel: no reset then
+    unsigned int* reset = (C.flags & NBX_FORCE_REPRUNE) ? nullptr : wk.scalars.p;
     if (!(C.flags & NBX_FORCE_ENERGY)) {
-      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, 0, nullptr, wk.scalars.p, bad);
+      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, 0, nullptr, wk.scalars.p, bad, reset);
     } else {
-      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, C.n_work, e_out, wk.scalars.p, bad);
+      count_launch(), k_energy<<<1, 256, 0, s>>>(wk.e_grp.p, C.n_work, e_out, wk.scalars.p, bad, reset);
     }
+    wk.scalars_clean = reset != nullptr;
   }
   if ((e = cudaGetLastError())) goto cuda_fail;
   // rolling prune at this call's coordinates (after the pass that used the old masks)

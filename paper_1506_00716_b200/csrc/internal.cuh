@@ -100,6 +100,7 @@ struct ForceWork {
   DBuf<float4> part_j;    // (n_entries * m) or (n_rows * m) j-side partials
   DBuf<double> e_grp;     // (2 * n_work_groups) per-group energies
   DBuf<unsigned int> scalars;   // [0] max displacement bits, [1..2] bad key (u64)
+  bool scalars_clean = false;   // reset by the last call's k_energy (skip k_init_scalars)
   DBuf<float4> lj;        // (t*t) {6 c6, 12 c12, shift_lj, 0}
   std::vector<double> lj_key;  // host copy of what `lj` was built from (skip re-uploads)
   // transposed index: entries (or rows) sorted by j-cluster

@@ -33,6 +33,38 @@ __global__ void k_max_disp(const double* __restrict__ ref, const double* __restr
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(d2));
 }
 
+// one-launch variant: block maxima into scratch[0], the last block (ticket
+// in scratch[1]) writes the result -- sqrt'ed when asked -- and re-zeroes the
+// scratch for the next call (no memset, no separate sqrt kernel)
+__global__ void k_max_disp_once(const double* __restrict__ ref, const double* __restrict__ cur, int64_t n, Box box,
+                                unsigned long long* __restrict__ scratch, double* __restrict__ out, int take_sqrt) {
+  __shared__ double s_max[8];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (i < n) {
+    const double dx = min_image_np(__dsub_rn(cur[3 * i], ref[3 * i]), box.L[0], box.invL[0]);
+    const double dy = min_image_np(__dsub_rn(cur[3 * i + 1], ref[3 * i + 1]), box.L[1], box.invL[1]);
+    const double dz = min_image_np(__dsub_rn(cur[3 * i + 2], ref[3 * i + 2]), box.L[2], box.invL[2]);
+    d2 = d2_einsum(dx, dy, dz);
+  }
+  for (int o = 16; o; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = d2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = s_max[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, s_max[w]);
+    // d2 >= 0: the IEEE bit pattern is monotone as an unsigned integer
+    atomicMax(scratch, (unsigned long long)__double_as_longlong(b));
+    __threadfence();
+    const unsigned long long t = atomicAdd(scratch + 1, 1ull);
+    if (t == gridDim.x - 1) {  // every block's maximum is in
+      const double m = __longlong_as_double((long long)atomicExch(scratch, 0ull));
+      *out = take_sqrt ? sqrt(m) : m;
+      scratch[1] = 0ull;
+    }
+  }
+}
+
 __global__ void k_vv(double* __restrict__ x, double* __restrict__ v, const double* __restrict__ f,
                      const double* __restrict__ mass, int64_t n, double half_dt, double dt, int move, Box box) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -197,6 +229,37 @@ extern "C" int nbx_max_displacement(const double* ref, const double* cur, int64_
   }
   if (e) {
     set_error("nbx_max_displacement: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
+}
+
+extern "C" int nbx_max_displacement_ex(const double* ref, const double* cur, int64_t n, const double box[3],
+                                       uint64_t* scratch, double* out, int32_t flags, void* stream) {
+  if ((n > 0 && (!ref || !cur)) || !box || !out || !scratch) {
+    set_error("nbx_max_displacement_ex: null argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+    if (e) {
+      set_error("nbx_max_displacement_ex: %s", cudaGetErrorString(e));
+      return NBX_ERR_CUDA;
+    }
+    return NBX_OK;
+  }
+  Box bx;
+  for (int d = 0; d < 3; ++d) {
+    bx.L[d] = box[d];
+    bx.invL[d] = 1.0 / box[d];
+  }
+  count_launch();
+  k_max_disp_once<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ref, cur, n, bx,
+                                                              reinterpret_cast<unsigned long long*>(scratch), out,
+                                                              flags & 1);
+  if (cudaError_t e = cudaGetLastError()) {
+    set_error("nbx_max_displacement_ex: %s", cudaGetErrorString(e));
     return NBX_ERR_CUDA;
   }
   return NBX_OK;

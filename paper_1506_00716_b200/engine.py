@@ -94,13 +94,21 @@ class DriftTracker:
         object.__setattr__(self, "reference_positions", ref)
 
 
+_disp_scratch: dict = {}  # device index -> 16-byte zeroed scratch of nbx_max_displacement_ex
+
+
 def max_displacement_device(ref: torch.Tensor, cur: torch.Tensor, box: SimBox) -> torch.Tensor:
-    """Device scalar: max_i |minimum_image(cur_i - ref_i)| (no host sync)."""
+    """Device scalar: max_i |minimum_image(cur_i - ref_i)| (no host sync;
+    one kernel launch)."""
     out = torch.empty(1, dtype=torch.float64, device=cur.device)
+    scratch = _disp_scratch.get(cur.device.index)
+    if scratch is None:
+        scratch = _disp_scratch[cur.device.index] = torch.zeros(2, dtype=torch.int64, device=cur.device)
     L = _lib.box3(box.lengths)
-    _lib.check(_lib.load().nbx_max_displacement(_lib.ptr(ref), _lib.ptr(cur), int(cur.shape[0]), _lib.ptr(L),
-                                                _lib.ptr(out), dev.stream()), "max_displacement")
-    return out.sqrt()
+    _lib.check(_lib.load().nbx_max_displacement_ex(_lib.ptr(ref), _lib.ptr(cur), int(cur.shape[0]), _lib.ptr(L),
+                                                   _lib.ptr(scratch), _lib.ptr(out), 1, dev.stream()),
+               "max_displacement")
+    return out
 
 
 def update_drift(tracker: DriftTracker, current_positions, box: SimBox) -> DriftTracker:
