@@ -1390,7 +1390,7 @@ __global__ void k_energy(const double* __restrict__ e_grp, int64_t n, double* __
 __global__ void k_init_scalars(unsigned int* scalars) {
   // [0] max displacement, [1] non-finite flag, [2..3] bad key, [4] work counter
   // [5] max displacement since the rolling prune
-  if (threadIdx.x < 6) scalars[threadIdx.x] = (threadIdx.x == 2 || threadIdx.x == 3) ? 0xffffffffu : 0u;
+  if (threadIdx.x < 7) scalars[threadIdx.x] = (threadIdx.x == 2 || threadIdx.x == 3) ? 0xffffffffu : 0u;
 }
 
 __global__ void k_build_lj(const double* __restrict__ tab, int nt, double rc2, int shift,
