@@ -132,6 +132,11 @@ def stage_in(a, dtype: torch.dtype, name: str) -> torch.Tensor:
     return d
 
 
+def scratch(name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
+    """Grow-only device buffer reused across calls under ``name``."""
+    return _buffer(_devbuf, "scratch:" + name, numel, dtype, pinned=False)
+
+
 def stage_out(t: torch.Tensor, name: str, copy: bool = True) -> np.ndarray:
     """CUDA tensor -> numpy through pinned memory (synchronises).  ``copy``
     False returns a view of the staging buffer, valid until the next

@@ -254,14 +254,18 @@ def compute_nonbonded_original(plist: ClusterPairList, grid: ClusterGrid, positi
     # host arrays move through pinned staging (read-only charges / types are
     # recognised and uploaded once); results come back in one synchronisation
     pos_t = dev.stage_in(positions, torch.float64, "positions")
-    f, e, bad = compute_nonbonded_device(plist, grid, pos_t, dev.stage_in(charges, torch.float64, "charges"),
-                                         dev.stage_in(lj_types, torch.int64, "lj_types"), params, box)
-    eb = torch.cat([e, bad.to(torch.float64)])
-    eb_h = dev.stage_out(eb, "energies")
-    f_h = dev.stage_out(f, "forces")  # a fresh array (ForcesEnergies freezes it in place)
-    bad_h = eb_h[2:].astype(np.int64)
+    # forces, energies and the singular-pair key in one device buffer: one
+    # read-back and one synchronisation
+    n = pos_shape[0]
+    buf = dev.scratch("nonbonded_out", 3 * n + 4, torch.float64)
+    f_d, e_d, bad_d = buf[:3 * n].view(n, 3), buf[3 * n:3 * n + 2], buf[3 * n + 2:].view(torch.int64)
+    compute_nonbonded_device(plist, grid, pos_t, dev.stage_in(charges, torch.float64, "charges"),
+                             dev.stage_in(lj_types, torch.int64, "lj_types"), params, box, out=f_d, e_out=e_d,
+                             bad=bad_d)
+    out = dev.stage_out(buf, "nonbonded_out")  # a fresh array (ForcesEnergies freezes the forces in place)
+    bad_h = out[3 * n + 2:].view(np.int64)
     _raise_if_singular(plist, grid, pos_t, bad_h, params, box)
-    return ForcesEnergies(forces=f_h, e_lj=float(eb_h[0]), e_coulomb=float(eb_h[1]))
+    return ForcesEnergies(forces=out[:3 * n].reshape(n, 3), e_lj=float(out[3 * n]), e_coulomb=float(out[3 * n + 1]))
 
 
 def flop_count(plist: ClusterPairList, grid: ClusterGrid, layout: KernelLayout, box: SimBox,
