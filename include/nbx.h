@@ -237,6 +237,14 @@ int nbx_vv_update(double* x, double* v, const double* f, const double* mass, int
  * that no bond length changes (x_old unused). */
 int nbx_settle(const double* x_old, double* x, double* v, int64_t n_mol, double m_o, double m_h, double d_oh,
                double d_hh, double dt, int32_t mode, const double box[3], void* stream);
+/* One velocity-Verlet half for rigid water (3 atoms per molecule, all atoms
+ * in molecules), fused with its constraint: phase 0 = half kick + drift +
+ * wrap (nbx_vv_update, move) + SETTLE against the pre-drift positions; phase
+ * 1 = half kick + RATTLE's velocity stage.  Bit-identical to the separate
+ * calls, one launch instead of two or three. */
+int nbx_vv_constrained(double* x, double* v, const double* f, const double* mass, int64_t n_mol, double m_o,
+                       double m_h, double d_oh, double d_hh, double dt, int32_t phase, const double box[3],
+                       void* stream);
 
 /* ---------------------------------------------------------------- domain decomposition
  * Halo exchange of the 1-D slab decomposition (paper_1506_00716_b200/dd.py,

@@ -101,12 +101,7 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) { retur
 
 // positions: x_old constrained (previous step), x drifted (unconstrained) ->
 // x constrained (wrapped), v += displacement / dt
-__global__ void k_settle(const double* __restrict__ x_old, double* __restrict__ x, double* __restrict__ v,
-                         int64_t n_mol, Settle P, Box box) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n_mol) return;
-  const double* A0 = x_old + 9 * k;
-  double* X = x + 9 * k;
+__device__ __forceinline__ void settle_mol(const double* A0, double* X, double* V, const Settle& P, const Box& box) {
   double b0[3], c0[3], B1[3], C1[3];
   mi3(A0 + 3, A0, box, b0);
   mi3(A0 + 6, A0, box, c0);
@@ -156,20 +151,23 @@ __global__ void k_settle(const double* __restrict__ x_old, double* __restrict__ 
     for (int d = 0; d < 3; ++d) {
       const double r = com[d] + loc[a][0] * ex[d] + loc[a][1] * ey[d] + loc[a][2] * n[d];
       const double disp = r - (a ? rel1[a][d] : 0.0);
-      v[9 * k + 3 * a + d] += disp * P.inv_dt;
+      V[3 * a + d] += disp * P.inv_dt;
       X[3 * a + d] = wrap_coord(X[3 * a + d] + disp, box.L[d]);
     }
   }
 }
 
+__global__ void k_settle(const double* __restrict__ x_old, double* __restrict__ x, double* __restrict__ v,
+                         int64_t n_mol, Settle P, Box box) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_mol) return;
+  settle_mol(x_old + 9 * k, x + 9 * k, v + 9 * k, P, box);
+}
+
 // RATTLE velocity stage: r_b . (v_j - v_i) = 0 for the bonds (O,H1), (O,H2),
 // (H1,H2); corrections v_i += l_b r_b / m_i, v_j -= l_b r_b / m_j with the
 // multipliers from the 3x3 system (Cramer's rule)
-__global__ void k_rattle_v(const double* __restrict__ x, double* __restrict__ v, int64_t n_mol, Settle P, Box box) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n_mol) return;
-  const double* X = x + 9 * k;
-  double* V = v + 9 * k;
+__device__ __forceinline__ void rattle_mol(const double* X, double* V, const Settle& P, const Box& box) {
   const int bi[3] = {0, 0, 1}, bj[3] = {1, 2, 2};
   const double m[3] = {P.mO, P.mH, P.mH};
   double r[3][3];
@@ -204,6 +202,40 @@ __global__ void k_rattle_v(const double* __restrict__ x, double* __restrict__ v,
       V[3 * bi[b] + d] += lam[b] / m[bi[b]] * r[b][d];
       V[3 * bj[b] + d] -= lam[b] / m[bj[b]] * r[b][d];
     }
+}
+
+__global__ void k_rattle_v(const double* __restrict__ x, double* __restrict__ v, int64_t n_mol, Settle P, Box box) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_mol) return;
+  rattle_mol(x + 9 * k, v + 9 * k, P, box);
+}
+
+// One rigid-water molecule per thread, the velocity-Verlet halves fused with
+// their constraint (k_vv's arithmetic, op for op, then k_settle / k_rattle_v):
+// phase 0 -- half kick, drift + wrap, SETTLE against the pre-drift positions
+// (kept in registers: no x_old copy); phase 1 -- half kick, RATTLE.
+__global__ void k_vv_constrained(double* __restrict__ x, double* __restrict__ v, const double* __restrict__ f,
+                                 const double* __restrict__ mass, int64_t n_mol, double half_dt, double dt,
+                                 int phase, Settle P, Box box) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_mol) return;
+  double* X = x + 9 * k;
+  double* V = v + 9 * k;
+  double A0[9];
+  for (int a = 0; a < 3; ++a) {
+    const int64_t i = 3 * k + a;
+    const double s = __ddiv_rn(half_dt, mass[i]);  // (0.5 dt) / m  (engine.py:558)
+    for (int d = 0; d < 3; ++d) {
+      const double vn = __dadd_rn(V[3 * a + d], __dmul_rn(f[3 * i + d], s));
+      V[3 * a + d] = vn;
+      if (phase == 0) {
+        A0[3 * a + d] = X[3 * a + d];
+        X[3 * a + d] = wrap_coord(__dadd_rn(X[3 * a + d], __dmul_rn(vn, dt)), box.L[d]);
+      }
+    }
+  }
+  if (phase == 0) settle_mol(A0, X, V, P, box);
+  else rattle_mol(X, V, P, box);
 }
 }  // namespace nbx
 
@@ -289,6 +321,46 @@ extern "C" int nbx_vv_update(double* x, double* v, const double* f, const double
   return NBX_OK;
 }
 
+static Settle make_settle(double m_o, double m_h, double d_oh, double d_hh, double dt, bool positions) {
+  Settle P;
+  P.mO = m_o;
+  P.mH = m_h;
+  P.wohh = m_o + 2.0 * m_h;
+  P.rc = 0.5 * d_hh;
+  const double h = sqrt(d_oh * d_oh - P.rc * P.rc);
+  P.ra = 2.0 * m_h * h / P.wohh;
+  P.rb = h - P.ra;
+  P.inv_dt = positions ? 1.0 / dt : 0.0;
+  return P;
+}
+
+extern "C" int nbx_vv_constrained(double* x, double* v, const double* f, const double* mass, int64_t n_mol,
+                                  double m_o, double m_h, double d_oh, double d_hh, double dt, int32_t phase,
+                                  const double box[3], void* stream) {
+  if ((n_mol > 0 && (!x || !v || !f || !mass)) || !box || !(m_o > 0.0) || !(m_h > 0.0) || !(d_hh > 0.0) ||
+      !(d_oh > 0.5 * d_hh) || !(dt > 0.0) || phase < 0 || phase > 1) {
+    set_error("nbx_vv_constrained: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  Box bx;
+  for (int d = 0; d < 3; ++d) {
+    bx.L[d] = box[d];
+    bx.invL[d] = 1.0 / box[d];
+  }
+  const Settle P = make_settle(m_o, m_h, d_oh, d_hh, dt, phase == 0);
+  if (n_mol > 0) {
+    count_launch();
+    k_vv_constrained<<<(unsigned)((n_mol + 127) / 128), 128, 0, s>>>(x, v, f, mass, n_mol, 0.5 * dt, dt, phase, P,
+                                                                     bx);
+  }
+  if (cudaError_t e = cudaGetLastError()) {
+    set_error("nbx_vv_constrained: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
+}
+
 extern "C" int nbx_settle(const double* x_old, double* x, double* v, int64_t n_mol, double m_o, double m_h,
                           double d_oh, double d_hh, double dt, int32_t mode, const double box[3], void* stream) {
   if ((n_mol > 0 && (!x || !v || (mode == 0 && !x_old))) || !box || !(m_o > 0.0) || !(m_h > 0.0) ||
@@ -302,15 +374,7 @@ extern "C" int nbx_settle(const double* x_old, double* x, double* v, int64_t n_m
     bx.L[d] = box[d];
     bx.invL[d] = 1.0 / box[d];
   }
-  Settle P;
-  P.mO = m_o;
-  P.mH = m_h;
-  P.wohh = m_o + 2.0 * m_h;
-  P.rc = 0.5 * d_hh;
-  const double h = sqrt(d_oh * d_oh - P.rc * P.rc);
-  P.ra = 2.0 * m_h * h / P.wohh;
-  P.rb = h - P.ra;
-  P.inv_dt = mode == 0 ? 1.0 / dt : 0.0;
+  const Settle P = make_settle(m_o, m_h, d_oh, d_hh, dt, mode == 0);
   if (n_mol > 0) {
     count_launch();
     if (mode == 0)

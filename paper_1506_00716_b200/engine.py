@@ -14,6 +14,7 @@ bit-identical across reruns *and* across worker counts.
 
 from __future__ import annotations
 
+import os
 import time
 from contextlib import contextmanager
 from dataclasses import dataclass, field, replace
@@ -178,6 +179,18 @@ class RigidWater:
 
     def dof(self, n: int) -> int:
         return max(6 * (n // 3) - 3, 1)
+
+
+def vv_constrained_device(x, v, f, m, water: RigidWater, m_o: float, m_h: float, dt: float, box: SimBox,
+                          phase: int) -> None:
+    """Rigid water: one velocity-Verlet half fused with its constraint
+    (phase 0: half kick + drift + SETTLE; phase 1: half kick + RATTLE),
+    nbx_vv_constrained -- bit-identical to vv_half_kick_device followed by
+    settle_device."""
+    L = _lib.box3(box.lengths)
+    _lib.check(_lib.load().nbx_vv_constrained(_lib.ptr(x), _lib.ptr(v), _lib.ptr(f), _lib.ptr(m), int(x.shape[0]) // 3,
+                                              float(m_o), float(m_h), float(water.d_oh), float(water.d_hh),
+                                              float(dt), int(phase), _lib.ptr(L), dev.stream()), "vv_constrained")
 
 
 def settle_device(x_old, x, v, water: RigidWater, m_o: float, m_h: float, dt: float, box: SimBox,
@@ -401,7 +414,10 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                            molecules=mol)
         x = dev.to_device(system.positions, torch.float64).clone()
         v = dev.to_device(system.velocities, torch.float64).clone()
-        x_old = torch.empty_like(x) if constraints is not None else None
+        # rigid water: each velocity-Verlet half fused with its constraint
+        # (bit-identical; NBX_MD_FUSED=0 runs the separate kernels)
+        fused = constraints is not None and os.environ.get("NBX_MD_FUSED", "1") != "0"
+        x_old = torch.empty_like(x) if constraints is not None and not fused else None
         if constraints is not None:  # start from velocities that keep the bonds rigid
             settle_device(None, x, v, constraints, m_o, m_h, dt, box, velocities_only=True)
         m = dev.to_device(system.masses, torch.float64)
@@ -447,11 +463,14 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
     for _ in range(n_steps):
         with timer.section("step"):
             with timer.section("integrate"):
-                if constraints is not None:
-                    x_old.copy_(x)
-                vv_half_kick_device(x, v, f, m, dt, box, move=True)
-                if constraints is not None:
-                    settle_device(x_old, x, v, constraints, m_o, m_h, dt, box)
+                if fused:  # half kick + drift + SETTLE in one kernel
+                    vv_constrained_device(x, v, f, m, constraints, m_o, m_h, dt, box, phase=0)
+                else:
+                    if constraints is not None:
+                        x_old.copy_(x)
+                    vv_half_kick_device(x, v, f, m, dt, box, move=True)
+                    if constraints is not None:
+                        settle_device(x_old, x, v, constraints, m_o, m_h, dt, box)
                 state.step += 1
             report = state.step % report_interval == 0 or state.step == n_steps
             with timer.section("lifecycle"):
@@ -500,9 +519,12 @@ def run_md(system: ParticleSystem, params: NonbondedParams, layout: KernelLayout
                 with timer.section("forces"):
                     force_pass(report)
             with timer.section("integrate"):
-                vv_half_kick_device(x, v, f, m, dt, box, move=False)
-                if constraints is not None:
-                    settle_device(None, x, v, constraints, m_o, m_h, dt, box, velocities_only=True)
+                if fused:  # half kick + RATTLE in one kernel
+                    vv_constrained_device(x, v, f, m, constraints, m_o, m_h, dt, box, phase=1)
+                else:
+                    vv_half_kick_device(x, v, f, m, dt, box, move=False)
+                    if constraints is not None:
+                        settle_device(None, x, v, constraints, m_o, m_h, dt, box, velocities_only=True)
             if report:
                 with timer.section("report"):
                     record()

@@ -113,3 +113,23 @@ def test_rigid_water_md_is_stable():
     assert np.abs(e - e[0]).max() < 0.02 * ke.mean(), (res.e_total, res.e_kinetic)
     t = res.temperature[2:]
     assert np.abs(t - t.mean()).max() < 0.05 * t.mean(), res.temperature
+
+
+def test_fused_constrained_integration_is_bit_identical(monkeypatch):
+    """nbx_vv_constrained (half kick + drift + SETTLE, half kick + RATTLE in
+    one kernel each) reproduces the separate kernels bit for bit."""
+    nbx, _, table, occ = _spc(3000)
+    from paper_1506_00716_b200.systems import spc_water
+
+    s, table = spc_water(3000, seed=7, temperature=300.0)
+    params = nbx.NonbondedParams(r_cut=1.0, r_list=1.1, lj_table=table, elec="reaction_field", epsilon_rf=0.0)
+    water = nbx.RigidWater()
+    runs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("NBX_MD_FUSED", fused)
+        runs.append(nbx.run_md(s, params, nbx.KernelLayout(4, 4), 0.002, 60, report_interval=10,
+                               target_occupancy=occ, constraints=water))
+    a, b = runs
+    assert np.array_equal(a.state.system.positions, b.state.system.positions)
+    assert np.array_equal(a.state.system.velocities, b.state.system.velocities)
+    assert np.array_equal(a.e_total, b.e_total)
