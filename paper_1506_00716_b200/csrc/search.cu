@@ -645,11 +645,16 @@ __device__ __forceinline__ float prune_r2(const float4& xi, const float4& xj, co
 // and conservative (hi_in = r_inner^2 (1 + 1e-4), no FP64 replay): a member
 // left out has no pair within r_inner.
 template <int M, int G, int W, bool MI>
-__device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, const uint32_t (&wd)[2 * W],
+__device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, const float4* __restrict__ s_xp,
+                                            const float2* __restrict__ s_zp, const uint32_t (&wd)[2 * W],
                                             const float4& xj, float lo, float hi, float hi_in, const float (&Lf)[3],
                                             const float (&iLf)[3], uint32_t& inbits, uint32_t& ibits, uint32_t& amb) {
   constexpr int MM = M * M;
   const float inf = __int_as_float(0x7f800000);
+  // packed FP32 over i-atom pairs (no per-pair minimum image): the same
+  // IEEE operations per element as prune_r2, so the same values
+  constexpr bool PACKED = !MI && (M % 2 == 0);
+  const float2 nx = make_float2(-xj.x, -xj.x), ny = make_float2(-xj.y, -xj.y), nz = make_float2(-xj.z, -xj.z);
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int p0 = W == 2 ? k * 64 : k * MM;
@@ -658,10 +663,24 @@ __device__ __forceinline__ void prune_batch(const float4* __restrict__ s_xi, con
     for (int a = 0; a < M; ++a) cb |= (wd[(p0 + a * M) >> 5] >> ((p0 + a * M) & 31)) & 1u ? (1u << a) : 0u;
     if (!__any_sync(0xffffffffu, cb != 0u)) continue;
     float fmin = inf;
+    if constexpr (PACKED) {
 #pragma unroll
-    for (int a = 0; a < M; ++a) {
-      const float f = prune_r2<M, G, W, MI>(s_xi[k * M + a], xj, Lf, iLf);
-      fmin = fminf(fmin, ((cb >> a) & 1u) ? f : inf);
+      for (int a = 0; a < M; a += 2) {
+        const float4 xy = s_xp[(k * M + a) >> 1];
+        const float2 zz = s_zp[(k * M + a) >> 1];
+        const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nx);
+        const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), ny);
+        const float2 dz = __fadd2_rn(zz, nz);
+        const float2 f = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+        fmin = fminf(fmin, ((cb >> a) & 1u) ? f.x : inf);
+        fmin = fminf(fmin, ((cb >> (a + 1)) & 1u) ? f.y : inf);
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        const float f = prune_r2<M, G, W, MI>(s_xi[k * M + a], xj, Lf, iLf);
+        fmin = fminf(fmin, ((cb >> a) & 1u) ? f : inf);
+      }
     }
     if (fmin <= hi_in) ibits |= 1u << k;
     if (fmin < lo) {
@@ -694,6 +713,8 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
   constexpr int W = (G * M * M > 64) ? 2 : 1;
   constexpr int U = 2;  // batches in flight per warp
   __shared__ float4 s_xi[IA];
+  __shared__ float4 s_xp[(IA + 1) / 2];  // i-atom pairs {x_a, x_b, y_a, y_b} (packed FP32 path)
+  __shared__ float2 s_zp[(IA + 1) / 2];  // {z_a, z_b}
   __shared__ int32_t s_cnt[PRUNE_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane / M, b = lane % M;
@@ -716,6 +737,10 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
         v.z = (float)((bbox[6 * c + 2] - bbox[6 * (int64_t)first + 2]) + (double)v.z);
       }
       s_xi[ia] = v;
+      float* xp = reinterpret_cast<float*>(&s_xp[ia >> 1]);
+      xp[ia & 1] = v.x;
+      xp[2 + (ia & 1)] = v.y;
+      reinterpret_cast<float*>(&s_zp[ia >> 1])[ia & 1] = v.z;
     }
     __syncthreads();
     const int32_t e_beg = ent_off[g], e_end = ent_off[g + 1];
@@ -753,9 +778,9 @@ k_prune_entries(const int32_t* __restrict__ grp_first, const int32_t* __restrict
         if (!__any_sync(0xffffffffu, valid[u])) break;
         uint32_t inbits = 0, ibits = 0, amb = 0;
         if (!__any_sync(0xffffffffu, valid[u] && xj[u].w < slack_thr))
-          prune_batch<M, G, W, false>(s_xi, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
+          prune_batch<M, G, W, false>(s_xi, s_xp, s_zp, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
         else
-          prune_batch<M, G, W, true>(s_xi, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
+          prune_batch<M, G, W, true>(s_xi, s_xp, s_zp, wd[u], xj[u], lo, hi, hi_in, Lf, iLf, inbits, ibits, amb);
         while (amb) {  // rare: exact FP64 replay of the reference decision
           const int ia = __ffs(amb) - 1;
           amb &= amb - 1;
