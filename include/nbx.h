@@ -272,6 +272,13 @@ int nbx_dd_reduce_forces(nbx_dd_t* dd, double* local_f, void* stream);
 int nbx_dd_force(nbx_dd_t* dd, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
                  const double* charges, const int64_t* lj_type, const nbx_params_t* params, const double box[3],
                  int32_t flags, double* f_out, double* e_out, int64_t* bad, void* stream);
+/* The sequential peer-path force step (halo rows in, then the whole pass)
+ * with the halo forces sent as soon as the clusters holding halo particles
+ * are reduced (the rest of k_reduce overlaps their transfer); NCCL path:
+ * the three calls in sequence.  Same arguments and results as nbx_dd_force. */
+int nbx_dd_force_seq(nbx_dd_t* dd, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
+                     const double* charges, const int64_t* lj_type, const nbx_params_t* params, const double box[3],
+                     int32_t flags, double* f_out, double* e_out, int64_t* bad, void* stream);
 int nbx_dd_allreduce_sum(nbx_dd_t* dd, double* buf, int64_t n, void* stream);
 /* rebuild-time bookkeeping (dd.SlabDecomposition.assign): from global
  * positions (device n x 3) and host boundaries (N+1), the rank's home / halo

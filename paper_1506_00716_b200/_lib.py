@@ -33,7 +33,7 @@ EXPORTS = (
     "nbx_dd_unique_id", "nbx_dd_create", "nbx_dd_set_layout", "nbx_dd_exchange_positions",
     "nbx_dd_reduce_forces", "nbx_dd_allreduce_sum", "nbx_dd_free", "nbx_pairlist_build_pruned",
     "nbx_dd_assign", "nbx_dd_assign_local", "nbx_dd_classify", "nbx_dd_allgather_home", "nbx_dd_p2p_alloc", "nbx_dd_p2p_open", "nbx_dd_p2p_error", "nbx_dd_p2p_error_seen",
-    "nbx_pairlist_prune_inner", "nbx_list_force_pairs", "nbx_list_diagnostics", "nbx_list_exclude", "nbx_settle", "nbx_vv_constrained", "nbx_dd_force", "nbx_list_step",
+    "nbx_pairlist_prune_inner", "nbx_list_force_pairs", "nbx_list_diagnostics", "nbx_list_exclude", "nbx_settle", "nbx_vv_constrained", "nbx_dd_force", "nbx_dd_force_seq", "nbx_list_step",
 )
 
 
@@ -120,6 +120,7 @@ def load():
         "nbx_settle": (ctypes.c_int, [P, P, P, I64, D, D, D, D, D, I32, P, P]),
         "nbx_vv_constrained": (ctypes.c_int, [P, P, P, P, I64, D, D, D, D, D, ctypes.c_int32, P, P]),
         "nbx_dd_force": (ctypes.c_int, [P, P, P, P, P, P, ctypes.POINTER(NbxParams), P, I32, P, P, P, P]),
+        "nbx_dd_force_seq": (ctypes.c_int, [P, P, P, P, P, P, ctypes.POINTER(NbxParams), P, I32, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

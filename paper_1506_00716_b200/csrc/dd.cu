@@ -214,6 +214,26 @@ static void p2p_take_positions(nbx_dd* d, double* local_pos, cudaStream_t s) {
   k_p2p_take<<<p2p_blocks(d->n_halo), 256, 0, s>>>(flag, d->seq_pos, own, d->n_halo, nullptr, local_pos + 3 * d->n_home, 0, d->err);
 }
 
+// halo forces to the +x owner (peer stores + flag); face forces from the -x
+// neighbour added to the send rows (bounded wait on my flag)
+static void p2p_put_forces(nbx_dd* d, const double* local_f, cudaStream_t s) {
+  const unsigned long long seq = ++d->seq_f;
+  const int64_t cap = d->cap;
+  double* peer_f = reinterpret_cast<double*>(d->peer_up + 24 * cap);
+  unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_up + 48 * cap) + 1;
+  count_launch();
+  k_p2p_put<<<p2p_blocks(d->n_halo), 256, 0, s>>>(local_f + 3 * d->n_home, nullptr, d->n_halo, peer_f, peer_flag,
+                                                  seq, d->err + 2);
+}
+static void p2p_take_forces(nbx_dd* d, double* local_f, cudaStream_t s) {
+  const int64_t cap = d->cap;
+  const double* own = reinterpret_cast<const double*>(d->p2p_base + 24 * cap);
+  const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap) + 1;
+  count_launch();
+  k_p2p_take<<<p2p_blocks(d->n_send), 256, 0, s>>>(flag, d->seq_f, own, d->n_send, d->send_local.p, local_f, 1,
+                                                   d->err);
+}
+
 extern "C" int nbx_dd_exchange_positions(nbx_dd_t* d, double* local_pos, void* stream) {
   if (!d || !local_pos) {
     set_error("nbx_dd_exchange_positions: bad argument");
@@ -257,16 +277,8 @@ extern "C" int nbx_dd_reduce_forces(nbx_dd_t* d, double* local_f, void* stream) 
   if (d->nranks == 1) return NBX_OK;
   cudaStream_t s = to_stream(stream);
   if (d->p2p) {
-    const unsigned long long seq = ++d->seq_f;
-    const int64_t cap = d->cap;
-    double* peer_f = reinterpret_cast<double*>(d->peer_up + 24 * cap);
-    unsigned long long* peer_flag = reinterpret_cast<unsigned long long*>(d->peer_up + 48 * cap) + 1;
-    unsigned int* done = d->err + 2;
-    count_launch(2);
-    k_p2p_put<<<p2p_blocks(d->n_halo), 256, 0, s>>>(local_f + 3 * d->n_home, nullptr, d->n_halo, peer_f, peer_flag, seq, done);
-    const double* own = reinterpret_cast<const double*>(d->p2p_base + 24 * cap);
-    const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(d->p2p_base + 48 * cap) + 1;
-    k_p2p_take<<<p2p_blocks(d->n_send), 256, 0, s>>>(flag, seq, own, d->n_send, d->send_local.p, local_f, 1, d->err);
+    p2p_put_forces(d, local_f, s);
+    p2p_take_forces(d, local_f, s);
     cudaError_t e = cudaGetLastError();
     if (e) {
       set_error("nbx_dd_reduce_forces: %s", cudaGetErrorString(e));
@@ -645,6 +657,44 @@ fail:
 // coordinate run while the halo travels, the halo rows are taken, the
 // boundary work items run, and the halo forces go back / the face forces
 // come in (nbx_dd_reduce_forces).  NCCL path and one rank: sequential.
+// Sequential peer-path force step with the halo forces leaving early: halo
+// rows in, force pass, k_reduce over the clusters that hold halo particles,
+// their forces out to the +x owner, k_reduce over the rest, face forces in.
+// Results bit-identical to nbx_dd_exchange_positions + nbx_force +
+// nbx_dd_reduce_forces.
+extern "C" int nbx_dd_force_seq(nbx_dd_t* d, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
+                                const double* charges, const int64_t* lj_type, const nbx_params_t* params,
+                                const double box[3], int32_t flags, double* f_out, double* e_out, int64_t* bad,
+                                void* stream) {
+  if (!d || !list || !grid || !local_pos || !params || !box || !f_out || (flags & NBX_FORCE_CANONICAL)) {
+    set_error("nbx_dd_force_seq: bad argument");
+    return NBX_ERR_PARAM;
+  }
+  cudaStream_t s = to_stream(stream);
+  if (d->nranks == 1 || !d->p2p) {
+    int st = nbx_dd_exchange_positions(d, local_pos, stream);
+    if (!st) st = nbx_force(list, grid, local_pos, charges, lj_type, params, box, nullptr, 0, flags, f_out, e_out, bad,
+                            stream);
+    if (!st) st = nbx_dd_reduce_forces(d, f_out, stream);
+    return st;
+  }
+  p2p_put_positions(d, local_pos, s);
+  p2p_take_positions(d, local_pos, s);
+  const std::function<int()> put = [&]() {
+    p2p_put_forces(d, f_out, s);
+    return NBX_OK;
+  };
+  int st = force_split(list, grid, local_pos, charges, lj_type, params, box, flags, f_out, e_out, bad, stream,
+                       [] { return NBX_OK; }, &put, false);
+  if (st) return st;
+  p2p_take_forces(d, f_out, s);
+  if (cudaError_t e = cudaGetLastError()) {
+    set_error("nbx_dd_force_seq: %s", cudaGetErrorString(e));
+    return NBX_ERR_CUDA;
+  }
+  return NBX_OK;
+}
+
 extern "C" int nbx_dd_force(nbx_dd_t* d, const nbx_list_t* list, const nbx_grid_t* grid, double* local_pos,
                             const double* charges, const int64_t* lj_type, const nbx_params_t* params,
                             const double box[3], int32_t flags, double* f_out, double* e_out, int64_t* bad,

@@ -1256,8 +1256,9 @@ __global__ void k_reduce(const float4* __restrict__ part_i, const float4* __rest
                          const int32_t* __restrict__ perm, const uint8_t* __restrict__ fill,
                          int64_t n_clusters, int m, int flags, double* __restrict__ f_out,
                          unsigned int* __restrict__ flag, int split, float inner_dmax,
-                         const unsigned int* __restrict__ dref, int parts, int64_t ns) {
-  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+                         const unsigned int* __restrict__ dref, int parts, int64_t ns, int64_t c_off) {
+  // clusters [c_off, n_clusters) (n_clusters: the end of this launch's range)
+  const int64_t c = c_off + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= n_clusters) return;
   const int S = 32 / m;
@@ -1965,19 +1966,41 @@ static cudaError_t force_regather(ForceCall& C) {
   return cudaGetLastError();
 }
 
-static int force_finish(ForceCall& C, const double box[3], double* f_out, double* e_out, int64_t* bad) {
+static int force_finish(ForceCall& C, const double box[3], double* f_out, double* e_out, int64_t* bad,
+                        const std::function<int()>* mid = nullptr) {
   nbx_list* l = C.l;
   ForceWork& wk = l->work;
   cudaStream_t s = C.s;
   const ForceArgs& A = C.A;
   cudaError_t e;
-  if (C.ns > 0)
-    count_launch(), k_reduce<<<nb(l->n_clusters, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, C.canonical ? wk.tc_first.p : wk.t_first.p,
-                                         C.canonical ? wk.tc_items.p : (C.sorted_j ? nullptr : wk.t_items.p), C.grid->perm.p,
-                                         C.grid->fill.p, l->n_clusters, C.m, C.flags, f_out, wk.scalars.p + 1,
-                                         !C.canonical && wk.t_split,
-                                         (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
-                                         wk.scalars.p + A.inner_slot, C.canonical ? 1 : A.split, C.ns);
+  // clusters [c0, c1) of each k_reduce launch; with a `mid` hook (the DD
+  // force step) the halo clusters go first, then the hook (their forces
+  // leave), then the rest -- the same per-cluster sums, any order
+  auto reduce = [&](int64_t c0, int64_t c1) {
+    if (c1 <= c0) return;
+    count_launch();
+    k_reduce<<<nb(c1 - c0, 8), 256, 0, s>>>(wk.part_i.p, wk.part_j.p, C.canonical ? wk.tc_first.p : wk.t_first.p,
+                                            C.canonical ? wk.tc_items.p : (C.sorted_j ? nullptr : wk.t_items.p),
+                                            C.grid->perm.p, C.grid->fill.p, c1, C.m, C.flags, f_out,
+                                            wk.scalars.p + 1, !C.canonical && wk.t_split,
+                                            (A.ent_fmask && l->tail_sorted) ? A.inner_dmax : -1.f,
+                                            wk.scalars.p + A.inner_slot, C.canonical ? 1 : A.split, C.ns, c0);
+  };
+  if (C.ns > 0) {
+    const int64_t nc = l->n_clusters;
+    if (mid && l->halo_c1 > l->halo_c0) {
+      reduce(l->halo_c0, l->halo_c1);
+      if (int st = (*mid)()) return st;
+      reduce(0, l->halo_c0);
+      reduce(l->halo_c1, nc);
+    } else {
+      reduce(0, nc);
+      if (mid)
+        if (int st = (*mid)()) return st;
+    }
+  } else if (mid) {
+    if (int st = (*mid)()) return st;
+  }
   if (!(C.flags & NBX_FORCE_ENERGY) && e_out == nullptr && bad == nullptr) {
     // nothing else to produce
   } else {
@@ -2003,21 +2026,24 @@ cuda_fail:
 
 int force_split(const nbx_list_t* lc, const nbx_grid_t* grid, const double* positions, const double* charges,
                 const int64_t* lj_type, const nbx_params_t* p, const double box[3], int32_t flags, double* f_out,
-                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between) {
+                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between,
+                const std::function<int()>* after_halo, bool split_launch) {
   ForceCall C;
   int st = force_setup(C, lc, grid, positions, charges, lj_type, p, box, nullptr, 0, flags, f_out, stream);
   if (st) return st;
-  const int64_t n_int = C.canonical ? -1 : (C.l->n_interior < 0 ? -1 : C.l->n_interior * C.A.split);
+  const int64_t n_int =
+      C.canonical || !split_launch ? -1 : (C.l->n_interior < 0 ? -1 : C.l->n_interior * C.A.split);
   cudaError_t e;
   if (n_int < 0) {  // no interior / boundary split: one range, the caller's hook first
     if ((st = between())) return st;
-    if ((e = force_regather(C)) || (e = force_launch(C, 0, C.n_work))) goto fail;
-    return force_finish(C, box, f_out, e_out, bad);
+    // (split_launch false: the positions were final before force_setup's gather)
+    if ((split_launch && (e = force_regather(C))) || (e = force_launch(C, 0, C.n_work))) goto fail;
+    return force_finish(C, box, f_out, e_out, bad, after_halo);
   }
   if ((e = force_launch(C, 0, n_int))) goto fail;
   if ((st = between())) return st;
   if ((e = force_regather(C)) || (e = force_launch(C, n_int, C.n_work))) goto fail;
-  return force_finish(C, box, f_out, e_out, bad);
+  return force_finish(C, box, f_out, e_out, bad, after_halo);
 fail:
   set_error("nbx_force: %s", cudaGetErrorString(e));
   return NBX_ERR_CUDA;

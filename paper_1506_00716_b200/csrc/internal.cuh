@@ -171,6 +171,7 @@ struct List {
   // items (groups touching no halo particle, first in group_order; -1: none)
   DBuf<uint8_t> halo_cl;
   int64_t n_interior = -1;
+  int64_t halo_c0 = 0, halo_c1 = 0;  // domain lists: clusters [c0, c1) hold every halo particle
   int mask_words() const { return m == 8 ? 2 : 1; }
 };
 
@@ -195,7 +196,8 @@ cudaError_t reprune_inner(List* l, const float4* xyzq, const unsigned int* scala
 // work items of a domain list (force.cu; dd.cu runs the halo exchange there)
 int force_split(const nbx_list_t* l, const nbx_grid_t* grid, const double* positions, const double* charges,
                 const int64_t* lj_type, const nbx_params_t* p, const double box[3], int32_t flags, double* f_out,
-                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between);
+                double* e_out, int64_t* bad, void* stream, const std::function<int()>& between,
+                const std::function<int()>* after_halo = nullptr, bool split_launch = true);
 
 // exclusive scan helpers (CUB), defined in scan.cu
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);

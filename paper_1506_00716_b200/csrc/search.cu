@@ -1185,6 +1185,16 @@ __global__ void k_group_boundary(const int32_t* __restrict__ grp_first, const in
   }
 }
 
+// range of the clusters holding a halo particle (k_reduce does them first in
+// the DD force step so that the halo forces can leave early)
+__global__ void k_halo_range(const uint8_t* __restrict__ halo_cl, int64_t nc, unsigned int* __restrict__ range) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < nc && halo_cl[c]) {
+    atomicMin(range, (unsigned int)c);
+    atomicMax(range + 1, (unsigned int)c);
+  }
+}
+
 static cudaError_t order_groups(List* l, cudaStream_t s) {
   DBuf<int32_t> keys, keys2, vals;
   DBuf<unsigned int> nint;
@@ -1199,16 +1209,22 @@ static cudaError_t order_groups(List* l, cudaStream_t s) {
                                                      keys.p, vals.p);
   const bool split = l->halo_cl.p != nullptr;
   if (split) {
-    if ((e = nint.alloc(1, s)) || (e = cudaMemsetAsync(nint.p, 0, 4, s))) return e;
+    const unsigned int init[3] = {0u, 0xffffffffu, 0u};  // interior count, halo cluster min, max
+    if ((e = nint.alloc(3, s)) || (e = cudaMemcpyAsync(nint.p, init, 12, cudaMemcpyHostToDevice, s))) return e;
+    if (l->n_clusters > 0)
+      count_launch(), k_halo_range<<<nb(l->n_clusters, 256), 256, 0, s>>>(l->halo_cl.p, l->n_clusters, nint.p + 1);
     count_launch();
     k_group_boundary<<<nb(l->n_groups, 8), 256, 0, s>>>(l->group_first.p, l->group_nmem.p, l->n_groups,
                                                          l->ent_offsets.p, l->ent_j.p, l->halo_cl.p, keys.p, nint.p);
   }
   e = sort_pairs_i32(keys.p, keys2.p, vals.p, l->group_order.p, l->n_groups, split ? 17 : 16, s);
   if (!e && split) {
-    unsigned int h = 0;
-    if (!(e = cudaMemcpyAsync(&h, nint.p, 4, cudaMemcpyDeviceToHost, s)) && !(e = cudaStreamSynchronize(s)))
-      l->n_interior = h;
+    unsigned int h[3] = {0u, 0u, 0u};
+    if (!(e = cudaMemcpyAsync(h, nint.p, 12, cudaMemcpyDeviceToHost, s)) && !(e = cudaStreamSynchronize(s))) {
+      l->n_interior = h[0];
+      l->halo_c0 = h[1] <= h[2] ? (int64_t)h[1] : 0;
+      l->halo_c1 = h[1] <= h[2] ? (int64_t)h[2] + 1 : 0;
+    }
   }
   keys.release(s); keys2.release(s); vals.release(s); nint.release(s);
   return e;

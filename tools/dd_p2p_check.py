@@ -54,10 +54,14 @@ def run(tag):
 fn, en = run("nccl (sequential)")
 ok = dd.enable_p2p(s.n)
 df.overlap = False
-fs, es = run("p2p sequential " + str(ok))
+df.halo_first = False
+fs, es = run("p2p sequential, three calls " + str(ok))
+df.halo_first = True
+fh, eh = run("p2p sequential, halo forces first (nbx_dd_force_seq) " + str(ok))
 df.overlap = True
 fp, ep = run("p2p overlapped (nbx_dd_force) " + str(ok))
-same = torch.equal(fn, fp) and torch.equal(en, ep) and torch.equal(fn, fs) and torch.equal(en, es)
+same = (torch.equal(fn, fp) and torch.equal(en, ep) and torch.equal(fn, fs) and torch.equal(en, es)
+        and torch.equal(fn, fh) and torch.equal(en, eh))
 flag = torch.tensor([0 if same else 1], device=dev)
 dist.all_reduce(flag)
 err = dd.p2p_error()
